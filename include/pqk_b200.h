@@ -1,0 +1,170 @@
+/*
+ * pqk_b200.h — C-ABI of the B200-native PQk-means compressed-domain Lloyd iteration.
+ *
+ * This is the drop-in boundary for the hot path of the reference package
+ * `pqclust` (arXiv 1709.03708, /root/reference/pkg/src/pqclust).  The reference
+ * is pure Python; its only plugin interface for this path is the assignment
+ * strategy registry
+ *
+ *     AssignStrategy = Callable[[codes, centers, DistanceTables, threads], uint32 labels]
+ *       (clustering.py:200, register_assignment_strategy clustering.py:207-216)
+ *
+ * and the functions with no hook that must be replaced by same-signature
+ * functions: `fit` (clustering.py:377-482), `assign` (clustering.py:255-282),
+ * `paired_distance_sq` (pq.py:271-290) and `encode` (pq.py:205-231).
+ * Every entry point below takes plain pointers and sizes (no torch types) and
+ * returns a pqk_status_t; the Python host layer maps PQK_EINVAL to ValueError and
+ * everything else to RuntimeError, mirroring the reference error behaviour.
+ *
+ * Two levels:
+ *   1. Host-buffer entry points (pqk_*_host): the calls a ctypes/cffi binding of
+ *      the reference's strategy plugin makes.  Inputs and outputs are host memory
+ *      (pageable or pinned); the library manages device buffers and one stream per
+ *      device internally.  Synchronous on return.
+ *   2. Device-pointer entry points (pqk_*_device): stream-ordered kernel launches on
+ *      caller-owned device memory.  Used by the resident Lloyd engine (fit) and the
+ *      multi-GPU driver, which allreduces the histogram between
+ *      pqk_histogram_device and pqk_vote_device.
+ *
+ * Device code layout: codes and centers are row-major uint8 with a padded row
+ * stride MP = pqk_padded_m(M) (pad bytes are 0; pad subspaces use all-zero
+ * tables).  Tables are the reference's float64 (M, L, L) DistanceTables
+ * (pq.py:64-95), C-contiguous.
+ */
+#ifndef PQK_B200_H
+#define PQK_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PQK_ABI_VERSION 1
+
+typedef enum {
+  PQK_OK = 0,
+  PQK_EINVAL = 1,       /* bad argument: maps to ValueError            */
+  PQK_ECUDA = 2,        /* CUDA runtime / launch failure: RuntimeError */
+  PQK_ENOMEM = 3,       /* device allocation failed: MemoryError       */
+  PQK_EUNSUPPORTED = 4, /* shape outside what the kernels support       */
+} pqk_status_t;
+
+/* Stats slots written by the device entry points (int64 array of PQK_STATS_LEN). */
+enum {
+  PQK_STAT_UNIQUE_CENTERS = 0, /* distinct center codes after dedup                 */
+  PQK_STAT_FLAGGED = 1,        /* codes whose fp32 winner was not certified (fp64 rescan) */
+  PQK_STAT_NNZ_TOTAL = 2,      /* sum of histogram support sizes over filled (k,m)  */
+  PQK_STAT_EMPTY = 3,          /* empty clusters repaired                           */
+  PQK_STAT_FILLED = 4,         /* clusters with >=1 member                          */
+  PQK_STAT_VOTE_EXACT = 5,     /* (k,m) votes resolved by the double-double path    */
+  PQK_STAT_ENCODE_FLAGGED = 6, /* encoder (vector,m) pairs recomputed in fp64       */
+  PQK_STAT_NCHUNKS = 7,        /* center chunks streamed by the assignment scan     */
+  PQK_STATS_LEN = 16
+};
+
+/* ---- library / device info -------------------------------------------------- */
+int pqk_abi_version(void);
+const char* pqk_last_error(void); /* thread-local message of the last failure */
+int pqk_device_info(int32_t device, int32_t* sm_count, int32_t* smem_optin_bytes);
+int32_t pqk_padded_m(int32_t m); /* row stride of device code layout, 0 if unsupported */
+
+/* ---- host-side helpers (pure functions, no GPU) ------------------------------ */
+/* Power-of-two exponent e such that ldexp(T, e) is representable in fp32 normal
+ * range with headroom for M-term sums; *fp64_only = 1 when no such e exists
+ * (then the assignment runs the exact fp64 scan for every code). */
+int pqk_table_scale(const double* tables, int64_t count, int32_t* exp2_out, int32_t* fp64_only_out);
+
+/* numpy pairwise-summation tree (numpy/_core/src/umath/loops_utils.h.src,
+ * pairwise_sum, PW_BLOCKSIZE=128) used by np.mean in clustering.py:448-449.
+ * Plan sizes, then the plan itself: leaves (offset,length) left-to-right, and per
+ * depth d (0 = root) a node list (a,b): b<0 -> leaf a; else children a,b at d+1. */
+int pqk_pairwise_plan_size(int64_t n, int64_t* nleaves, int32_t* ndepth, int64_t* nnodes);
+int pqk_pairwise_plan_build(int64_t n, int64_t* leaf_off, int32_t* leaf_len,
+                            int64_t* depth_start /* ndepth+1 */, int32_t* node_a, int32_t* node_b);
+
+/* ---- device-pointer entry points (stream-ordered; stream is a cudaStream_t) -- */
+/* T32[mp][l][l] = fl32(ldexp(T64[m][l][l], exp2)), zeros for pad subspaces. */
+int pqk_tables_to_f32(const double* d_t64, int32_t m, int32_t l, int32_t exp2, float* d_t32, void* stream);
+
+/* Pad (n, m) codes to the (n, MP) device layout. */
+int pqk_pad_codes_device(const uint8_t* d_raw, int64_t n, int32_t m, uint8_t* d_padded, void* stream);
+
+/* Nearest-center assignment (replaces _assign_linear_scan clustering.py:167-197 and
+ * paired_distance_sq at clustering.py:447): labels[n] = argmin_k sum_m T[m][x_n^m][c_k^m]
+ * in float64 ascending-m order with lowest index on ties, and sd_sq[n] the float64
+ * distance to that center, bit-identical to the reference. */
+size_t pqk_assign_workspace_bytes(int64_t n, int64_t k, int32_t m, int32_t l);
+int pqk_assign_device(const uint8_t* d_codes, int64_t n, int32_t m, int32_t l,
+                      const uint8_t* d_centers, int64_t k,
+                      const double* d_t64, const float* d_t32, int32_t fp64_only,
+                      void* d_ws, size_t ws_bytes,
+                      uint32_t* d_labels, double* d_sd_sq, int64_t* d_stats, void* stream);
+
+/* sd[n] = sum_m T[m][a_n^m][b_{idx_n}^m] (float64, ascending m) — pq.py:271-290 with
+ * b = centers[labels] (clustering.py:447).  idx may be NULL (b row-aligned with a). */
+int pqk_paired_distance_device(const uint8_t* d_a, const uint8_t* d_b, const uint32_t* d_idx, int64_t n,
+                               int32_t m, int32_t l, const double* d_t64, double* d_out, void* stream);
+
+/* Histogram of member subindices (clustering.py:344-347) and counts (clustering.py:458):
+ * hist[k][m][s] (int32, zeroed here), counts[k] (int32, zeroed here). */
+int pqk_histogram_device(const uint8_t* d_codes, int64_t n, int32_t m, int32_t l,
+                         const uint32_t* d_labels, int64_t k, int32_t* d_hist, int32_t* d_counts, void* stream);
+
+/* Sparse-voting update (clustering.py:349-356): for filled k,
+ * new_centers[k][m] = argmin_j sum_s hist[k][m][s] * T[m][s][j] (lowest j on ties,
+ * exact-arithmetic argmin certified in fp64, double-double on near ties).  Empty
+ * clusters get code 0 (repaired by pqk_repair_device).  Writes NNZ_TOTAL, FILLED,
+ * EMPTY, VOTE_EXACT stats.  Requires hist/counts already reduced over all shards. */
+int pqk_vote_device(const int32_t* d_hist, const int32_t* d_counts, int64_t k, int32_t m, int32_t l,
+                    const double* d_t64, uint8_t* d_new_centers, int64_t* d_stats, void* stream);
+
+/* Empty-cluster repair (clustering.py:460-466): the E empty clusters (ascending k)
+ * take the codes of the E codes with largest sd_sq (lowest index among ties). */
+size_t pqk_repair_workspace_bytes(int64_t n, int64_t k);
+int pqk_repair_device(const double* d_sd_sq, const uint8_t* d_codes, int64_t n, int32_t m,
+                      const int32_t* d_counts, int64_t k, uint8_t* d_new_centers,
+                      void* d_ws, size_t ws_bytes, int64_t* d_stats, void* stream);
+/* Local top-E candidates for the multi-GPU repair: writes E (key,index) pairs
+ * sorted by (sd_sq desc, index asc); index offset by base_index. */
+int pqk_repair_candidates_device(const double* d_sd_sq, int64_t n, int64_t base_index, int64_t e,
+                                 void* d_ws, size_t ws_bytes, uint64_t* d_out_keys, int64_t* d_out_index,
+                                 void* stream);
+
+/* Objective sums (clustering.py:448-449): out[0] = pairwise_sum(sqrt(sd)), out[1] =
+ * pairwise_sum(sd) with numpy's exact tree (plan from pqk_pairwise_plan_build, uploaded). */
+size_t pqk_objective_workspace_bytes(int64_t nleaves, int64_t nnodes);
+int pqk_objective_device(const double* d_sd_sq, int64_t n, int64_t nleaves, int32_t ndepth,
+                         const int64_t* d_leaf_off, const int32_t* d_leaf_len,
+                         const int64_t* h_depth_start, const int32_t* d_node_a, const int32_t* d_node_b,
+                         void* d_ws, size_t ws_bytes, double* d_out2, void* stream);
+
+/* PQ encoder (pq.py:205-231): codes[n][m] = argmin_l sum_d (x - c_l)^2 in float64
+ * sequential order (scipy cdist), lowest l on ties.  vectors (n, d) fp32,
+ * codewords (m, l, d/m) fp32; code rows written with stride code_stride (pad bytes 0). */
+int pqk_encode_device(const float* d_vectors, int64_t n, int32_t d, const float* d_codewords,
+                      int32_t m, int32_t l, uint8_t* d_codes, int32_t code_stride,
+                      int64_t* d_stats, void* stream);
+
+/* ---- host-buffer entry points (the reference-facing plugin boundary) ---------- */
+/* AssignStrategy (clustering.py:200): labels (and optionally sd_sq) for host codes. */
+int pqk_assign_host(const uint8_t* codes, int64_t n, int32_t m, const uint8_t* centers, int64_t k,
+                    const double* tables, int32_t l, uint32_t* labels, double* sd_sq /* nullable */,
+                    int32_t device);
+/* encode (pq.py:205): vectors (n,d) fp32 host, codewords (m,l,d/m) fp32 host -> codes (n,m) */
+int pqk_encode_host(const float* vectors, int64_t n, int32_t d, const float* codewords, int32_t m,
+                    int32_t l, uint8_t* codes, int32_t device);
+/* One Lloyd iteration of fit (clustering.py:443-466) on host buffers: assign,
+ * objective sums, histogram, sparse vote, repair.  Outputs labels (n), new centers
+ * (k,m), obj2[2] = {sum sqrt(sd), sum sd} and stats (PQK_STATS_LEN). */
+int pqk_lloyd_step_host(const uint8_t* codes, int64_t n, int32_t m, const uint8_t* centers, int64_t k,
+                        const double* tables, int32_t l, uint32_t* labels, uint8_t* new_centers,
+                        double* obj2, int64_t* stats, int32_t device);
+/* Release the cached per-device context of the host entry points. */
+int pqk_host_release(int32_t device);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PQK_B200_H */

@@ -1,0 +1,635 @@
+// pqk_update.cu — histogram, sparse-voting update, empty-cluster repair and the
+// numpy-exact objective sums of one PQk-means Lloyd iteration on sm_100a.
+//
+//   histogram : clustering.py:344-347 (bincount(labels*L + codes[:,m])) and the
+//               counts of clustering.py:458, as integer atomics (order independent,
+//               bit exact).
+//   vote      : clustering.py:349-356.  votes_j = sum_s hist[s] * T[m][s][j] for the
+//               support s of each (filled k, m); center = argmin_j, lowest j on ties.
+//               Computed in fp64 (ascending s, FMA); the argmin is certified against
+//               the rounding error of any summation order (the reference uses an
+//               OpenBLAS dgemv whose order is kernel specific), and near ties are
+//               re-decided in double-double arithmetic (exact-arithmetic argmin).
+//   repair    : clustering.py:460-466.  The E empty clusters (ascending k) take the
+//               codes of the E largest sd_sq (lowest index first among equal
+//               values) — a radix select over the 96-bit key (sd_sq bits, ~index).
+//   objective : clustering.py:448-449, float(np.mean(np.sqrt(sd))) and
+//               float(np.mean(sd)), evaluated with numpy's pairwise-summation tree so
+//               the sums (and hence the exact-equality stop rule at :450) match.
+#include <algorithm>
+#include <cmath>
+
+#include "pqk_common.cuh"
+
+namespace pqk {
+
+
+// ---------------------------------------------------------------------------
+// histogram
+__global__ void histogram_kernel(const uint8_t* __restrict__ codes, int64_t n, int mp, int m, int l,
+                                 const uint32_t* __restrict__ labels, int32_t* __restrict__ hist,
+                                 int32_t* __restrict__ counts) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t k = labels[i];
+    const uint8_t* x = codes + i * mp;
+    atomicAdd(&counts[k], 1);
+    int32_t* hk = hist + k * m * l;
+    for (int mm = 0; mm < m; ++mm) atomicAdd(&hk[mm * l + x[mm]], 1);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// vote
+struct Best {
+  double v1;
+  int l1;
+  double v2;
+};
+
+__device__ __forceinline__ Best merge_best(const Best& a, const Best& b) {
+  Best r;
+  if (b.v1 < a.v1 || (b.v1 == a.v1 && b.l1 < a.l1)) {
+    r.v1 = b.v1;
+    r.l1 = b.l1;
+    r.v2 = fmin(a.v1, b.v2);
+  } else {
+    r.v1 = a.v1;
+    r.l1 = a.l1;
+    r.v2 = fmin(a.v2, b.v1);
+  }
+  return r;
+}
+
+__device__ __forceinline__ Best shfl_best(const Best& a, int off) {
+  Best b;
+  b.v1 = __shfl_xor_sync(0xffffffffu, a.v1, off);
+  b.l1 = __shfl_xor_sync(0xffffffffu, a.l1, off);
+  b.v2 = __shfl_xor_sync(0xffffffffu, a.v2, off);
+  return b;
+}
+
+struct DD {
+  double hi, lo;
+  int l;
+};
+
+__device__ __forceinline__ void two_sum(double a, double b, double& s, double& e) {
+  s = __dadd_rn(a, b);
+  const double bb = __dsub_rn(s, a);
+  e = __dadd_rn(__dsub_rn(a, __dsub_rn(s, bb)), __dsub_rn(b, bb));
+}
+
+// a < b in (value, index) order; values closer than 2^-100 relative count as equal.
+__device__ __forceinline__ bool dd_less(const DD& a, const DD& b) {
+  const double diff = __dadd_rn(__dsub_rn(a.hi, b.hi), __dsub_rn(a.lo, b.lo));
+  const double tol = ldexp(fmax(fabs(a.hi), fabs(b.hi)), -100);
+  if (diff < -tol) return true;
+  if (diff > tol) return false;
+  return a.l < b.l;
+}
+
+__global__ void __launch_bounds__(256) vote_kernel(const int32_t* __restrict__ hist, const int32_t* __restrict__ counts,
+                                                   int64_t k, int m, int l, int mp, const double* __restrict__ t64,
+                                                   uint8_t* __restrict__ newc, unsigned long long* __restrict__ acc) {
+  __shared__ int s_s[kMaxL];
+  __shared__ double s_h[kMaxL];
+  __shared__ int s_wc[8];
+  __shared__ Best s_best[8];
+  __shared__ DD s_dd[8];
+  __shared__ int s_nnz;
+  const int64_t km = blockIdx.x;
+  const int64_t kk = km / m;
+  const int mm = (int)(km - kk * m);
+  if (counts[kk] == 0) return;  // empty: left 0, repaired later
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int hv = (tid < l) ? hist[(kk * m + mm) * l + tid] : 0;
+  const unsigned bal = __ballot_sync(0xffffffffu, hv != 0);
+  if (lane == 0) s_wc[warp] = __popc(bal);
+  __syncthreads();
+  int off = 0, nnz = 0;
+#pragma unroll
+  for (int w = 0; w < 8; ++w) {
+    off += (w < warp) ? s_wc[w] : 0;
+    nnz += s_wc[w];
+  }
+  if (hv != 0) {
+    const int pos = off + __popc(bal & ((1u << lane) - 1u));
+    s_s[pos] = tid;
+    s_h[pos] = (double)hv;
+  }
+  if (tid == 0) {
+    s_nnz = nnz;
+    atomicAdd(&acc[0], (unsigned long long)nnz);
+  }
+  __syncthreads();
+  const double* tm = t64 + (size_t)mm * l * l;
+  double v = __longlong_as_double(0x7ff0000000000000LL);
+  if (tid < l) {
+    v = 0.0;
+    for (int j = 0; j < nnz; ++j) v = __fma_rn(s_h[j], __ldg(&tm[(size_t)s_s[j] * l + tid]), v);
+  }
+  Best b{v, tid, __longlong_as_double(0x7ff0000000000000LL)};
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) b = merge_best(b, shfl_best(b, o));
+  if (lane == 0) s_best[warp] = b;
+  __syncthreads();
+  if (warp == 0) {
+    b = s_best[lane & 7];
+#pragma unroll
+    for (int o = 4; o > 0; o >>= 1) b = merge_best(b, shfl_best(b, o));
+    if (lane == 0) s_best[0] = b;
+  }
+  __syncthreads();
+  b = s_best[0];
+  // Any summation order of nnz nonnegative products is within (nnz+1)u of the exact
+  // sum; a relative gap above 4(nnz+2)u proves the exact (and the reference's) argmin.
+  const double margin = 4.0 * (double)(nnz + 2) * ldexp(1.0, -53);
+  const bool cert = (b.v2 - b.v1) > margin * b.v2;
+  if (cert) {
+    if (tid == 0) newc[kk * mp + mm] = (uint8_t)b.l1;
+    return;
+  }
+  // near tie: double-double sums (exact products via FMA, compensated additions)
+  DD d{__longlong_as_double(0x7ff0000000000000LL), 0.0, tid};
+  if (tid < l) {
+    double hi = 0.0, lo = 0.0;
+    for (int j = 0; j < nnz; ++j) {
+      const double t = __ldg(&tm[(size_t)s_s[j] * l + tid]);
+      const double p = __dmul_rn(s_h[j], t);
+      const double pe = __fma_rn(s_h[j], t, -p);
+      double s, e;
+      two_sum(hi, p, s, e);
+      e = __dadd_rn(e, __dadd_rn(lo, pe));
+      hi = __dadd_rn(s, e);
+      lo = __dsub_rn(e, __dsub_rn(hi, s));
+    }
+    d.hi = hi;
+    d.lo = lo;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    DD od;
+    od.hi = __shfl_xor_sync(0xffffffffu, d.hi, o);
+    od.lo = __shfl_xor_sync(0xffffffffu, d.lo, o);
+    od.l = __shfl_xor_sync(0xffffffffu, d.l, o);
+    if (dd_less(od, d)) d = od;
+  }
+  if (lane == 0) s_dd[warp] = d;
+  __syncthreads();
+  if (tid == 0) {
+    DD w = s_dd[0];
+    for (int i = 1; i < 8; ++i)
+      if (dd_less(s_dd[i], w)) w = s_dd[i];
+    newc[kk * mp + mm] = (uint8_t)w.l;
+    atomicAdd(&acc[1], 1ull);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// order-preserving compaction of a flag array (two kernels; blockDim == 1024)
+__global__ void empty_count_kernel(const int32_t* __restrict__ counts, int64_t k, int32_t* __restrict__ blockcnt) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int f = (i < k) && counts[i] == 0;
+  const int c = __syncthreads_count(f);
+  if (threadIdx.x == 0) blockcnt[blockIdx.x] = c;
+}
+
+__global__ void empty_compact_kernel(const int32_t* __restrict__ counts, int64_t k,
+                                     const int32_t* __restrict__ blockcnt, int32_t* __restrict__ empty_list) {
+  __shared__ int s_off;
+  __shared__ int s_warp[32];
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (threadIdx.x == 0) {
+    int s = 0;
+    for (int b = 0; b < (int)blockIdx.x; ++b) s += blockcnt[b];
+    s_off = s;
+  }
+  const int f = (i < k) && counts[i] == 0;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned bal = __ballot_sync(0xffffffffu, f);
+  const int pre = __popc(bal & ((1u << lane) - 1u));
+  if (lane == 31) s_warp[warp] = pre + f;
+  __syncthreads();
+  if (warp == 0) {
+    const int v = s_warp[lane];
+    int x = v;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    s_warp[lane] = x - v;
+  }
+  __syncthreads();
+  if (f) empty_list[s_off + s_warp[warp] + pre] = (int32_t)i;
+}
+
+// number of empty clusters (acc[2]) and the public vote stats
+__global__ void empties_kernel(const int32_t* __restrict__ counts, int64_t k, unsigned long long* __restrict__ acc) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int c = __syncthreads_count((i < k) && counts[i] == 0);
+  if (threadIdx.x == 0 && c) atomicAdd(&acc[2], (unsigned long long)c);
+}
+
+__global__ void vote_stats_kernel(int64_t k, const unsigned long long* __restrict__ acc, int64_t* __restrict__ stats) {
+  stats[PQK_STAT_NNZ_TOTAL] = (int64_t)acc[0];
+  stats[PQK_STAT_VOTE_EXACT] = (int64_t)acc[1];
+  stats[PQK_STAT_EMPTY] = (int64_t)acc[2];
+  stats[PQK_STAT_FILLED] = k - (int64_t)acc[2];
+}
+
+// ---------------------------------------------------------------------------
+// repair: radix select of the top-E 96-bit keys (sd bits desc, index asc)
+struct SelState {
+  unsigned long long prefix_hi;
+  unsigned int prefix_lo;
+  unsigned int pad;
+  long long remaining;
+  unsigned long long count;
+};
+
+__device__ __forceinline__ void comp_key(const double* sd, int64_t i, int64_t base, uint64_t& hi, uint32_t& lo) {
+  hi = (uint64_t)__double_as_longlong(sd[i]);
+  lo = ~(uint32_t)(base + i);
+}
+
+// digit pass p (0..11): p<8 -> bits of hi from the top, else bits of lo from the top.
+__device__ __forceinline__ bool sel_match(uint64_t hi, uint32_t lo, int p, const SelState& st, int& digit) {
+  if (p < 8) {
+    const int sh = 56 - 8 * p;
+    const uint64_t mask_hi = (p == 0) ? 0ull : (~0ull << (sh + 8));
+    if ((hi & mask_hi) != (st.prefix_hi & mask_hi)) return false;
+    digit = (int)((hi >> sh) & 0xff);
+    return true;
+  }
+  if (hi != st.prefix_hi) return false;
+  const int q = p - 8;
+  const int sh = 24 - 8 * q;
+  const uint32_t mask_lo = (q == 0) ? 0u : (~0u << (sh + 8));
+  if ((lo & mask_lo) != (st.prefix_lo & mask_lo)) return false;
+  digit = (int)((lo >> sh) & 0xff);
+  return true;
+}
+
+__global__ void sel_hist_kernel(const double* __restrict__ sd, int64_t n, int64_t base, int p,
+                                const SelState* __restrict__ stp, unsigned int* __restrict__ ghist) {
+  __shared__ unsigned int h[256];
+  const SelState st = *stp;
+  if (st.remaining <= 0) return;
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) h[i] = 0;
+  __syncthreads();
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t hi;
+    uint32_t lo;
+    comp_key(sd, i, base, hi, lo);
+    int d;
+    if (sel_match(hi, lo, p, st, d)) atomicAdd(&h[d], 1u);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < 256; i += blockDim.x)
+    if (h[i]) atomicAdd(&ghist[i], h[i]);
+}
+
+__global__ void sel_choose_kernel(int p, SelState* stp, unsigned int* ghist) {
+  if (threadIdx.x == 0) {
+    SelState st = *stp;
+    if (st.remaining > 0) {
+      long long cum = 0;
+      int dstar = 0;
+      for (int d = 255; d >= 0; --d) {
+        const long long c = ghist[d];
+        if (cum + c >= st.remaining) {
+          dstar = d;
+          break;
+        }
+        cum += c;
+      }
+      st.remaining -= cum;
+      if (p < 8)
+        st.prefix_hi |= (unsigned long long)dstar << (56 - 8 * p);
+      else
+        st.prefix_lo |= (unsigned int)dstar << (24 - 8 * (p - 8));
+      *stp = st;
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) ghist[i] = 0;
+}
+
+__global__ void sel_init_kernel(SelState* st, unsigned int* ghist, const int64_t* __restrict__ e_src, int64_t e_const,
+                                int64_t n) {
+  if (threadIdx.x == 0) {
+    int64_t e = e_src ? e_src[PQK_STAT_EMPTY] : e_const;
+    if (e > n) e = n;
+    st->prefix_hi = 0;
+    st->prefix_lo = 0;
+    st->remaining = e;
+    st->count = 0;
+  }
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) ghist[i] = 0;
+}
+
+// after 12 passes the prefix is the E-th largest key exactly (keys are unique)
+__global__ void sel_collect_kernel(const double* __restrict__ sd, int64_t n, int64_t base, SelState* stp,
+                                   uint64_t* __restrict__ ck_hi, uint32_t* __restrict__ ck_lo,
+                                   const int64_t* __restrict__ e_src, int64_t e_const) {
+  const int64_t e = e_src ? e_src[PQK_STAT_EMPTY] : e_const;
+  if (e <= 0) return;
+  const uint64_t th = stp->prefix_hi;
+  const uint32_t tl = stp->prefix_lo;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t hi;
+    uint32_t lo;
+    comp_key(sd, i, base, hi, lo);
+    if (hi > th || (hi == th && lo >= tl)) {
+      const unsigned long long pos = atomicAdd(&stp->count, 1ull);
+      ck_hi[pos] = hi;
+      ck_lo[pos] = lo;
+    }
+  }
+}
+
+// rank sort of the (exactly E, unique) candidates, descending
+__global__ void sel_rank_kernel(const SelState* __restrict__ stp, const uint64_t* __restrict__ ck_hi,
+                                const uint32_t* __restrict__ ck_lo, uint64_t* __restrict__ out_hi,
+                                uint32_t* __restrict__ out_lo) {
+  const int64_t cnt = (int64_t)stp->count;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cnt; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t hi = ck_hi[i];
+    const uint32_t lo = ck_lo[i];
+    int64_t r = 0;
+    for (int64_t j = 0; j < cnt; ++j) {
+      const uint64_t h2 = ck_hi[j];
+      r += (h2 > hi) || (h2 == hi && ck_lo[j] > lo);
+    }
+    out_hi[r] = hi;
+    out_lo[r] = lo;
+  }
+}
+
+__global__ void repair_apply_kernel(const SelState* __restrict__ stp, const uint32_t* __restrict__ sorted_lo,
+                                    const int32_t* __restrict__ empty_list, const uint8_t* __restrict__ codes,
+                                    int mp, uint8_t* __restrict__ newc) {
+  const int64_t cnt = (int64_t)stp->count;
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < cnt; r += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t idx = (int64_t)(~sorted_lo[r]);
+    const int64_t kk = empty_list[r];
+    for (int j = 0; j < mp; ++j) newc[kk * mp + j] = codes[idx * mp + j];
+  }
+}
+
+__global__ void cand_out_kernel(const SelState* __restrict__ stp, const uint64_t* __restrict__ s_hi,
+                                const uint32_t* __restrict__ s_lo, uint64_t* __restrict__ out_keys,
+                                int64_t* __restrict__ out_index) {
+  const int64_t cnt = (int64_t)stp->count;
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < cnt; r += (int64_t)gridDim.x * blockDim.x) {
+    out_keys[r] = s_hi[r];
+    out_index[r] = (int64_t)(~s_lo[r]);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// numpy pairwise-sum objective
+__device__ __forceinline__ void leaf_pairwise(const double* __restrict__ a, int n, bool do_sqrt, double& res) {
+  auto val = [&](int i) { return do_sqrt ? __dsqrt_rn(a[i]) : a[i]; };
+  if (n < 8) {
+    double r = 0.0;
+    for (int i = 0; i < n; ++i) r = __dadd_rn(r, val(i));
+    res = r;
+    return;
+  }
+  double r[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) r[j] = val(j);
+  int i = 8;
+  for (; i < n - (n % 8); i += 8) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], val(i + j));
+  }
+  double s = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                       __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+  for (; i < n; ++i) s = __dadd_rn(s, val(i));
+  res = s;
+}
+
+__global__ void obj_leaf_kernel(const double* __restrict__ sd, int64_t nleaves, const int64_t* __restrict__ leaf_off,
+                                const int32_t* __restrict__ leaf_len, double2* __restrict__ leafval) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nleaves; t += (int64_t)gridDim.x * blockDim.x) {
+    const double* a = sd + leaf_off[t];
+    const int n = leaf_len[t];
+    double s1, s2;
+    leaf_pairwise(a, n, true, s1);
+    leaf_pairwise(a, n, false, s2);
+    leafval[t] = make_double2(s1, s2);
+  }
+}
+
+__global__ void obj_level_kernel(int64_t start, int64_t count, int64_t child_start, const int32_t* __restrict__ na,
+                                 const int32_t* __restrict__ nb, const double2* __restrict__ leafval,
+                                 double2* __restrict__ nodeval) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < count; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t id = start + t;
+    const int a = na[id], b = nb[id];
+    double2 r;
+    if (b < 0) {
+      r = leafval[a];
+    } else {
+      const double2 x = nodeval[child_start + a];
+      const double2 y = nodeval[child_start + b];
+      r = make_double2(__dadd_rn(x.x, y.x), __dadd_rn(x.y, y.y));
+    }
+    nodeval[id] = r;
+  }
+}
+
+__global__ void obj_out_kernel(const double2* __restrict__ nodeval, double* __restrict__ out2) {
+  out2[0] = nodeval[0].x;
+  out2[1] = nodeval[0].y;
+}
+
+// ---------------------------------------------------------------------------
+struct RepairWS {
+  SelState* st;
+  unsigned int* ghist;
+  unsigned long long* acc;
+  int32_t* blockcnt;
+  int32_t* empty_list;
+  uint64_t* ck_hi;
+  uint32_t* ck_lo;
+  uint64_t* s_hi;
+  uint32_t* s_lo;
+  size_t total;
+};
+
+static RepairWS repair_layout(void* base, int64_t n, int64_t k) {
+  RepairWS w{};
+  const int64_t cap = std::max<int64_t>(1, std::min(n, k));
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    off = align_up(off, 256);
+    const size_t o = off;
+    off += bytes;
+    return o;
+  };
+  const size_t o_st = take(sizeof(SelState));
+  const size_t o_gh = take(256 * sizeof(unsigned int));
+  const size_t o_acc = take(4 * sizeof(unsigned long long));
+  const size_t o_bc = take(((k + 1023) / 1024 + 1) * sizeof(int32_t));
+  const size_t o_el = take(std::max<int64_t>(k, 1) * sizeof(int32_t));
+  const size_t o_ch = take(cap * sizeof(uint64_t));
+  const size_t o_cl = take(cap * sizeof(uint32_t));
+  const size_t o_sh = take(cap * sizeof(uint64_t));
+  const size_t o_sl = take(cap * sizeof(uint32_t));
+  w.total = align_up(off, 256);
+  char* b = static_cast<char*>(base);
+  if (b) {
+    w.st = reinterpret_cast<SelState*>(b + o_st);
+    w.ghist = reinterpret_cast<unsigned int*>(b + o_gh);
+    w.acc = reinterpret_cast<unsigned long long*>(b + o_acc);
+    w.blockcnt = reinterpret_cast<int32_t*>(b + o_bc);
+    w.empty_list = reinterpret_cast<int32_t*>(b + o_el);
+    w.ck_hi = reinterpret_cast<uint64_t*>(b + o_ch);
+    w.ck_lo = reinterpret_cast<uint32_t*>(b + o_cl);
+    w.s_hi = reinterpret_cast<uint64_t*>(b + o_sh);
+    w.s_lo = reinterpret_cast<uint32_t*>(b + o_sl);
+  }
+  return w;
+}
+
+static int run_select(const double* d_sd, int64_t n, int64_t base, const int64_t* e_src, int64_t e_const,
+                      RepairWS& w, cudaStream_t stream) {
+  const DevInfo& di = dev_info();
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, (int64_t)di.sms * 4));
+  sel_init_kernel<<<1, 256, 0, stream>>>(w.st, w.ghist, e_src, e_const, n);
+  PQK_LAUNCH_CHECK("sel_init_kernel");
+  for (int p = 0; p < 12; ++p) {
+    sel_hist_kernel<<<grid, 256, 0, stream>>>(d_sd, n, base, p, w.st, w.ghist);
+    PQK_LAUNCH_CHECK("sel_hist_kernel");
+    sel_choose_kernel<<<1, 256, 0, stream>>>(p, w.st, w.ghist);
+    PQK_LAUNCH_CHECK("sel_choose_kernel");
+  }
+  sel_collect_kernel<<<grid, 256, 0, stream>>>(d_sd, n, base, w.st, w.ck_hi, w.ck_lo, e_src, e_const);
+  PQK_LAUNCH_CHECK("sel_collect_kernel");
+  sel_rank_kernel<<<di.sms * 2, 256, 0, stream>>>(w.st, w.ck_hi, w.ck_lo, w.s_hi, w.s_lo);
+  PQK_LAUNCH_CHECK("sel_rank_kernel");
+  return PQK_OK;
+}
+
+}  // namespace pqk
+
+using namespace pqk;
+
+extern "C" int pqk_histogram_device(const uint8_t* d_codes, int64_t n, int32_t m, int32_t l,
+                                    const uint32_t* d_labels, int64_t k, int32_t* d_hist, int32_t* d_counts,
+                                    void* stream_) {
+  cudaStream_t stream = (cudaStream_t)stream_;
+  const int mp = padded_m(m);
+  if (mp == 0 || l < 1 || l > kMaxL || k < 1 || n < 0) return fail(PQK_EINVAL, "pqk_histogram_device: bad arguments");
+  PQK_CUDA_TRY(cudaMemsetAsync(d_hist, 0, (size_t)k * m * l * sizeof(int32_t), stream));
+  PQK_CUDA_TRY(cudaMemsetAsync(d_counts, 0, (size_t)k * sizeof(int32_t), stream));
+  if (n == 0) return PQK_OK;
+  const DevInfo& di = dev_info();
+  const int grid = (int)std::min<int64_t>((n + 255) / 256, (int64_t)di.sms * 8);
+  histogram_kernel<<<grid, 256, 0, stream>>>(d_codes, n, mp, m, l, d_labels, d_hist, d_counts);
+  PQK_LAUNCH_CHECK("histogram_kernel");
+  return PQK_OK;
+}
+
+// d_stats has PQK_STATS_LEN slots: 0..7 public, 8..15 scratch accumulators of the vote.
+extern "C" int pqk_vote_device(const int32_t* d_hist, const int32_t* d_counts, int64_t k, int32_t m, int32_t l,
+                               const double* d_t64, uint8_t* d_new_centers, int64_t* d_stats, void* stream_) {
+  cudaStream_t stream = (cudaStream_t)stream_;
+  const int mp = padded_m(m);
+  if (mp == 0 || l < 2 || l > kMaxL || k < 1 || !d_stats) return fail(PQK_EINVAL, "pqk_vote_device: bad arguments");
+  if ((int64_t)k * m >= ((int64_t)1 << 31)) return fail(PQK_EUNSUPPORTED, "pqk_vote_device: k*m too large");
+  unsigned long long* acc = reinterpret_cast<unsigned long long*>(d_stats + 8);
+  PQK_CUDA_TRY(cudaMemsetAsync(acc, 0, 4 * sizeof(unsigned long long), stream));
+  PQK_CUDA_TRY(cudaMemsetAsync(d_new_centers, 0, (size_t)k * mp, stream));
+  vote_kernel<<<(unsigned)(k * m), 256, 0, stream>>>(d_hist, d_counts, k, m, l, mp, d_t64, d_new_centers, acc);
+  PQK_LAUNCH_CHECK("vote_kernel");
+  empties_kernel<<<(unsigned)((k + 1023) / 1024), 1024, 0, stream>>>(d_counts, k, acc);
+  PQK_LAUNCH_CHECK("empties_kernel");
+  vote_stats_kernel<<<1, 1, 0, stream>>>(k, acc, d_stats);
+  PQK_LAUNCH_CHECK("vote_stats_kernel");
+  return PQK_OK;
+}
+
+extern "C" size_t pqk_repair_workspace_bytes(int64_t n, int64_t k) {
+  if (n < 0 || k < 1) return 0;
+  return repair_layout(nullptr, n, k).total;
+}
+
+extern "C" int pqk_repair_device(const double* d_sd_sq, const uint8_t* d_codes, int64_t n, int32_t m,
+                                 const int32_t* d_counts, int64_t k, uint8_t* d_new_centers, void* d_ws,
+                                 size_t ws_bytes, int64_t* d_stats, void* stream_) {
+  cudaStream_t stream = (cudaStream_t)stream_;
+  const int mp = padded_m(m);
+  if (mp == 0 || k < 1 || n < 1 || !d_ws || !d_stats) return fail(PQK_EINVAL, "pqk_repair_device: bad arguments");
+  RepairWS w = repair_layout(d_ws, n, k);
+  if (ws_bytes < w.total) return fail(PQK_EINVAL, "pqk_repair_device: workspace too small");
+  const int kb = (int)((k + 1023) / 1024);
+  // empty clusters in ascending k; E itself is d_stats[PQK_STAT_EMPTY] from pqk_vote_device
+  empty_count_kernel<<<kb, 1024, 0, stream>>>(d_counts, k, w.blockcnt);
+  PQK_LAUNCH_CHECK("empty_count_kernel");
+  empty_compact_kernel<<<kb, 1024, 0, stream>>>(d_counts, k, w.blockcnt, w.empty_list);
+  PQK_LAUNCH_CHECK("empty_compact_kernel");
+  int rc = run_select(d_sd_sq, n, 0, d_stats, 0, w, stream);
+  if (rc != PQK_OK) return rc;
+  const DevInfo& di = dev_info();
+  repair_apply_kernel<<<di.sms, 256, 0, stream>>>(w.st, w.s_lo, w.empty_list, d_codes, mp, d_new_centers);
+  PQK_LAUNCH_CHECK("repair_apply_kernel");
+  return PQK_OK;
+}
+
+extern "C" int pqk_repair_candidates_device(const double* d_sd_sq, int64_t n, int64_t base_index, int64_t e,
+                                            void* d_ws, size_t ws_bytes, uint64_t* d_out_keys, int64_t* d_out_index,
+                                            void* stream_) {
+  cudaStream_t stream = (cudaStream_t)stream_;
+  if (n < 1 || e < 0 || !d_ws) return fail(PQK_EINVAL, "pqk_repair_candidates_device: bad arguments");
+  if (e == 0) return PQK_OK;
+  RepairWS w = repair_layout(d_ws, n, std::max<int64_t>(e, 1));
+  if (ws_bytes < w.total) return fail(PQK_EINVAL, "pqk_repair_candidates_device: workspace too small");
+  int rc = run_select(d_sd_sq, n, base_index, nullptr, std::min(e, n), w, stream);
+  if (rc != PQK_OK) return rc;
+  const DevInfo& di = dev_info();
+  cand_out_kernel<<<di.sms, 256, 0, stream>>>(w.st, w.s_hi, w.s_lo, d_out_keys, d_out_index);
+  PQK_LAUNCH_CHECK("cand_out_kernel");
+  return PQK_OK;
+}
+
+extern "C" size_t pqk_objective_workspace_bytes(int64_t nleaves, int64_t nnodes) {
+  return align_up((size_t)std::max<int64_t>(nleaves, 1) * sizeof(double2), 256) +
+         (size_t)std::max<int64_t>(nnodes, 1) * sizeof(double2);
+}
+
+extern "C" int pqk_objective_device(const double* d_sd_sq, int64_t n, int64_t nleaves, int32_t ndepth,
+                                    const int64_t* d_leaf_off, const int32_t* d_leaf_len,
+                                    const int64_t* h_depth_start, const int32_t* d_node_a,
+                                    const int32_t* d_node_b, void* d_ws, size_t ws_bytes, double* d_out2,
+                                    void* stream_) {
+  cudaStream_t stream = (cudaStream_t)stream_;
+  if (n < 1 || nleaves < 1 || ndepth < 1 || !h_depth_start || !d_ws)
+    return fail(PQK_EINVAL, "pqk_objective_device: bad arguments");
+  const int64_t nnodes = h_depth_start[ndepth];
+  if (ws_bytes < pqk_objective_workspace_bytes(nleaves, nnodes))
+    return fail(PQK_EINVAL, "pqk_objective_device: workspace too small");
+  double2* leafval = reinterpret_cast<double2*>(d_ws);
+  double2* nodeval = reinterpret_cast<double2*>(static_cast<char*>(d_ws) +
+                                                align_up((size_t)nleaves * sizeof(double2), 256));
+  const DevInfo& di = dev_info();
+  {
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((nleaves + 127) / 128, (int64_t)di.sms * 8));
+    obj_leaf_kernel<<<grid, 128, 0, stream>>>(d_sd_sq, nleaves, d_leaf_off, d_leaf_len, leafval);
+    PQK_LAUNCH_CHECK("obj_leaf_kernel");
+  }
+  for (int d = ndepth - 1; d >= 0; --d) {
+    const int64_t start = h_depth_start[d];
+    const int64_t count = h_depth_start[d + 1] - start;
+    const int64_t child = h_depth_start[d + 1];
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((count + 255) / 256, (int64_t)di.sms * 8));
+    obj_level_kernel<<<grid, 256, 0, stream>>>(start, count, child, d_node_a, d_node_b, leafval, nodeval);
+    PQK_LAUNCH_CHECK("obj_level_kernel");
+  }
+  obj_out_kernel<<<1, 1, 0, stream>>>(nodeval, d_out2);
+  PQK_LAUNCH_CHECK("obj_out_kernel");
+  return PQK_OK;
+}

@@ -1,0 +1,419 @@
+"""Device-resident state of the compressed-domain Lloyd iteration.
+
+PyTorch provides device memory, streams and (in :mod:`.distributed`) NCCL;
+every computation is a launch of the sm_100a C-ABI in ``libpqk_b200.so``.
+There is no CPU path: without CUDA these functions raise ``RuntimeError``.
+
+Data layout in HBM (one device, one shard of N codes):
+  codes    (N, MP) uint8   MP = padded M (pad subspaces are zero)
+  t64      (M, L, L) f64   reference DistanceTables, used for every exact result
+  t32      (MP, L, L) f32  ldexp-scaled copy, the assignment filter's source
+  labels   (N,) int32 (bit pattern of the reference's uint32 labels)
+  sd       (N,) f64        distance of each code to its center (clustering.py:447)
+  hist     (K, M, L) int32 member histograms (clustering.py:344-347)
+  counts   (K,) int32
+  centers  (K, MP) uint8 ×2 (current / next)
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import threading
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from ._lib import STATS_LEN, call
+
+try:
+    import torch
+except ImportError as exc:  # pragma: no cover - torch is part of the image
+    raise ImportError("paper_1709_03708_b200 needs PyTorch for device memory and streams") from exc
+
+
+def device_of(device: int | None = None) -> "torch.device":
+    if not torch.cuda.is_available():
+        raise RuntimeError(
+            "paper_1709_03708_b200 runs on a CUDA device (sm_100a); no GPU is visible and there is no CPU fallback"
+        )
+    _lib.load()
+    idx = torch.cuda.current_device() if device is None else int(device)
+    return torch.device("cuda", idx)
+
+
+def _ptr(t: "torch.Tensor | None") -> C.c_void_p:
+    return C.c_void_p(0 if t is None else t.data_ptr())
+
+
+def _stream(dev: "torch.device") -> C.c_void_p:
+    return C.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
+
+
+def _empty(n_bytes: int, dev) -> "torch.Tensor":
+    return torch.empty(max(int(n_bytes), 1), dtype=torch.uint8, device=dev)
+
+
+# ---------------------------------------------------------------------------
+# tables
+@dataclass
+class DeviceTables:
+    t64: "torch.Tensor"
+    t32: "torch.Tensor"
+    m: int
+    l: int
+    mp: int
+    fp64_only: int
+    exp2: int
+
+
+_TABLE_CACHE: dict = {}
+_TABLE_LOCK = threading.Lock()
+
+
+def device_tables(tables: np.ndarray, dev) -> DeviceTables:
+    """Upload (M, L, L) float64 tables and build the scaled fp32 filter copy (cached)."""
+    t = np.ascontiguousarray(tables, dtype=np.float64)
+    if t.flags.writeable:
+        key = (dev.index, t.shape, hash(t.tobytes()))
+        hold = None
+    else:
+        key = (dev.index, t.shape, id(t), t.ctypes.data)
+        hold = t
+    with _TABLE_LOCK:
+        hit = _TABLE_CACHE.get(key)
+        if hit is not None:
+            return hit[0]
+    m, l, _ = t.shape
+    lib = _lib.load()
+    e = C.c_int32(0)
+    f64 = C.c_int32(0)
+    _lib.check(lib.pqk_table_scale(t.ctypes.data_as(C.c_void_p), t.size, C.byref(e), C.byref(f64)), "pqk_table_scale")
+    mp = _lib.padded_m(m)
+    t64 = torch.from_numpy(t).to(dev)
+    t32 = torch.empty(mp * l * l, dtype=torch.float32, device=dev)
+    call("pqk_tables_to_f32", _ptr(t64), m, l, e.value, _ptr(t32), _stream(dev))
+    dt = DeviceTables(t64, t32, m, l, mp, int(f64.value), int(e.value))
+    with _TABLE_LOCK:
+        if len(_TABLE_CACHE) >= 8:
+            _TABLE_CACHE.pop(next(iter(_TABLE_CACHE)))
+        _TABLE_CACHE[key] = (dt, hold)
+    return dt
+
+
+def upload_codes(codes: np.ndarray, m: int, dev) -> "torch.Tensor":
+    """(N, M) integer host codes (already validated) -> (N, MP) uint8 device layout."""
+    mp = _lib.padded_m(m)
+    host = np.ascontiguousarray(codes, dtype=np.uint8)
+    n = host.shape[0]
+    if mp == m:
+        return torch.from_numpy(host).to(dev)
+    out = torch.empty((n, mp), dtype=torch.uint8, device=dev)
+    if n:
+        raw = torch.from_numpy(host).to(dev)
+        call("pqk_pad_codes_device", _ptr(raw), n, m, _ptr(out), _stream(dev))
+    return out
+
+
+def download_codes(codes_dev: "torch.Tensor", m: int) -> np.ndarray:
+    return np.ascontiguousarray(codes_dev[:, :m].cpu().numpy())
+
+
+# ---------------------------------------------------------------------------
+# numpy pairwise-sum plan (objective)
+@dataclass
+class PairwisePlan:
+    n: int
+    nleaves: int
+    ndepth: int
+    depth_start: np.ndarray  # host int64 (ndepth+1)
+    leaf_off: "torch.Tensor"
+    leaf_len: "torch.Tensor"
+    node_a: "torch.Tensor"
+    node_b: "torch.Tensor"
+    ws: "torch.Tensor"
+
+
+def host_plan(n: int) -> tuple[np.ndarray, np.ndarray, np.ndarray, np.ndarray, np.ndarray]:
+    """numpy's pairwise_sum tree for n elements (built by the C-ABI helper)."""
+    lib = _lib.load()
+    nl, nd, nn = C.c_int64(0), C.c_int32(0), C.c_int64(0)
+    _lib.check(lib.pqk_pairwise_plan_size(n, C.byref(nl), C.byref(nd), C.byref(nn)), "pqk_pairwise_plan_size")
+    leaf_off = np.empty(nl.value, np.int64)
+    leaf_len = np.empty(nl.value, np.int32)
+    depth_start = np.empty(nd.value + 1, np.int64)
+    na = np.empty(nn.value, np.int32)
+    nb = np.empty(nn.value, np.int32)
+    _lib.check(
+        lib.pqk_pairwise_plan_build(
+            n, *(x.ctypes.data_as(C.c_void_p) for x in (leaf_off, leaf_len, depth_start, na, nb))
+        ),
+        "pqk_pairwise_plan_build",
+    )
+    return leaf_off, leaf_len, depth_start, na, nb
+
+
+def pairwise_plan(n: int, dev) -> PairwisePlan:
+    leaf_off, leaf_len, depth_start, na, nb = host_plan(n)
+    ws_bytes = _lib.load().pqk_objective_workspace_bytes(len(leaf_off), len(na))
+    return PairwisePlan(
+        n,
+        len(leaf_off),
+        len(depth_start) - 1,
+        depth_start,
+        torch.from_numpy(leaf_off).to(dev),
+        torch.from_numpy(leaf_len).to(dev),
+        torch.from_numpy(na).to(dev),
+        torch.from_numpy(nb).to(dev),
+        _empty(ws_bytes, dev),
+    )
+
+
+def objective_sums(sd: "torch.Tensor", plan: PairwisePlan, out2: "torch.Tensor", dev) -> None:
+    """out2 <- (pairwise_sum(sqrt(sd)), pairwise_sum(sd)) exactly as numpy."""
+    call(
+        "pqk_objective_device",
+        _ptr(sd),
+        plan.n,
+        plan.nleaves,
+        plan.ndepth,
+        _ptr(plan.leaf_off),
+        _ptr(plan.leaf_len),
+        plan.depth_start.ctypes.data_as(C.c_void_p),
+        _ptr(plan.node_a),
+        _ptr(plan.node_b),
+        _ptr(plan.ws),
+        plan.ws.numel(),
+        _ptr(out2),
+        _stream(dev),
+    )
+
+
+def mean_from_sum(total: float, n: int) -> float:
+    """np.mean's final step: float64 sum divided by the count (true_divide)."""
+    return float(np.float64(total) / n)
+
+
+# ---------------------------------------------------------------------------
+class ShardEngine:
+    """One device's share of the Lloyd iteration (all N codes on a single GPU)."""
+
+    def __init__(self, codes_dev: "torch.Tensor", tables: DeviceTables, k: int, dev, base_index: int = 0):
+        self.dev = dev
+        self.tables = tables
+        self.codes = codes_dev
+        self.n = int(codes_dev.shape[0])
+        self.k = int(k)
+        self.base_index = int(base_index)
+        m, l, mp = tables.m, tables.l, tables.mp
+        lib = _lib.load()
+        self.labels = torch.empty(max(self.n, 1), dtype=torch.int32, device=dev)
+        self.sd = torch.empty(max(self.n, 1), dtype=torch.float64, device=dev)
+        self.ws_bytes = int(lib.pqk_assign_workspace_bytes(max(self.n, 1), self.k, m, l))
+        self.ws = _empty(self.ws_bytes, dev)
+        self.stats = torch.zeros(STATS_LEN, dtype=torch.int64, device=dev)
+        self.hist = torch.empty(self.k * m * l, dtype=torch.int32, device=dev)
+        self.counts = torch.empty(self.k, dtype=torch.int32, device=dev)
+        self.new_centers = torch.zeros((self.k, mp), dtype=torch.uint8, device=dev)
+        self.rws_bytes = int(lib.pqk_repair_workspace_bytes(max(self.n, 1), self.k))
+        self.rws = _empty(self.rws_bytes, dev)
+        self.obj = torch.zeros(2, dtype=torch.float64, device=dev)
+        self.plan = pairwise_plan(self.n, dev) if self.n else None
+
+    # -- stream-ordered launches ------------------------------------------------
+    def assign(self, centers_dev: "torch.Tensor") -> None:
+        t = self.tables
+        if self.n == 0:
+            return
+        call(
+            "pqk_assign_device",
+            _ptr(self.codes),
+            self.n,
+            t.m,
+            t.l,
+            _ptr(centers_dev),
+            int(centers_dev.shape[0]),
+            _ptr(t.t64),
+            _ptr(t.t32),
+            t.fp64_only,
+            _ptr(self.ws),
+            self.ws_bytes,
+            _ptr(self.labels),
+            _ptr(self.sd),
+            _ptr(self.stats),
+            _stream(self.dev),
+        )
+
+    def distances_for_labels(self, centers_dev: "torch.Tensor") -> None:
+        """sd <- paired distance of every code to centers[labels] (external strategies)."""
+        t = self.tables
+        call(
+            "pqk_paired_distance_device",
+            _ptr(self.codes),
+            _ptr(centers_dev),
+            _ptr(self.labels),
+            self.n,
+            t.m,
+            t.l,
+            _ptr(t.t64),
+            _ptr(self.sd),
+            _stream(self.dev),
+        )
+
+    def objective(self) -> None:
+        if self.n:
+            objective_sums(self.sd[: self.n], self.plan, self.obj, self.dev)
+
+    def histogram(self) -> None:
+        t = self.tables
+        call(
+            "pqk_histogram_device",
+            _ptr(self.codes),
+            self.n,
+            t.m,
+            t.l,
+            _ptr(self.labels),
+            self.k,
+            _ptr(self.hist),
+            _ptr(self.counts),
+            _stream(self.dev),
+        )
+
+    def vote(self) -> None:
+        t = self.tables
+        call(
+            "pqk_vote_device",
+            _ptr(self.hist),
+            _ptr(self.counts),
+            self.k,
+            t.m,
+            t.l,
+            _ptr(t.t64),
+            _ptr(self.new_centers),
+            _ptr(self.stats),
+            _stream(self.dev),
+        )
+
+    def repair(self) -> None:
+        call(
+            "pqk_repair_device",
+            _ptr(self.sd),
+            _ptr(self.codes),
+            self.n,
+            self.tables.m,
+            _ptr(self.counts),
+            self.k,
+            _ptr(self.new_centers),
+            _ptr(self.rws),
+            self.rws_bytes,
+            _ptr(self.stats),
+            _stream(self.dev),
+        )
+
+    def repair_candidates(self, e: int) -> tuple["torch.Tensor", "torch.Tensor"]:
+        """Local top-e (sd desc, global index asc) candidates: (uint64 keys, int64 global index)."""
+        keys = torch.empty(max(e, 1), dtype=torch.int64, device=self.dev)
+        index = torch.empty(max(e, 1), dtype=torch.int64, device=self.dev)
+        e_eff = min(e, self.n)
+        if e_eff > 0:
+            need = int(_lib.load().pqk_repair_workspace_bytes(self.n, max(e_eff, 1)))
+            ws = self.rws if need <= self.rws_bytes else _empty(need, self.dev)
+            call(
+                "pqk_repair_candidates_device",
+                _ptr(self.sd),
+                self.n,
+                self.base_index,
+                e_eff,
+                _ptr(ws),
+                ws.numel(),
+                _ptr(keys),
+                _ptr(index),
+                _stream(self.dev),
+            )
+        return keys[:e_eff], index[:e_eff]
+
+    # -- host reads ---------------------------------------------------------------
+    def stats_host(self) -> np.ndarray:
+        return self.stats.cpu().numpy()
+
+    def labels_host(self) -> np.ndarray:
+        return self.labels[: self.n].cpu().numpy().view(np.uint32)
+
+    def sd_host(self) -> np.ndarray:
+        return self.sd[: self.n].cpu().numpy()
+
+
+# ---------------------------------------------------------------------------
+# one-shot host helpers used by the public API
+def assign_host(codes: np.ndarray, centers: np.ndarray, tables: np.ndarray, *, device=None, want_sd=False):
+    dev = device_of(device)
+    dt = device_tables(tables, dev)
+    with torch.cuda.device(dev):
+        codes_dev = upload_codes(codes, dt.m, dev)
+        centers_dev = upload_codes(centers, dt.m, dev)
+        eng = ShardEngine(codes_dev, dt, len(centers), dev)
+        eng.assign(centers_dev)
+        labels = eng.labels_host()
+        sd = eng.sd_host() if want_sd else None
+    return (labels, sd) if want_sd else labels
+
+
+def paired_distance_host(tables: np.ndarray, a: np.ndarray, b: np.ndarray, *, device=None) -> np.ndarray:
+    dev = device_of(device)
+    dt = device_tables(tables, dev)
+    n = len(a)
+    if n == 0:
+        return np.zeros(0, dtype=np.float64)
+    with torch.cuda.device(dev):
+        a_dev = upload_codes(a, dt.m, dev)
+        b_dev = upload_codes(b, dt.m, dev)
+        out = torch.empty(n, dtype=torch.float64, device=dev)
+        call(
+            "pqk_paired_distance_device",
+            _ptr(a_dev),
+            _ptr(b_dev),
+            _ptr(None),
+            n,
+            dt.m,
+            dt.l,
+            _ptr(dt.t64),
+            _ptr(out),
+            _stream(dev),
+        )
+        return out.cpu().numpy()
+
+
+def mean_objectives(sd_dev: "torch.Tensor", n: int, dev) -> tuple[float, float]:
+    """(mean(sqrt(sd)), mean(sd)) with numpy's summation tree, on device."""
+    plan = pairwise_plan(n, dev)
+    out = torch.zeros(2, dtype=torch.float64, device=dev)
+    objective_sums(sd_dev, plan, out, dev)
+    s = out.cpu().numpy()
+    return mean_from_sum(s[0], n), mean_from_sum(s[1], n)
+
+
+def encode_host(codewords: np.ndarray, vectors: np.ndarray, *, device=None, stride: int | None = None):
+    """(N, D) float32 -> (N, M) uint8 codes on device; returns host codes."""
+    dev = device_of(device)
+    m, l, sub = codewords.shape
+    n, d = vectors.shape
+    with torch.cuda.device(dev):
+        out = encode_device(
+            torch.from_numpy(np.ascontiguousarray(vectors, dtype=np.float32)).to(dev),
+            torch.from_numpy(np.ascontiguousarray(codewords, dtype=np.float32)).to(dev),
+            m,
+            l,
+            dev,
+            stride=m,
+        )
+        return out.cpu().numpy()
+
+
+def encode_device(vec_dev, cw_dev, m: int, l: int, dev, stride: int | None = None, stats=None):
+    n, d = int(vec_dev.shape[0]), int(vec_dev.shape[1])
+    stride = m if stride is None else stride
+    out = torch.empty((n, stride), dtype=torch.uint8, device=dev)
+    st = stats if stats is not None else torch.zeros(STATS_LEN, dtype=torch.int64, device=dev)
+    if n:
+        call("pqk_encode_device", _ptr(vec_dev), n, d, _ptr(cw_dev), m, l, _ptr(out), stride, _ptr(st), _stream(dev))
+    return out

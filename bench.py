@@ -1,0 +1,428 @@
+#!/usr/bin/env python
+"""Benchmark of the B200-native PQk-means Lloyd iteration (BASELINE.json metric).
+
+Metric: code-center distance evaluations per second (N*K per Lloyd iteration /
+seconds per iteration), whole job over all ranks.  Workload at N=1:
+BASELINE.json configs[1] ("SIFT-like": N=1e6 128-D vectors, M=4, L=256,
+K=1e4), synthetic data of that shape (paper datasets absent).  One step = one
+full Lloyd iteration resident on the GPU: assignment scan (+ exact fp64
+certificate/rescan), objective sums, histogram, [NCCL allreduce], sparse vote,
+empty-cluster repair.  L2 (126 MB) is flushed by writing 512 MB between timed
+steps.  Weak scaling: every rank holds its own N codes (tree-aligned shards).
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+
+Rank 0 prints one JSON line.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+CONFIGS = {
+    # name: (n_per_gpu, k, m, l, dim)
+    "c2": dict(n=1_000_000, k=10_000, m=4, l=256, dim=128, workload="config2 SIFT-like N=1e6/GPU K=1e4 M=4 L=256"),
+    "c1": dict(n=100_000, k=1_000, m=4, l=256, dim=128, workload="config1 mixture N=1e5 K=1e3 M=4 L=256"),
+}
+SEED = 20260419
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+# ---------------------------------------------------------------------------
+# workload (host, seeded)
+def make_vectors(cfg_name: str, n: int, rank: int) -> np.ndarray:
+    from paper_1709_03708_b200 import synth
+
+    if cfg_name == "c1":
+        return synth.mixture(n, 128, 1000, synth.stage_seed(SEED, 100 + rank))
+    return synth.sift_like(n, synth.stage_seed(SEED, 100 + rank))
+
+
+def make_codebook(cfg_name: str, m: int, l_count: int) -> np.ndarray:
+    from paper_1709_03708_b200 import synth
+
+    if cfg_name == "c1":
+        sample = synth.mixture(20_000, 128, 1000, synth.stage_seed(SEED, 1))
+    else:
+        sample = synth.sift_like(100_000, synth.stage_seed(SEED, 1))
+    return synth.train_codebook_fast(sample, m, l_count, iterations=8, seed=synth.stage_seed(SEED, 2))
+
+
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}", "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+def cpu_baseline_sample(codes: np.ndarray, centers: np.ndarray, tables: np.ndarray, n_total: int,
+                        budget_s: float = 10.0) -> dict:
+    """Reference algorithm on host cores (oracle C port, all threads): bounded sample.
+
+    assignment: first n_s codes vs all K centers (C restatement of
+    clustering.py:167-197, every host thread); update: the sparse vote of the
+    sample's histograms (numpy restatement of clustering.py:327-356).  The
+    iteration time is extrapolated to the full N (assignment is O(N*K*M)).
+    """
+    from oracle import pqk_oracle as O
+
+    threads = os.cpu_count() or 1
+    k = len(centers)
+    n0 = min(len(codes), max(256, threads * 64))
+    t0 = time.perf_counter()
+    O.assign_c(codes[:n0], centers, tables, threads)
+    rate = n0 * k / max(time.perf_counter() - t0, 1e-6)
+    ns = int(min(len(codes), max(n0, rate * budget_s * 0.6 / k)))
+    t0 = time.perf_counter()
+    labels = O.assign_c(codes[:ns], centers, tables, threads)
+    t_assign = time.perf_counter() - t0
+    counts = np.bincount(labels.astype(np.intp), minlength=k)
+    t0 = time.perf_counter()
+    O.sparse_update_all(codes[:ns], labels, counts, tables)
+    t_update = time.perf_counter() - t0
+    t_iter = t_assign * (n_total / ns) + t_update
+    return {"value": n_total * k / t_iter, "unit": "evals/s", "cores": threads, "kind": "port",
+            "sample": f"assign {ns} of {n_total} codes x {k} centers ({t_assign:.2f}s, {threads} threads, C port of "
+                      f"clustering.py:167-197) + sparse update of the sample ({t_update:.2f}s, numpy port of "
+                      f"clustering.py:327-356); iteration extrapolated linearly in N",
+            "assign_evals_per_s": ns * k / t_assign, "s_per_iteration": t_iter}
+
+
+def run_reference(args) -> None:
+    """--impl reference: the reference algorithm (oracle port) on the box's host cores."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from oracle import pqk_oracle as O
+
+    cfgn = args.config
+    cfg = CONFIGS[cfgn]
+    book = make_codebook(cfgn, cfg["m"], cfg["l"])
+    tables = O.build_distance_tables(book)
+    vectors = make_vectors(cfgn, cfg["n"], 0)
+    rng = np.random.default_rng(SEED)
+    cidx = rng.choice(cfg["n"], size=cfg["k"], replace=False)
+    centers = O.encode(book, vectors[cidx])
+    codes = np.concatenate([O.encode(book, vectors[s : s + 10_000]) for s in range(0, min(cfg["n"], 50_000), 10_000)])
+    vals = []
+    for _ in range(args.warmup):
+        cpu_baseline_sample(codes, centers, tables, cfg["n"] * args.gpus, budget_s=2.0)
+    for _ in range(args.steps):
+        vals.append(cpu_baseline_sample(codes, centers, tables, cfg["n"] * args.gpus, budget_s=4.0))
+    v = float(np.median([x["value"] for x in vals]))
+    spi = float(np.median([x["s_per_iteration"] for x in vals]))
+    out = {
+        "metric": "code-center distance evals/s", "impl": "reference", "value": v, "unit": "evals/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": spi * 1e3,
+        "s_per_iteration": spi, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": {"workload": cfg["workload"], "n": cfg["n"] * args.gpus, "k": cfg["k"], "m": cfg["m"],
+                   "l": cfg["l"]},
+        "cpu_baseline": {"value": v, "unit": "evals/s", "cores": vals[-1]["cores"], "kind": "port",
+                         "sample": vals[-1]["sample"]},
+        "e2e": {"value": v, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out), flush=True)
+
+
+# ---------------------------------------------------------------------------
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "b200" else args.warmup
+    if args.impl == "reference":
+        run_reference(args)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_1709_03708_b200 import _lib, engine, synth
+    from paper_1709_03708_b200.distributed import DistributedLloyd, GpuShardBackend, shard_bounds
+    from paper_1709_03708_b200.pq import build_distance_tables, PQCodebook
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    lib = _lib.load()
+
+    cfgn = args.config
+    cfg = CONFIGS[cfgn]
+    n_loc, k, m, l_count = cfg["n"], cfg["k"], cfg["m"], cfg["l"]
+    n_total = n_loc * world
+
+    # ---- workload -----------------------------------------------------------------
+    t0 = time.perf_counter()
+    book = make_codebook(cfgn, m, l_count)
+    tables = build_distance_tables(PQCodebook(book)).tables
+    vectors = make_vectors(cfgn, n_loc, rank)
+    with torch.cuda.device(dev):
+        stats_enc = torch.zeros(_lib.STATS_LEN, dtype=torch.int64, device=dev)
+        vec_dev = torch.from_numpy(vectors).to(dev)
+        cw_dev = torch.from_numpy(book).to(dev)
+        codes_dev = engine.encode_device(vec_dev, cw_dev, m, l_count, dev, stride=_lib.padded_m(m), stats=stats_enc)
+        del vec_dev
+        codes_host = engine.download_codes(codes_dev, m)
+    log(f"[bench] rank {rank}: workload ready in {time.perf_counter() - t0:.1f}s")
+
+    offset, length = shard_bounds(n_total, world, rank)
+    assert length == n_loc, (length, n_loc)
+    backend = GpuShardBackend(codes_host, offset, tables, k, device=local)
+    drv = DistributedLloyd(backend, n_total, k, m) if world > 1 else None
+    if world > 1:
+        centers0 = drv.init_centers(SEED, codes_host)
+    else:
+        rng = np.random.default_rng(SEED)
+        centers0 = codes_host[rng.choice(n_loc, size=k, replace=False)].copy()
+    eng = backend.eng
+
+    def step_single(cur):
+        eng.assign(cur)
+        eng.objective()
+        eng.obj.cpu()  # host read of the objective (stop-rule check of fit)
+        eng.histogram()
+        eng.vote()
+        st = eng.stats_host()
+        if st[_lib.STAT_EMPTY]:
+            eng.repair()
+        return eng.new_centers.clone(), st
+
+    def step(cur):
+        if world == 1:
+            return step_single(cur)
+        st, nxt, _ = drv.iteration(cur, None)
+        return nxt, eng.stats_host()
+
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+    ev_scan0 = torch.cuda.Event(enable_timing=True)
+    ev_scan1 = torch.cuda.Event(enable_timing=True)
+    ev_scan0.record()
+    ev_scan1.record()
+    torch.cuda.synchronize(dev)
+    lib.pqk_set_profile_events(ev_scan0.cuda_event, ev_scan1.cuda_event)
+
+    with torch.cuda.device(dev):
+        cur = backend.upload_centers(centers0)
+        for _ in range(args.warmup):
+            cur, _ = step(cur)
+        torch.cuda.synchronize(dev)
+        step_ms, scan_ms, uniq, flagged = [], [], [], []
+        launches0 = lib.pqk_launch_count()
+        with ClockSampler(local) as clocks:
+            for _ in range(args.steps):
+                flush.fill_(1)
+                if world > 1:
+                    dist.barrier()
+                torch.cuda.synchronize(dev)
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record()
+                cur, st = step(cur)
+                e1.record()
+                torch.cuda.synchronize(dev)
+                step_ms.append(e0.elapsed_time(e1))
+                scan_ms.append(ev_scan0.elapsed_time(ev_scan1))
+                uniq.append(int(st[_lib.STAT_UNIQUE_CENTERS]))
+                flagged.append(int(st[_lib.STAT_FLAGGED]))
+        launches = lib.pqk_launch_count() - launches0
+    lib.pqk_set_profile_events(None, None)
+
+    total_ms = float(np.sum(step_ms))
+    if world > 1:
+        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    value = n_total * k / (ms_per_step / 1e3)
+
+    # roofline of the dominant kernel (assignment scan): shared-memory lookups
+    u = int(np.median(uniq))
+    lookup_bytes = n_loc * u * m * 4  # algorithmic: one 4-byte table lookup per (code, center, subspace)
+    scan_s = float(np.mean(scan_ms)) / 1e3
+    sm_count = torch.cuda.get_device_properties(dev).multi_processor_count
+    clk = clocks.summary()
+    peak_clock = 1965.0
+    peak = sm_count * 128 * peak_clock * 1e6 / 1e9  # GB/s: 128 B/clk/SM shared-memory bandwidth
+    achieved = lookup_bytes / scan_s / 1e9
+    traffic = None
+    prof = ROOT / "profiles" / "scan_traffic.json"
+    if prof.exists():
+        try:
+            traffic = json.loads(prof.read_text()).get(cfgn)
+        except Exception:
+            traffic = None
+
+    out = {
+        "metric": "code-center distance evals/s",
+        "value": value,
+        "unit": "evals/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms_per_step,
+        "s_per_iteration": ms_per_step / 1e3,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f32+f64",
+        "data": "synthetic",
+        "config": {"workload": cfg["workload"], "n": n_total, "k": k, "m": m, "l": l_count,
+                   "unique_centers": u, "flagged_codes_per_iter": int(np.median(flagged)),
+                   "l2": "flushed (512 MB write) between timed iterations",
+                   "step": "assign+certify+objective+histogram+allreduce+vote+repair",
+                   "parallelism": f"codes sharded dp{world}"},
+        "roofline": {"bound": "smem", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": traffic,
+                     "note": f"scan_kernel: {n_loc}x{u}x{m} 4-byte lookups per launch / {scan_s * 1e3:.3f} ms; peak = "
+                             f"{sm_count} SMs x 128 B/clk x {peak_clock:.0f} MHz (architectural, not in "
+                             "MEASURED_PEAKS.json)",
+                     "scan_ms": scan_s * 1e3, "scan_share_of_step": scan_s * 1e3 / ms_per_step},
+        "clocks": clk,
+        "gpu_launches": int(launches),
+    }
+
+    # ---- e2e through the C-ABI host entry (host buffers, H2D/D2H inside) ------------
+    if not args.no_e2e and world == 1:
+        import ctypes as C
+
+        pin_codes = torch.from_numpy(codes_host).pin_memory()
+        pin_cent = torch.from_numpy(centers0).pin_memory()
+        pin_tab = torch.from_numpy(np.ascontiguousarray(tables)).pin_memory()
+        pin_lab = torch.empty(n_loc, dtype=torch.int32).pin_memory()
+        pin_new = torch.empty((k, m), dtype=torch.uint8).pin_memory()
+        obj2 = np.zeros(2)
+        stats = np.zeros(_lib.STATS_LEN, np.int64)
+        p = lambda t: C.c_void_p(t.data_ptr())
+        pa = lambda a: a.ctypes.data_as(C.c_void_p)
+
+        def host_step():
+            _lib.check(lib.pqk_lloyd_step_host(p(pin_codes), n_loc, m, p(pin_cent), k, p(pin_tab), l_count,
+                                               p(pin_lab), p(pin_new), pa(obj2), pa(stats), local))
+            pin_cent.copy_(pin_new)
+
+        for _ in range(args.warmup):
+            host_step()
+        times = []
+        for _ in range(args.steps):
+            flush.fill_(1)
+            torch.cuda.synchronize(dev)
+            t0 = time.perf_counter()
+            host_step()
+            times.append(time.perf_counter() - t0)
+        e2e_s = float(np.mean(times))
+        h2d = codes_host.nbytes + centers0.nbytes + tables.nbytes
+        d2h = n_loc * 4 + k * m + 16 + _lib.STATS_LEN * 8
+        out["e2e"] = {"value": n_total * k / e2e_s, "unit": "evals/s", "h2d_bytes_per_step": int(h2d),
+                      "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_s * 1e3,
+                      "api": "pqk_lloyd_step_host (C-ABI, pinned host buffers)"}
+        lib.pqk_host_release(local)
+    elif not args.no_e2e:
+        # multi-GPU: host buffers through the sharded driver (H2D shard + centers, D2H labels + centers)
+        times = []
+        pin_codes = torch.from_numpy(codes_host).pin_memory()
+        for it in range(args.warmup + args.steps):
+            dist.barrier()
+            torch.cuda.synchronize(dev)
+            t0 = time.perf_counter()
+            eng.codes[:, :m].copy_(pin_codes.to(dev, non_blocking=True))
+            c = backend.upload_centers(centers0)
+            st, nxt, _ = drv.iteration(c, None)
+            lab = eng.labels_host()
+            _ = backend.centers_host(nxt)
+            torch.cuda.synchronize(dev)
+            dt = time.perf_counter() - t0
+            if it >= args.warmup:
+                times.append(dt)
+        t = torch.tensor([float(np.mean(times))], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+        out["e2e"] = {"value": n_total * k / e2e_s, "unit": "evals/s",
+                      "h2d_bytes_per_step": int(codes_host.nbytes + centers0.nbytes),
+                      "d2h_bytes_per_step": int(n_loc * 4 + k * m), "ms_per_step": e2e_s * 1e3,
+                      "api": "distributed.DistributedLloyd.iteration with host buffers"}
+
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline_sample(codes_host, centers0, tables, n_total)
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

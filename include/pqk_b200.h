@@ -69,6 +69,10 @@ int pqk_abi_version(void);
 const char* pqk_last_error(void); /* thread-local message of the last failure */
 int pqk_device_info(int32_t device, int32_t* sm_count, int32_t* smem_optin_bytes);
 int32_t pqk_padded_m(int32_t m); /* row stride of device code layout, 0 if unsupported */
+int64_t pqk_launch_count(void);  /* kernels launched by this library since load */
+/* Record the given cudaEvent_t handles (NULL to clear) immediately before and after
+ * every assignment-scan kernel launch (benchmark roofline timing). */
+int pqk_set_profile_events(void* before_scan, void* after_scan);
 
 /* ---- host-side helpers (pure functions, no GPU) ------------------------------ */
 /* Power-of-two exponent e such that ldexp(T, e) is representable in fp32 normal

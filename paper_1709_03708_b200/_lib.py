@@ -39,6 +39,8 @@ SIGNATURES: dict[str, tuple] = {
     "pqk_last_error": (C.c_char_p, []),
     "pqk_device_info": (C.c_int, [_i32, C.POINTER(_i32), C.POINTER(_i32)]),
     "pqk_padded_m": (_i32, [_i32]),
+    "pqk_launch_count": (_i64, []),
+    "pqk_set_profile_events": (C.c_int, [_p, _p]),
     "pqk_table_scale": (C.c_int, [_p, _i64, C.POINTER(_i32), C.POINTER(_i32)]),
     "pqk_pairwise_plan_size": (C.c_int, [_i64, C.POINTER(_i64), C.POINTER(_i32), C.POINTER(_i64)]),
     "pqk_pairwise_plan_build": (C.c_int, [_i64, _p, _p, _p, _p, _p]),

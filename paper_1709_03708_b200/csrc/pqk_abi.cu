@@ -1,6 +1,7 @@
 // pqk_abi.cu — C-ABI glue: error state, host-side helpers (table scale, numpy
 // pairwise-sum plan) and the host-buffer entry points that a binding of the
 // reference's AssignStrategy plugin (clustering.py:200-216) calls.
+#include <atomic>
 #include <cmath>
 #include <cstring>
 #include <mutex>
@@ -12,6 +13,11 @@
 namespace pqk {
 
 static thread_local std::string g_last_error;
+static std::atomic<long long> g_launches{0};
+static ProfileEvents g_prof;
+
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+ProfileEvents& profile_events() { return g_prof; }
 
 void set_error(const std::string& msg) { g_last_error = msg; }
 
@@ -139,6 +145,14 @@ using namespace pqk;
 extern "C" int pqk_abi_version(void) { return PQK_ABI_VERSION; }
 
 extern "C" const char* pqk_last_error(void) { return g_last_error.c_str(); }
+
+extern "C" int64_t pqk_launch_count(void) { return g_launches.load(); }
+
+extern "C" int pqk_set_profile_events(void* before_scan, void* after_scan) {
+  g_prof.before = (cudaEvent_t)before_scan;
+  g_prof.after = (cudaEvent_t)after_scan;
+  return PQK_OK;
+}
 
 extern "C" int pqk_device_info(int32_t device, int32_t* sm_count, int32_t* smem_optin_bytes) {
   int n = 0;

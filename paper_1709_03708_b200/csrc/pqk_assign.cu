@@ -556,8 +556,11 @@ static int launch_scan(const ScanParams& base_params, int l, cudaStream_t stream
   p.npasses = npasses;
   const int grid = (int)std::min<int64_t>(G, npasses);
   if (grid <= 0) return PQK_OK;
+  ProfileEvents& pe = profile_events();
+  if (pe.before) PQK_CUDA_TRY(cudaEventRecord(pe.before, stream));
   kern<<<grid, (NW + 1) * 32, smem, stream>>>(p);
   PQK_LAUNCH_CHECK("scan_kernel");
+  if (pe.after) PQK_CUDA_TRY(cudaEventRecord(pe.after, stream));
   return PQK_OK;
 }
 

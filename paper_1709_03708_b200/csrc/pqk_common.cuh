@@ -22,11 +22,21 @@ int cuda_fail(cudaError_t err, const char* what);
     if (_e != cudaSuccess) return ::pqk::cuda_fail(_e, #expr); \
   } while (0)
 
+// every kernel launch of the library is followed by exactly one PQK_LAUNCH_CHECK,
+// which also counts it (pqk_launch_count)
+void count_launch();
 #define PQK_LAUNCH_CHECK(what)                              \
   do {                                                      \
     cudaError_t _e = cudaGetLastError();                    \
     if (_e != cudaSuccess) return ::pqk::cuda_fail(_e, what); \
+    ::pqk::count_launch();                                  \
   } while (0)
+
+// optional events recorded around the assignment scan kernel (bench roofline)
+struct ProfileEvents {
+  cudaEvent_t before = nullptr, after = nullptr;
+};
+ProfileEvents& profile_events();
 
 constexpr int kMaxL = 256;
 

@@ -1,0 +1,248 @@
+"""Multi-GPU compressed-domain Lloyd iteration (one process per GPU).
+
+Codes are row-sharded along the top splits of numpy's pairwise-summation tree
+(:func:`pairwise.tree_split`), so each rank sums its objective subtree locally
+and the host combines G partials in tree order — bit-identical to the
+single-GPU / reference ``np.mean``.  Tables and centers are replicated; the
+vote is deterministic on identical reduced histograms, so centers need no
+broadcast.  Per iteration:
+
+1. assign on the local shard (no communication);
+2. allgather of 2 float64 objective partials;
+3. allreduce(sum) of the K x M x L int32 histograms and K counts — the one bulk
+   collective (NCCL over NVLink on GPUs, gloo in the CPU tests);
+4. replicated vote;
+5. if E clusters are empty: every rank proposes its local top-E (sd desc, global
+   index asc) codes, an allgather merges them and all ranks apply the same E.
+
+The loop is written against a small backend protocol so that the same host
+logic runs with the GPU :class:`GpuShardBackend` (product) and, in tests, with a
+CPU backend over gloo.
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass
+
+import numpy as np
+
+from .pairwise import tree_combine, tree_split
+
+try:
+    import torch
+    import torch.distributed as dist
+except ImportError as exc:  # pragma: no cover
+    raise ImportError("paper_1709_03708_b200.distributed needs torch.distributed") from exc
+
+
+@dataclass
+class StepStats:
+    objective: float
+    objective_sq: float
+    empty: int
+    filled: int
+    nnz_total: int
+    assign_seconds: float
+    update_seconds: float
+
+
+class GpuShardBackend:
+    """Backend over :class:`engine.ShardEngine` (sm_100a kernels)."""
+
+    def __init__(self, codes_local: np.ndarray, offset: int, tables: np.ndarray, k: int, device=None):
+        from . import engine
+
+        self.engine_mod = engine
+        self.dev = engine.device_of(device)
+        self.m = tables.shape[0]
+        self.dt = engine.device_tables(tables, self.dev)
+        with torch.cuda.device(self.dev):
+            codes_dev = engine.upload_codes(codes_local, self.m, self.dev)
+        self.eng = engine.ShardEngine(codes_dev, self.dt, k, self.dev, base_index=offset)
+        self.n = len(codes_local)
+        self.offset = offset
+
+    def upload_centers(self, centers: np.ndarray):
+        return self.engine_mod.upload_codes(centers, self.m, self.dev)
+
+    def assign(self, centers_dev) -> None:
+        self.eng.assign(centers_dev)
+
+    def sync(self) -> None:
+        torch.cuda.current_stream(self.dev).synchronize()
+
+    def objective_sums(self) -> np.ndarray:
+        if self.n == 0:
+            return np.zeros(2)
+        self.eng.objective()
+        return self.eng.obj.cpu().numpy()
+
+    def histogram(self):
+        self.eng.histogram()
+        return self.eng.hist, self.eng.counts
+
+    def vote(self) -> np.ndarray:
+        self.eng.vote()
+        return self.eng.stats_host()
+
+    def counts_host(self) -> np.ndarray:
+        return self.eng.counts.cpu().numpy()
+
+    def local_candidates(self, e: int):
+        keys, index = self.eng.repair_candidates(e)
+        local = (index - self.offset).clamp_(min=0)
+        rows = self.eng.codes[local][:, : self.m] if len(index) else torch.empty((0, self.m), dtype=torch.uint8)
+        return keys.cpu().numpy().view(np.uint64), index.cpu().numpy(), rows.cpu().numpy()
+
+    def apply_repair(self, empty: np.ndarray, rows: np.ndarray) -> None:
+        if len(empty):
+            idx = torch.from_numpy(empty.astype(np.int64)).to(self.dev)
+            val = self.engine_mod.upload_codes(rows, self.m, self.dev)
+            self.eng.new_centers[idx] = val
+
+    def take_new_centers(self):
+        return self.eng.new_centers.clone()
+
+    def centers_host(self, centers_dev) -> np.ndarray:
+        return self.engine_mod.download_codes(centers_dev, self.m)
+
+    def labels_host(self) -> np.ndarray:
+        return self.eng.labels_host()
+
+    def collective_device(self):
+        return self.dev
+
+
+def _allgather_obj(values, group) -> list:
+    out = [None] * dist.get_world_size(group)
+    dist.all_gather_object(out, values, group=group)
+    return out
+
+
+def merge_candidates(parts, e: int):
+    """Global top-e by (sd desc, index asc) from per-rank candidate lists."""
+    keys = np.concatenate([p[0] for p in parts]) if parts else np.zeros(0, np.uint64)
+    index = np.concatenate([p[1] for p in parts]) if parts else np.zeros(0, np.int64)
+    rows = np.concatenate([p[2] for p in parts]) if parts else np.zeros((0, 1), np.uint8)
+    order = np.lexsort((index, ~keys))[:e]  # primary: key desc (as ~key asc), then index asc
+    return keys[order], index[order], rows[order]
+
+
+class DistributedLloyd:
+    """Sharded PQk-means fit; every rank calls the same methods in lockstep."""
+
+    def __init__(self, backend, n_total: int, k: int, m: int, group=None):
+        self.b = backend
+        self.n_total = int(n_total)
+        self.k = int(k)
+        self.m = int(m)
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+
+    def init_centers(self, seed: int, codes_local: np.ndarray) -> np.ndarray:
+        """clustering.py:149-157 over the global index space, rows gathered from owners."""
+        rng = np.random.default_rng(seed)
+        idx = rng.choice(self.n_total, size=self.k, replace=False)
+        lo, hi = self.b.offset, self.b.offset + self.b.n
+        mine = {int(i): codes_local[int(i) - lo] for i in idx if lo <= i < hi}
+        parts = _allgather_obj(mine, self.group)
+        rows = {}
+        for p in parts:
+            rows.update(p)
+        return np.stack([rows[int(i)] for i in idx]).astype(np.uint8)
+
+    def iteration(self, centers_dev, previous: float | None) -> tuple[StepStats, object, bool]:
+        """One Lloyd iteration; returns (stats, next centers, stopped)."""
+        t0 = time.perf_counter()
+        self.b.assign(centers_dev)
+        self.b.sync()
+        assign_seconds = time.perf_counter() - t0
+        sums = self.b.objective_sums()
+        parts = _allgather_obj((float(sums[0]), float(sums[1])), self.group)
+        s1 = tree_combine(self.n_total, [p[0] for p in parts])
+        s2 = tree_combine(self.n_total, [p[1] for p in parts])
+        objective = float(np.float64(s1) / self.n_total)
+        objective_sq = float(np.float64(s2) / self.n_total)
+        if previous is not None and objective == previous:
+            return StepStats(objective, objective_sq, 0, 0, 0, assign_seconds, 0.0), centers_dev, True
+        t1 = time.perf_counter()
+        hist, counts = self.b.histogram()
+        if self.world > 1:
+            dist.all_reduce(hist, op=dist.ReduceOp.SUM, group=self.group)
+            dist.all_reduce(counts, op=dist.ReduceOp.SUM, group=self.group)
+        stats = self.b.vote()
+        empty_n = int(stats[3])
+        if empty_n:
+            counts_h = self.b.counts_host()
+            empty = np.flatnonzero(counts_h == 0)
+            cand = self.b.local_candidates(empty_n)
+            allc = _allgather_obj(cand, self.group)
+            _, _, rows = merge_candidates(allc, empty_n)
+            self.b.apply_repair(empty, rows)
+        nxt = self.b.take_new_centers()
+        self.b.sync()
+        update_seconds = time.perf_counter() - t1
+        st = StepStats(objective, objective_sq, empty_n, int(stats[4]), int(stats[2]), assign_seconds, update_seconds)
+        return st, nxt, False
+
+
+def shard_bounds(n_total: int, world: int, rank: int) -> tuple[int, int]:
+    """(offset, length) of this rank's tree-aligned shard."""
+    return tree_split(n_total, world)[rank]
+
+
+def fit_sharded(codes_local: np.ndarray, n_total: int, tables, k: int, max_iterations: int = 20, seed: int = 0, *,
+                update: str = "sparse", initial_centers=None, backend=None, group=None):
+    """``fit`` over row-sharded codes (clustering.py:377-482 semantics).
+
+    ``codes_local`` must be this rank's :func:`shard_bounds` slice.  Returns a
+    ``ClusteringResult`` whose labels are the local shard's labels.
+    """
+    from .clustering import ClusteringResult, IterationStats
+    from .pq import _validate_codes, as_tables
+
+    t = as_tables(tables)
+    m_count = t.num_subspaces
+    codes_local = _validate_codes(codes_local, m_count, t.num_codewords)
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    offset, length = shard_bounds(n_total, world, rank)
+    if length != len(codes_local):
+        raise ValueError(f"rank {rank} holds {len(codes_local)} codes, expected the tree-aligned shard of {length}")
+    if not 1 <= k <= n_total:
+        raise ValueError(f"k must be in [1, {n_total}], got {k}")
+    if backend is None:
+        backend = GpuShardBackend(codes_local, offset, t.tables, k)
+    drv = DistributedLloyd(backend, n_total, k, m_count, group)
+    if initial_centers is None:
+        centers = drv.init_centers(seed, codes_local)
+    else:
+        centers = _validate_codes(initial_centers, m_count, t.num_codewords).astype(np.uint8)
+    cur = backend.upload_centers(centers)
+    trace = []
+    previous = None
+    converged = False
+    for iteration in range(1, max_iterations + 1):
+        st, nxt, stop = drv.iteration(cur, previous)
+        if stop:
+            trace.append(IterationStats(iteration, st.objective, st.objective_sq, st.assign_seconds, 0.0))
+            converged = True
+            break
+        mean_nnz = st.nnz_total / (st.filled * m_count) if st.filled else 0.0
+        trace.append(
+            IterationStats(
+                iteration,
+                st.objective,
+                st.objective_sq,
+                st.assign_seconds,
+                st.update_seconds,
+                repaired_clusters=st.empty,
+                mean_histogram_nnz=None if update == "naive" else mean_nnz,
+            )
+        )
+        cur = nxt
+        previous = st.objective
+    return ClusteringResult(backend.centers_host(cur).astype(np.uint8), backend.labels_host().copy(), trace,
+                            len(trace), converged)

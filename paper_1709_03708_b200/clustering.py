@@ -55,6 +55,55 @@ class ClusteringResult:
     converged: bool = False
 
 
+@dataclass(frozen=True)
+class FrequencyHistogram:
+    """Counts of codeword indices inside one (cluster, subspace) pair (clustering.py:68-83)."""
+
+    counts: np.ndarray
+    support: np.ndarray
+
+    @property
+    def nnz(self) -> int:
+        return len(self.support)
+
+
+def build_histogram(subindices: np.ndarray, num_codewords: int) -> FrequencyHistogram:
+    """Tally subindices into L bins (clustering.py:86-105; host-side input helper)."""
+    values = np.asarray(subindices)
+    if values.ndim != 1:
+        raise ValueError(f"subindices must be 1-d, got shape {values.shape}")
+    if values.size and (values.min() < 0 or values.max() >= num_codewords):
+        raise ValueError(
+            f"subindices must lie in [0, {num_codewords}), got range [{values.min()}, {values.max()}]"
+        )
+    counts = np.bincount(values.astype(np.intp), minlength=num_codewords)
+    return FrequencyHistogram(counts, np.flatnonzero(counts))
+
+
+def update_center_sparse(histograms, tables) -> np.ndarray:
+    """One center from per-subspace member histograms by sparse voting on the GPU (clustering.py:125-146)."""
+    t = as_tables(tables)
+    if len(histograms) != t.num_subspaces:
+        raise ValueError(f"expected {t.num_subspaces} histograms, got {len(histograms)}")
+    hist = np.zeros((1, t.num_subspaces, t.num_codewords), dtype=np.int64)
+    for m, h in enumerate(histograms):
+        if h.nnz == 0:
+            raise ValueError(f"histogram for subspace {m} is empty")
+        hist[0, m, : len(h.counts)] = h.counts
+    return engine.vote_host(hist, t.tables)[0]
+
+
+def update_center_naive(member_codes: np.ndarray, tables) -> np.ndarray:
+    """One center by candidate scan (clustering.py:108-122); same argmin as the vote, computed on the GPU."""
+    t = as_tables(tables)
+    codes = _validate_codes(member_codes, t.num_subspaces, t.num_codewords)
+    if len(codes) == 0:
+        raise ValueError("cannot update a center from an empty cluster")
+    hist = np.stack([np.bincount(codes[:, m].astype(np.intp), minlength=t.num_codewords)
+                     for m in range(t.num_subspaces)])[None]
+    return engine.vote_host(hist, t.tables)[0]
+
+
 def init_centers(codes: np.ndarray, k: int, seed: int = 0) -> np.ndarray:
     """Pick K initial centers by sampling input codes without replacement."""
     codes = np.asarray(codes)

@@ -207,11 +207,11 @@ struct ScanParams {
 };
 
 template <int W>
-__device__ __forceinline__ void load_rotated(const uint8_t* __restrict__ codes, int64_t idx, bool valid, int c,
+__device__ __forceinline__ void load_rotated(const uint8_t* __restrict__ codes, int idx, bool valid, int c,
                                              uint32_t (&out)[W]) {
   uint32_t w[W];
   if (valid) {
-    const uint32_t* p = reinterpret_cast<const uint32_t*>(codes + idx * (4 * W));
+    const uint32_t* p = reinterpret_cast<const uint32_t*>(codes + (size_t)idx * (4 * W));
     if constexpr (W == 1) {
       w[0] = __ldg(p);
     } else if constexpr (W == 2) {
@@ -298,21 +298,20 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) scan_kernel(const ScanParams
 #pragma unroll
   for (int i = 0; i < MP; ++i) lc[i] = (uint32_t)(((c + i) % MP) * (KC * 4) + h * 16);
   const uint32_t stage0 = smem_u32(stages);
+  const int n = (int)p.n;
+  const int pass_size = (int)p.pass_size;
 
-  int64_t g = 0;
-  for (int64_t pi = 0; pi < my_passes; ++pi) {
-    const int64_t pass = blockIdx.x + pi * G;
-    const int64_t base = pass * p.pass_size;
-    const int64_t end = min(p.n, base + p.pass_size);
+  uint32_t g = 0;
+  for (int pi = 0; pi < (int)my_passes; ++pi) {
+    const int base = ((int)blockIdx.x + pi * (int)G) * pass_size;
+    const int end = min(n, base + pass_size);
+    const int my0 = base + warp * OWN_W + o;  // code of slot j: my0 + j*OWN
 
     uint32_t cw[C][W];
     uint32_t bk[C], sk[C], bc[C];
-    bool on[C];
 #pragma unroll
     for (int j = 0; j < C; ++j) {
-      const int64_t first = base + (int64_t)j * OWN + warp * OWN_W;
-      on[j] = first < end;
-      const int64_t idx = first + o;
+      const int idx = my0 + j * OWN;
       load_rotated<W>(p.codes, idx, idx < end, c, cw[j]);
       bk[j] = 0xffffffffu;
       sk[j] = 0xffffffffu;
@@ -321,38 +320,48 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) scan_kernel(const ScanParams
 
     for (int t = 0; t < nchunks; ++t, ++g) {
       const int st = (int)(g % S);
-      const uint32_t ph = (uint32_t)((g / S) & 1);
+      const uint32_t ph = (g / S) & 1u;
       mbar_wait(&full[st], ph);
       const uint32_t sb = stage0 + (uint32_t)st * chunk_bytes;
       uint32_t lcs[MP];
 #pragma unroll
       for (int i = 0; i < MP; ++i) lcs[i] = sb + lc[i];
+      // software pipeline: the LDS.128s of code j+1 are in flight while code j is reduced
+      float4 buf[2][MP];
+#pragma unroll
+      for (int i = 0; i < MP; ++i)
+        buf[0][i] = lds128(__byte_perm(cw[0][i >> 2], 0u, 0x4440u | (uint32_t)(i & 3)) * ROW + lcs[i]);
 #pragma unroll
       for (int j = 0; j < C; ++j) {
-        if (on[j]) {
-          uint32_t x = __byte_perm(cw[j][0], 0u, 0x4440u);
-          float4 acc = lds128(x * ROW + lcs[0]);
+        if (j + 1 < C) {
 #pragma unroll
-          for (int i = 1; i < MP; ++i) {
-            x = __byte_perm(cw[j][i >> 2], 0u, 0x4440u | (uint32_t)(i & 3));
-            const float4 v = lds128(x * ROW + lcs[i]);
-            acc.x += v.x;
-            acc.y += v.y;
-            acc.z += v.z;
-            acc.w += v.w;
-          }
-          const uint32_t k0 = (__float_as_uint(acc.x) & ~3u);
-          const uint32_t k1 = (__float_as_uint(acc.y) & ~3u) | 1u;
-          const uint32_t k2 = (__float_as_uint(acc.z) & ~3u) | 2u;
-          const uint32_t k3 = (__float_as_uint(acc.w) & ~3u) | 3u;
-          const uint32_t lo01 = min(k0, k1), hi01 = max(k0, k1);
-          const uint32_t lo23 = min(k2, k3), hi23 = max(k2, k3);
-          const uint32_t lo = min(lo01, lo23);
-          const uint32_t mid = min(max(lo01, lo23), min(hi01, hi23));
-          bc[j] = (lo < bk[j]) ? (uint32_t)t : bc[j];
-          sk[j] = min(max(bk[j], lo), min(sk[j], mid));
-          bk[j] = min(bk[j], lo);
+          for (int i = 0; i < MP; ++i)
+            buf[(j + 1) & 1][i] =
+                lds128(__byte_perm(cw[j + 1][i >> 2], 0u, 0x4440u | (uint32_t)(i & 3)) * ROW + lcs[i]);
         }
+        float4* v = buf[j & 1];
+        // pairwise tree over the MP subspace terms (any order is covered by the certificate)
+#pragma unroll
+        for (int w = 1; w < MP; w *= 2) {
+#pragma unroll
+          for (int i = 0; i + w < MP; i += 2 * w) {
+            v[i].x += v[i + w].x;
+            v[i].y += v[i + w].y;
+            v[i].z += v[i + w].z;
+            v[i].w += v[i + w].w;
+          }
+        }
+        const uint32_t k0 = (__float_as_uint(v[0].x) & ~3u);
+        const uint32_t k1 = (__float_as_uint(v[0].y) & ~3u) | 1u;
+        const uint32_t k2 = (__float_as_uint(v[0].z) & ~3u) | 2u;
+        const uint32_t k3 = (__float_as_uint(v[0].w) & ~3u) | 3u;
+        const uint32_t lo01 = min(k0, k1), hi01 = max(k0, k1);
+        const uint32_t lo23 = min(k2, k3), hi23 = max(k2, k3);
+        const uint32_t lo = min(lo01, lo23);
+        const uint32_t mid = min(max(lo01, lo23), min(hi01, hi23));
+        bc[j] = (lo < bk[j]) ? (uint32_t)t : bc[j];
+        sk[j] = min(max(bk[j], lo), min(sk[j], mid));
+        bk[j] = min(bk[j], lo);
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[st]);
@@ -361,7 +370,6 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) scan_kernel(const ScanParams
     // ---------------- finalize: merge lanes, certify, exact fp64 distance ----------------
 #pragma unroll
     for (int j = 0; j < C; ++j) {
-      if (!on[j]) continue;
       uint32_t b = bk[j], s = sk[j];
       uint32_t ci = bc[j] * KC + h * 4 + (b & 3u);
       if constexpr (H == 2) {
@@ -375,7 +383,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) scan_kernel(const ScanParams
         }
         s = ns;
       }
-      const int64_t idx = base + (int64_t)j * OWN + warp * OWN_W + o;
+      const int idx = my0 + j * OWN;
       if (h == 0 && idx < end) {
         const uint32_t sm = s & ~3u;
         bool cert;
@@ -387,7 +395,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) scan_kernel(const ScanParams
           cert = (double)fsl > (double)fbh * p.cert_factor;
         }
         if (cert) {
-          const uint8_t* xc = p.codes + idx * MP;
+          const uint8_t* xc = p.codes + (size_t)idx * MP;
           const uint8_t* cc = p.ucodes + (size_t)ci * MP;
           double acc = 0.0;
           for (int mm = 0; mm < p.m; ++mm)
@@ -396,7 +404,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) scan_kernel(const ScanParams
           p.sd_sq[idx] = acc;
         } else {
           const int f = atomicAdd(p.flag_count, 1);
-          p.flags[f] = (int32_t)idx;
+          p.flags[f] = idx;
         }
       }
     }
@@ -530,23 +538,40 @@ static AssignWS assign_ws_layout(void* base, int64_t n, int64_t k, int mp, int l
   return w;
 }
 
-template <int MP, int KC, int C, int NW, int S>
-static int launch_scan(const ScanParams& base_params, int l, cudaStream_t stream) {
-  constexpr int H = KC / 4;
-  constexpr int NB = NW * (32 / H) * C;  // codes per pass (register capacity of a CTA)
+template <int MP, int KC, int NW, int S, int C, int... Cs>
+static int launch_scan_c(int c_need, const ScanParams& p, int grid, int l, cudaStream_t stream) {
+  if constexpr (sizeof...(Cs) > 0) {
+    if (c_need > C) return launch_scan_c<MP, KC, NW, S, Cs...>(c_need, p, grid, l, stream);
+  }
   const DevInfo& di = dev_info();
   const size_t smem = 128 + (size_t)S * l * MP * KC * 4;
   if ((int)smem > di.smem_optin) return fail(PQK_EUNSUPPORTED, "assignment chunk ring exceeds shared memory");
   auto kern = scan_kernel<MP, KC, C, NW, S>;
   PQK_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  ProfileEvents& pe = profile_events();
+  if (pe.before) PQK_CUDA_TRY(cudaEventRecord(pe.before, stream));
+  kern<<<grid, (NW + 1) * 32, smem, stream>>>(p);
+  PQK_LAUNCH_CHECK("scan_kernel");
+  if (pe.after) PQK_CUDA_TRY(cudaEventRecord(pe.after, stream));
+  return PQK_OK;
+}
+
+// Balanced persistent schedule: every CTA runs the same number of equal passes and
+// the kernel variant with the smallest register slot count C that holds a pass.
+template <int MP, int KC, int NW, int S, int... Cs>
+static int launch_scan(const ScanParams& base_params, int l, cudaStream_t stream) {
+  constexpr int H = KC / 4;
+  constexpr int OWN = NW * (32 / H);
+  constexpr int CMAX = std::max({Cs...});
+  constexpr int NB = OWN * CMAX;  // codes per pass (register capacity of a CTA)
+  const DevInfo& di = dev_info();
   ScanParams p = base_params;
   const int64_t n = p.n;
   const int64_t G = di.sms;
-  // Balanced persistent schedule: every CTA runs the same number of equal passes.
   const int64_t per_cta = std::max<int64_t>(1, (n + G * NB - 1) / (G * NB));
   int64_t npasses = G * per_cta;
   int64_t pass_size = (n + npasses - 1) / npasses;
-  // Small inputs: do not spread below ~1/4 of a CTA's register capacity per pass.
+  // Small inputs: fewer CTAs rather than passes below ~1/4 of the register capacity.
   const int64_t min_pass = std::max<int64_t>(1, NB / 4);
   if (pass_size < min_pass) {
     pass_size = min_pass;
@@ -556,12 +581,8 @@ static int launch_scan(const ScanParams& base_params, int l, cudaStream_t stream
   p.npasses = npasses;
   const int grid = (int)std::min<int64_t>(G, npasses);
   if (grid <= 0) return PQK_OK;
-  ProfileEvents& pe = profile_events();
-  if (pe.before) PQK_CUDA_TRY(cudaEventRecord(pe.before, stream));
-  kern<<<grid, (NW + 1) * 32, smem, stream>>>(p);
-  PQK_LAUNCH_CHECK("scan_kernel");
-  if (pe.after) PQK_CUDA_TRY(cudaEventRecord(pe.after, stream));
-  return PQK_OK;
+  const int c_need = (int)((pass_size + OWN - 1) / OWN);
+  return launch_scan_c<MP, KC, NW, S, Cs...>(c_need, p, grid, l, stream);
 }
 
 }  // namespace pqk
@@ -658,10 +679,10 @@ extern "C" int pqk_assign_device(const uint8_t* d_codes, int64_t n, int32_t m, i
     sp.flags = w.flags;
     sp.flag_count = w.counters + 1;
     switch (mp) {
-      case 4: rc = launch_scan<4, 8, 16, 11, 4>(sp, l, stream); break;
-      case 8: rc = launch_scan<8, 4, 12, 11, 4>(sp, l, stream); break;
-      case 16: rc = launch_scan<16, 4, 8, 11, 3>(sp, l, stream); break;
-      case 32: rc = launch_scan<32, 4, 4, 11, 1>(sp, l, stream); break;
+      case 4: rc = launch_scan<4, 8, 11, 4, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14>(sp, l, stream); break;
+      case 8: rc = launch_scan<8, 4, 11, 4, 1, 2, 3, 4, 5, 6, 7, 8>(sp, l, stream); break;
+      case 16: rc = launch_scan<16, 4, 11, 3, 1, 2, 3, 4>(sp, l, stream); break;
+      case 32: rc = launch_scan<32, 4, 11, 1, 1, 2>(sp, l, stream); break;
     }
     if (rc != PQK_OK) return rc;
   }

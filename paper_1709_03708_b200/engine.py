@@ -383,6 +383,23 @@ def paired_distance_host(tables: np.ndarray, a: np.ndarray, b: np.ndarray, *, de
         return out.cpu().numpy()
 
 
+def vote_host(hist: np.ndarray, tables: np.ndarray, *, device=None) -> np.ndarray:
+    """Sparse-vote centers for (K, M, L) host histograms; (K, M) uint8 (empty rows -> 0)."""
+    dev = device_of(device)
+    dt = device_tables(tables, dev)
+    k = hist.shape[0]
+    if hist.max(initial=0) >= 2**31:
+        raise ValueError("histogram counts must fit in int32")
+    with torch.cuda.device(dev):
+        h = torch.from_numpy(np.ascontiguousarray(hist, dtype=np.int32)).to(dev)
+        counts = torch.from_numpy(hist[:, 0, :].sum(axis=1).astype(np.int32)).to(dev)
+        out = torch.zeros((k, dt.mp), dtype=torch.uint8, device=dev)
+        stats = torch.zeros(STATS_LEN, dtype=torch.int64, device=dev)
+        call("pqk_vote_device", _ptr(h), _ptr(counts), k, dt.m, dt.l, _ptr(dt.t64), _ptr(out), _ptr(stats),
+             _stream(dev))
+        return download_codes(out, dt.m)
+
+
 def mean_objectives(sd_dev: "torch.Tensor", n: int, dev) -> tuple[float, float]:
     """(mean(sqrt(sd)), mean(sd)) with numpy's summation tree, on device."""
     plan = pairwise_plan(n, dev)

@@ -251,12 +251,12 @@ def main() -> None:
     eng = backend.eng
 
     def step_single(cur):
+        # the iteration body of fit(): one host read (objective + stats) per iteration
         eng.assign(cur)
         eng.objective()
-        eng.obj.cpu()  # host read of the objective (stop-rule check of fit)
         eng.histogram()
         eng.vote()
-        st = eng.stats_host()
+        _, st = eng.read_obj_stats()
         if st[_lib.STAT_EMPTY]:
             eng.repair()
         return eng.new_centers.clone(), st
@@ -280,7 +280,7 @@ def main() -> None:
         for _ in range(args.warmup):
             cur, _ = step(cur)
         torch.cuda.synchronize(dev)
-        step_ms, scan_ms, uniq, flagged = [], [], [], []
+        step_ms, scan_ms, uniq, flagged, vote_fp64, vote_dd = [], [], [], [], [], []
         launches0 = lib.pqk_launch_count()
         with ClockSampler(local) as clocks:
             for _ in range(args.steps):
@@ -298,6 +298,8 @@ def main() -> None:
                 scan_ms.append(ev_scan0.elapsed_time(ev_scan1))
                 uniq.append(int(st[_lib.STAT_UNIQUE_CENTERS]))
                 flagged.append(int(st[_lib.STAT_FLAGGED]))
+                vote_fp64.append(int(st[_lib.STAT_VOTE_FP64]))
+                vote_dd.append(int(st[_lib.STAT_VOTE_EXACT]))
         launches = lib.pqk_launch_count() - launches0
     lib.pqk_set_profile_events(None, None)
 
@@ -342,6 +344,7 @@ def main() -> None:
         "data": "synthetic",
         "config": {"workload": cfg["workload"], "n": n_total, "k": k, "m": m, "l": l_count,
                    "unique_centers": u, "flagged_codes_per_iter": int(np.median(flagged)),
+                   "votes_fp64_per_iter": int(np.median(vote_fp64)), "votes_dd_per_iter": int(np.median(vote_dd)),
                    "l2": "flushed (512 MB write) between timed iterations",
                    "step": "assign+certify+objective+histogram+allreduce+vote+repair",
                    "parallelism": f"codes sharded dp{world}"},

@@ -61,7 +61,8 @@ enum {
   PQK_STAT_VOTE_EXACT = 5,     /* (k,m) votes resolved by the double-double path    */
   PQK_STAT_ENCODE_FLAGGED = 6, /* encoder (vector,m) pairs recomputed in fp64       */
   PQK_STAT_NCHUNKS = 7,        /* center chunks streamed by the assignment scan     */
-  PQK_STATS_LEN = 16
+  PQK_STAT_VOTE_FP64 = 8,      /* (k,m) votes not certified by the fp32 filter      */
+  PQK_STATS_LEN = 24           /* slots 0..15 public, 16..23 scratch accumulators   */
 };
 
 /* ---- library / device info -------------------------------------------------- */
@@ -118,11 +119,13 @@ int pqk_histogram_device(const uint8_t* d_codes, int64_t n, int32_t m, int32_t l
 
 /* Sparse-voting update (clustering.py:349-356): for filled k,
  * new_centers[k][m] = argmin_j sum_s hist[k][m][s] * T[m][s][j] (lowest j on ties,
- * exact-arithmetic argmin certified in fp64, double-double on near ties).  Empty
- * clusters get code 0 (repaired by pqk_repair_device).  Writes NNZ_TOTAL, FILLED,
- * EMPTY, VOTE_EXACT stats.  Requires hist/counts already reduced over all shards. */
+ * exact-arithmetic argmin: certified fp32 filter on d_t32 (nullable), then certified
+ * fp64, double-double on near ties).  Empty clusters get code 0 (repaired by
+ * pqk_repair_device).  Writes NNZ_TOTAL, FILLED, EMPTY, VOTE_EXACT stats.  Requires
+ * hist/counts already reduced over all shards. */
 int pqk_vote_device(const int32_t* d_hist, const int32_t* d_counts, int64_t k, int32_t m, int32_t l,
-                    const double* d_t64, uint8_t* d_new_centers, int64_t* d_stats, void* stream);
+                    const double* d_t64, const float* d_t32, uint8_t* d_new_centers, int64_t* d_stats,
+                    void* stream);
 
 /* Empty-cluster repair (clustering.py:460-466): the E empty clusters (ascending k)
  * take the codes of the E codes with largest sd_sq (lowest index among ties). */

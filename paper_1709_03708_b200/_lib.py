@@ -26,7 +26,8 @@ STAT_FILLED = 4
 STAT_VOTE_EXACT = 5
 STAT_ENCODE_FLAGGED = 6
 STAT_NCHUNKS = 7
-STATS_LEN = 16
+STAT_VOTE_FP64 = 8
+STATS_LEN = 24
 
 _p = C.c_void_p
 _i32 = C.c_int32
@@ -53,7 +54,7 @@ SIGNATURES: dict[str, tuple] = {
     ),
     "pqk_paired_distance_device": (C.c_int, [_p, _p, _p, _i64, _i32, _i32, _p, _p, _p]),
     "pqk_histogram_device": (C.c_int, [_p, _i64, _i32, _i32, _p, _i64, _p, _p, _p]),
-    "pqk_vote_device": (C.c_int, [_p, _p, _i64, _i32, _i32, _p, _p, _p, _p]),
+    "pqk_vote_device": (C.c_int, [_p, _p, _i64, _i32, _i32, _p, _p, _p, _p, _p]),
     "pqk_repair_workspace_bytes": (_sz, [_i64, _i64]),
     "pqk_repair_device": (C.c_int, [_p, _p, _i64, _i32, _p, _i64, _p, _p, _sz, _p, _p]),
     "pqk_repair_candidates_device": (C.c_int, [_p, _i64, _i64, _i64, _p, _sz, _p, _p, _p]),

@@ -303,8 +303,13 @@ def fit(
         trace: list[IterationStats] = []
         previous = None
         converged = False
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
         for iteration in range(1, max_iterations + 1):
-            start = time.perf_counter()
+            # One stream-ordered iteration: assign, objective sums, histogram and the
+            # (speculative) vote into the next-centers buffer, then a single host read of
+            # objective + stats.  If the stop rule fires the vote result is discarded, so
+            # the observable semantics are the reference's (clustering.py:442-481).
+            ev[0].record()
             if device_scan:
                 eng.assign(cur)
             else:
@@ -312,11 +317,13 @@ def fit(
                 lab = np.asarray(external(codes, host_centers, t, threads), dtype=np.uint32)
                 eng.labels[:n].copy_(torch.from_numpy(lab.view(np.int32)).to(dev))
                 eng.distances_for_labels(cur)
-            torch.cuda.current_stream(dev).synchronize()
-            assign_seconds = time.perf_counter() - start
-
+            ev[1].record()
             eng.objective()
-            sums = eng.obj.cpu().numpy()
+            eng.histogram()
+            eng.vote()
+            ev[2].record()
+            sums, stats = eng.read_obj_stats()
+            assign_seconds = ev[0].elapsed_time(ev[1]) / 1e3
             objective = engine.mean_from_sum(sums[0], n)
             objective_sq = engine.mean_from_sum(sums[1], n)
             if previous is not None and objective == previous:
@@ -325,15 +332,12 @@ def fit(
                 break
 
             start = time.perf_counter()
-            eng.histogram()
-            eng.vote()
-            stats = eng.stats_host()
             empty = int(stats[engine._lib.STAT_EMPTY])
             if empty:
                 eng.repair()
             nxt = eng.new_centers.clone()
             torch.cuda.current_stream(dev).synchronize()
-            update_seconds = time.perf_counter() - start
+            update_seconds = ev[1].elapsed_time(ev[2]) / 1e3 + (time.perf_counter() - start)
             filled = int(stats[engine._lib.STAT_FILLED])
             nnz_total = int(stats[engine._lib.STAT_NNZ_TOTAL])
             mean_nnz = nnz_total / (filled * m_count) if filled else 0.0

@@ -344,6 +344,7 @@ extern "C" int pqk_lloyd_step_host(const uint8_t* codes, int64_t n, int32_t m, c
   PQK_TRY(pqk_histogram_device((const uint8_t*)c->codes.p, n, m, l, (const uint32_t*)c->labels.p, k,
                                (int32_t*)c->hist.p, (int32_t*)c->counts.p, c->stream));
   PQK_TRY(pqk_vote_device((const int32_t*)c->hist.p, (const int32_t*)c->counts.p, k, m, l, (const double*)c->t64.p,
+                          fp64_only ? nullptr : (const float*)c->t32.p,
                           (uint8_t*)c->newc.p, dstats, c->stream));
   int64_t hstats[PQK_STATS_LEN];
   PQK_CUDA_TRY(cudaMemcpyAsync(hstats, dstats, sizeof(hstats), cudaMemcpyDeviceToHost, c->stream));

@@ -453,6 +453,65 @@ __global__ void rescan_kernel(const uint8_t* __restrict__ codes, int64_t n, int 
   }
 }
 
+// Same exact scan, one CTA per code: the code's M float64 table rows T[m][x^m][:]
+// are staged in shared memory, threads stride over the distinct centers.
+__global__ void __launch_bounds__(256) rescan_cta_kernel(
+    const uint8_t* __restrict__ codes, int64_t n, int mp, int m, int l, const uint8_t* __restrict__ ucodes,
+    const int32_t* __restrict__ counters, const int32_t* __restrict__ flags, const int32_t* __restrict__ flag_count,
+    const int32_t* __restrict__ pos2idx, const double* __restrict__ t64, uint32_t* __restrict__ labels,
+    double* __restrict__ sd_sq, int all_mode) {
+  extern __shared__ double s_rows[];  // m * l
+  __shared__ double s_best[8];
+  __shared__ int s_bu[8];
+  const int64_t nf = all_mode ? n : (int64_t)(*flag_count);
+  const int U = counters[0];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int64_t f = blockIdx.x; f < nf; f += gridDim.x) {
+    const int64_t idx = all_mode ? f : (int64_t)flags[f];
+    const uint8_t* xc = codes + idx * mp;
+    __syncthreads();
+    for (int e = tid; e < m * l; e += blockDim.x) {
+      const int mm = e / l, s = e - mm * l;
+      s_rows[e] = __ldg(&t64[((size_t)mm * l + xc[mm]) * l + s]);
+    }
+    __syncthreads();
+    double best = __longlong_as_double(0x7ff0000000000000LL);
+    int bu = 0x7fffffff;
+    for (int u = tid; u < U; u += blockDim.x) {
+      const uint8_t* cc = ucodes + (size_t)u * mp;
+      double d = 0.0;
+      for (int mm = 0; mm < m; ++mm) d = dadd(d, s_rows[mm * l + cc[mm]]);
+      if (d < best) {
+        best = d;
+        bu = u;
+      }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, off);
+      const int ou = __shfl_xor_sync(0xffffffffu, bu, off);
+      if (ob < best || (ob == best && ou < bu)) {
+        best = ob;
+        bu = ou;
+      }
+    }
+    if (lane == 0) {
+      s_best[warp] = best;
+      s_bu[warp] = bu;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      for (int w = 1; w < (int)(blockDim.x >> 5); ++w)
+        if (s_best[w] < best || (s_best[w] == best && s_bu[w] < bu)) {
+          best = s_best[w];
+          bu = s_bu[w];
+        }
+      labels[idx] = (uint32_t)pos2idx[bu];
+      sd_sq[idx] = best;
+    }
+  }
+}
+
 __global__ void assign_stats_kernel(const int32_t* __restrict__ counters, int64_t* __restrict__ stats) {
   stats[PQK_STAT_UNIQUE_CENTERS] = counters[0];
   stats[PQK_STAT_FLAGGED] = counters[1];
@@ -688,11 +747,27 @@ extern "C" int pqk_assign_device(const uint8_t* d_codes, int64_t n, int32_t m, i
   }
   // 4. exact rescan of uncertified codes (or every code in fp64-only mode)
   {
-    const int64_t warps = fast ? (int64_t)di.sms * 32 : std::min<int64_t>(n, (int64_t)di.sms * 64);
-    const int grid = (int)std::max<int64_t>(1, (warps * 32 + 255) / 256);
-    rescan_kernel<<<grid, 256, 0, stream>>>(d_codes, n, mp, m, l, w.ucodes, w.counters, w.flags, w.counters + 1,
-                                            w.pos2idx, d_t64, d_labels, d_sd_sq, fast ? 0 : 1);
-    PQK_LAUNCH_CHECK("rescan_kernel");
+    const size_t rows_bytes = (size_t)m * l * sizeof(double);
+    if (rows_bytes <= 96 * 1024) {
+      static bool attr_set[64] = {};
+      int dev = 0;
+      cudaGetDevice(&dev);
+      if (!attr_set[dev & 63]) {
+        PQK_CUDA_TRY(cudaFuncSetAttribute(rescan_cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
+        attr_set[dev & 63] = true;
+      }
+      const int grid = (int)std::min<int64_t>(fast ? (int64_t)di.sms * 2 : n, (int64_t)di.sms * 8);
+      rescan_cta_kernel<<<std::max(grid, 1), 256, rows_bytes, stream>>>(
+          d_codes, n, mp, m, l, w.ucodes, w.counters, w.flags, w.counters + 1, w.pos2idx, d_t64, d_labels, d_sd_sq,
+          fast ? 0 : 1);
+      PQK_LAUNCH_CHECK("rescan_cta_kernel");
+    } else {
+      const int64_t warps = fast ? (int64_t)di.sms * 32 : std::min<int64_t>(n, (int64_t)di.sms * 64);
+      const int grid = (int)std::max<int64_t>(1, (warps * 32 + 255) / 256);
+      rescan_kernel<<<grid, 256, 0, stream>>>(d_codes, n, mp, m, l, w.ucodes, w.counters, w.flags, w.counters + 1,
+                                              w.pos2idx, d_t64, d_labels, d_sd_sq, fast ? 0 : 1);
+      PQK_LAUNCH_CHECK("rescan_kernel");
+    }
   }
   if (d_stats) {
     assign_stats_kernel<<<1, 1, 0, stream>>>(w.counters, d_stats);

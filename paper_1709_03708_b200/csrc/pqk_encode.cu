@@ -118,7 +118,7 @@ extern "C" int pqk_encode_device(const float* d_vectors, int64_t n, int32_t d, c
   if (n == 0) return PQK_OK;
   if (m > 65535) return fail(PQK_EUNSUPPORTED, "pqk_encode_device: too many subspaces");
   const int dsub = d / m;
-  unsigned long long* flagged = reinterpret_cast<unsigned long long*>(d_stats + 12);
+  unsigned long long* flagged = reinterpret_cast<unsigned long long*>(d_stats + 20);
   PQK_CUDA_TRY(cudaMemsetAsync(flagged, 0, sizeof(unsigned long long), stream));
   if (code_stride > m) PQK_CUDA_TRY(cudaMemsetAsync(d_codes, 0, (size_t)n * code_stride, stream));
   dim3 grid((unsigned)((n + 127) / 128), (unsigned)m);

@@ -90,16 +90,16 @@ __device__ __forceinline__ bool dd_less(const DD& a, const DD& b) {
 
 __global__ void __launch_bounds__(256) vote_kernel(const int32_t* __restrict__ hist, const int32_t* __restrict__ counts,
                                                    int64_t k, int m, int l, int mp, const double* __restrict__ t64,
-                                                   uint8_t* __restrict__ newc, unsigned long long* __restrict__ acc) {
+                                                   const float* __restrict__ t32, uint8_t* __restrict__ newc,
+                                                   unsigned long long* __restrict__ acc) {
   __shared__ int s_s[kMaxL];
   __shared__ double s_h[kMaxL];
   __shared__ int s_wc[8];
   __shared__ Best s_best[8];
   __shared__ DD s_dd[8];
-  __shared__ int s_nnz;
-  const int64_t km = blockIdx.x;
-  const int64_t kk = km / m;
-  const int mm = (int)(km - kk * m);
+  // m-major block order: concurrently running blocks share one subspace table
+  const int mm = (int)(blockIdx.x / k);
+  const int64_t kk = blockIdx.x - (int64_t)mm * k;
   if (counts[kk] == 0) return;  // empty: left 0, repaired later
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int hv = (tid < l) ? hist[(kk * m + mm) * l + tid] : 0;
@@ -117,13 +117,50 @@ __global__ void __launch_bounds__(256) vote_kernel(const int32_t* __restrict__ h
     s_s[pos] = tid;
     s_h[pos] = (double)hv;
   }
-  if (tid == 0) {
-    s_nnz = nnz;
-    atomicAdd(&acc[0], (unsigned long long)nnz);
-  }
+  if (tid == 0) atomicAdd(&acc[0], (unsigned long long)nnz);
   __syncthreads();
+  const double inf = __longlong_as_double(0x7ff0000000000000LL);
+  if (t32) {
+    // fp32 filter: every term h*t >= 0 carries relative error <= 2u (count and table
+    // conversion) plus one FMA rounding, so a gap above 4(nnz+3)u32 proves the
+    // exact-arithmetic argmin.
+    const float* tf = t32 + (size_t)mm * l * l;
+    float vf = __int_as_float(0x7f800000);
+    if (tid < l) {
+      // 8 independent partial sums keep 8 table loads in flight per thread
+      float part[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+      int j = 0;
+      for (; j + 8 <= nnz; j += 8) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          part[q] = __fmaf_rn((float)s_h[j + q], __ldg(&tf[(size_t)s_s[j + q] * l + tid]), part[q]);
+      }
+      for (int q = 0; j < nnz; ++j, ++q) part[q] = __fmaf_rn((float)s_h[j], __ldg(&tf[(size_t)s_s[j] * l + tid]), part[q]);
+      vf = ((part[0] + part[1]) + (part[2] + part[3])) + ((part[4] + part[5]) + (part[6] + part[7]));
+    }
+    Best bf{(double)vf, tid, inf};
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) bf = merge_best(bf, shfl_best(bf, o));
+    if (lane == 0) s_best[warp] = bf;
+    __syncthreads();
+    if (warp == 0) {
+      bf = s_best[lane & 7];
+#pragma unroll
+      for (int o = 4; o > 0; o >>= 1) bf = merge_best(bf, shfl_best(bf, o));
+      if (lane == 0) s_best[0] = bf;
+    }
+    __syncthreads();
+    bf = s_best[0];
+    const double margin32 = 4.0 * (double)(nnz + 3) * 5.9604644775390625e-08;
+    if ((bf.v2 - bf.v1) > margin32 * bf.v2) {
+      if (tid == 0) newc[kk * mp + mm] = (uint8_t)bf.l1;
+      return;
+    }
+    if (tid == 0) atomicAdd(&acc[3], 1ull);
+    __syncthreads();  // s_best is reused below
+  }
   const double* tm = t64 + (size_t)mm * l * l;
-  double v = __longlong_as_double(0x7ff0000000000000LL);
+  double v = inf;
   if (tid < l) {
     v = 0.0;
     for (int j = 0; j < nnz; ++j) v = __fma_rn(s_h[j], __ldg(&tm[(size_t)s_s[j] * l + tid]), v);
@@ -235,6 +272,7 @@ __global__ void vote_stats_kernel(int64_t k, const unsigned long long* __restric
   stats[PQK_STAT_VOTE_EXACT] = (int64_t)acc[1];
   stats[PQK_STAT_EMPTY] = (int64_t)acc[2];
   stats[PQK_STAT_FILLED] = k - (int64_t)acc[2];
+  stats[PQK_STAT_VOTE_FP64] = (int64_t)acc[3];
 }
 
 // ---------------------------------------------------------------------------
@@ -411,15 +449,49 @@ __device__ __forceinline__ void leaf_pairwise(const double* __restrict__ a, int 
   res = s;
 }
 
-__global__ void obj_leaf_kernel(const double* __restrict__ sd, int64_t nleaves, const int64_t* __restrict__ leaf_off,
-                                const int32_t* __restrict__ leaf_len, double2* __restrict__ leafval) {
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nleaves; t += (int64_t)gridDim.x * blockDim.x) {
-    const double* a = sd + leaf_off[t];
-    const int n = leaf_len[t];
-    double s1, s2;
-    leaf_pairwise(a, n, true, s1);
-    leaf_pairwise(a, n, false, s2);
-    leafval[t] = make_double2(s1, s2);
+// Eight lanes per leaf: lane j owns numpy's accumulator r[j] (elements 8i+j), the
+// three shuffle levels add ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)), lane 0 adds the
+// n%8 tail sequentially; leaves shorter than 8 are summed sequentially from 0.0.
+__global__ void obj_leaf8_kernel(const double* __restrict__ sd, int64_t nleaves, const int64_t* __restrict__ leaf_off,
+                                 const int32_t* __restrict__ leaf_len, double2* __restrict__ leafval) {
+  const int lane = threadIdx.x & 31, grp = lane >> 3, j = lane & 7;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t t0 = warp * 4; t0 < nleaves; t0 += nwarps * 4) {
+    const int64_t t = t0 + grp;
+    const bool valid = t < nleaves;
+    const int n = valid ? leaf_len[t] : 0;
+    const double* a = sd + (valid ? leaf_off[t] : 0);
+    double r1 = 0.0, r2 = 0.0;
+    const int nb = n - (n % 8);
+    if (n >= 8) {
+      r2 = a[j];
+      r1 = __dsqrt_rn(r2);
+      for (int i = 8; i < nb; i += 8) {
+        const double x = a[i + j];
+        r2 = __dadd_rn(r2, x);
+        r1 = __dadd_rn(r1, __dsqrt_rn(x));
+      }
+    }
+#pragma unroll
+    for (int o = 1; o < 8; o <<= 1) {
+      const double y1 = __shfl_xor_sync(0xffffffffu, r1, o);
+      const double y2 = __shfl_xor_sync(0xffffffffu, r2, o);
+      r1 = __dadd_rn(r1, y1);
+      r2 = __dadd_rn(r2, y2);
+    }
+    if (valid && j == 0) {
+      if (n < 8) {
+        r1 = 0.0;
+        r2 = 0.0;
+      }
+      for (int i = (n < 8 ? 0 : nb); i < n; ++i) {
+        const double x = a[i];
+        r2 = __dadd_rn(r2, x);
+        r1 = __dadd_rn(r1, __dsqrt_rn(x));
+      }
+      leafval[t] = make_double2(r1, r2);
+    }
   }
 }
 
@@ -441,9 +513,37 @@ __global__ void obj_level_kernel(int64_t start, int64_t count, int64_t child_sta
   }
 }
 
-__global__ void obj_out_kernel(const double2* __restrict__ nodeval, double* __restrict__ out2) {
-  out2[0] = nodeval[0].x;
-  out2[1] = nodeval[0].y;
+struct DepthStarts {
+  long long v[64];
+};
+
+// All remaining (small) levels, deepest first, in one CTA; writes the root sums.
+__global__ void __launch_bounds__(1024) obj_levels_tail_kernel(int top_depth, DepthStarts ds,
+                                                               const int32_t* __restrict__ na,
+                                                               const int32_t* __restrict__ nb,
+                                                               const double2* __restrict__ leafval,
+                                                               double2* __restrict__ nodeval, double* __restrict__ out2) {
+  for (int d = top_depth; d >= 0; --d) {
+    const int64_t start = ds.v[d], count = ds.v[d + 1] - ds.v[d], child = ds.v[d + 1];
+    for (int64_t t = threadIdx.x; t < count; t += blockDim.x) {
+      const int64_t id = start + t;
+      const int a = na[id], b = nb[id];
+      double2 r;
+      if (b < 0) {
+        r = leafval[a];
+      } else {
+        const double2 x = nodeval[child + a];
+        const double2 y = nodeval[child + b];
+        r = make_double2(__dadd_rn(x.x, y.x), __dadd_rn(x.y, y.y));
+      }
+      nodeval[id] = r;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    out2[0] = nodeval[0].x;
+    out2[1] = nodeval[0].y;
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -534,17 +634,18 @@ extern "C" int pqk_histogram_device(const uint8_t* d_codes, int64_t n, int32_t m
   return PQK_OK;
 }
 
-// d_stats has PQK_STATS_LEN slots: 0..7 public, 8..15 scratch accumulators of the vote.
+// d_stats has PQK_STATS_LEN slots: 0..15 public, 16..19 scratch accumulators of the vote.
 extern "C" int pqk_vote_device(const int32_t* d_hist, const int32_t* d_counts, int64_t k, int32_t m, int32_t l,
-                               const double* d_t64, uint8_t* d_new_centers, int64_t* d_stats, void* stream_) {
+                               const double* d_t64, const float* d_t32, uint8_t* d_new_centers, int64_t* d_stats,
+                               void* stream_) {
   cudaStream_t stream = (cudaStream_t)stream_;
   const int mp = padded_m(m);
   if (mp == 0 || l < 2 || l > kMaxL || k < 1 || !d_stats) return fail(PQK_EINVAL, "pqk_vote_device: bad arguments");
   if ((int64_t)k * m >= ((int64_t)1 << 31)) return fail(PQK_EUNSUPPORTED, "pqk_vote_device: k*m too large");
-  unsigned long long* acc = reinterpret_cast<unsigned long long*>(d_stats + 8);
+  unsigned long long* acc = reinterpret_cast<unsigned long long*>(d_stats + 16);
   PQK_CUDA_TRY(cudaMemsetAsync(acc, 0, 4 * sizeof(unsigned long long), stream));
   PQK_CUDA_TRY(cudaMemsetAsync(d_new_centers, 0, (size_t)k * mp, stream));
-  vote_kernel<<<(unsigned)(k * m), 256, 0, stream>>>(d_hist, d_counts, k, m, l, mp, d_t64, d_new_centers, acc);
+  vote_kernel<<<(unsigned)(k * m), 256, 0, stream>>>(d_hist, d_counts, k, m, l, mp, d_t64, d_t32, d_new_centers, acc);
   PQK_LAUNCH_CHECK("vote_kernel");
   empties_kernel<<<(unsigned)((k + 1023) / 1024), 1024, 0, stream>>>(d_counts, k, acc);
   PQK_LAUNCH_CHECK("empties_kernel");
@@ -616,20 +717,26 @@ extern "C" int pqk_objective_device(const double* d_sd_sq, int64_t n, int64_t nl
   double2* nodeval = reinterpret_cast<double2*>(static_cast<char*>(d_ws) +
                                                 align_up((size_t)nleaves * sizeof(double2), 256));
   const DevInfo& di = dev_info();
+  if (ndepth > 63) return fail(PQK_EUNSUPPORTED, "pqk_objective_device: tree too deep");
   {
-    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((nleaves + 127) / 128, (int64_t)di.sms * 8));
-    obj_leaf_kernel<<<grid, 128, 0, stream>>>(d_sd_sq, nleaves, d_leaf_off, d_leaf_len, leafval);
-    PQK_LAUNCH_CHECK("obj_leaf_kernel");
+    const int64_t warps = (nleaves + 3) / 4;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((warps * 32 + 255) / 256, (int64_t)di.sms * 16));
+    obj_leaf8_kernel<<<grid, 256, 0, stream>>>(d_sd_sq, nleaves, d_leaf_off, d_leaf_len, leafval);
+    PQK_LAUNCH_CHECK("obj_leaf8_kernel");
   }
-  for (int d = ndepth - 1; d >= 0; --d) {
+  int d = ndepth - 1;
+  for (; d >= 0; --d) {
     const int64_t start = h_depth_start[d];
     const int64_t count = h_depth_start[d + 1] - start;
+    if (count <= 4096) break;
     const int64_t child = h_depth_start[d + 1];
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((count + 255) / 256, (int64_t)di.sms * 8));
     obj_level_kernel<<<grid, 256, 0, stream>>>(start, count, child, d_node_a, d_node_b, leafval, nodeval);
     PQK_LAUNCH_CHECK("obj_level_kernel");
   }
-  obj_out_kernel<<<1, 1, 0, stream>>>(nodeval, d_out2);
-  PQK_LAUNCH_CHECK("obj_out_kernel");
+  DepthStarts ds{};
+  for (int i = 0; i <= ndepth; ++i) ds.v[i] = h_depth_start[i];
+  obj_levels_tail_kernel<<<1, 1024, 0, stream>>>(d, ds, d_node_a, d_node_b, leafval, nodeval, d_out2);
+  PQK_LAUNCH_CHECK("obj_levels_tail_kernel");
   return PQK_OK;
 }

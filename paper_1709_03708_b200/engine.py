@@ -289,6 +289,7 @@ class ShardEngine:
             t.m,
             t.l,
             _ptr(t.t64),
+            _ptr(None if t.fp64_only else t.t32),
             _ptr(self.new_centers),
             _ptr(self.stats),
             _stream(self.dev),
@@ -333,6 +334,16 @@ class ShardEngine:
         return keys[:e_eff], index[:e_eff]
 
     # -- host reads ---------------------------------------------------------------
+    def read_obj_stats(self) -> tuple[np.ndarray, np.ndarray]:
+        """Objective sums and stats with two async D2H copies and one stream sync."""
+        if not hasattr(self, "_pin_obj"):
+            self._pin_obj = torch.empty(2, dtype=torch.float64).pin_memory()
+            self._pin_stats = torch.empty(STATS_LEN, dtype=torch.int64).pin_memory()
+        self._pin_obj.copy_(self.obj, non_blocking=True)
+        self._pin_stats.copy_(self.stats, non_blocking=True)
+        torch.cuda.current_stream(self.dev).synchronize()
+        return self._pin_obj.numpy().copy(), self._pin_stats.numpy().copy()
+
     def stats_host(self) -> np.ndarray:
         return self.stats.cpu().numpy()
 
@@ -395,8 +406,8 @@ def vote_host(hist: np.ndarray, tables: np.ndarray, *, device=None) -> np.ndarra
         counts = torch.from_numpy(hist[:, 0, :].sum(axis=1).astype(np.int32)).to(dev)
         out = torch.zeros((k, dt.mp), dtype=torch.uint8, device=dev)
         stats = torch.zeros(STATS_LEN, dtype=torch.int64, device=dev)
-        call("pqk_vote_device", _ptr(h), _ptr(counts), k, dt.m, dt.l, _ptr(dt.t64), _ptr(out), _ptr(stats),
-             _stream(dev))
+        call("pqk_vote_device", _ptr(h), _ptr(counts), k, dt.m, dt.l, _ptr(dt.t64),
+             _ptr(None if dt.fp64_only else dt.t32), _ptr(out), _ptr(stats), _stream(dev))
         return download_codes(out, dt.m)
 
 

@@ -88,120 +88,118 @@ __device__ __forceinline__ bool dd_less(const DD& a, const DD& b) {
   return a.l < b.l;
 }
 
-__global__ void __launch_bounds__(256) vote_kernel(const int32_t* __restrict__ hist, const int32_t* __restrict__ counts,
-                                                   int64_t k, int m, int l, int mp, const double* __restrict__ t64,
-                                                   const float* __restrict__ t32, uint8_t* __restrict__ newc,
-                                                   unsigned long long* __restrict__ acc) {
-  __shared__ int s_s[kMaxL];
-  __shared__ double s_h[kMaxL];
-  __shared__ int s_wc[8];
-  __shared__ Best s_best[8];
-  __shared__ DD s_dd[8];
-  // m-major block order: concurrently running blocks share one subspace table
-  const int mm = (int)(blockIdx.x / k);
-  const int64_t kk = blockIdx.x - (int64_t)mm * k;
-  if (counts[kk] == 0) return;  // empty: left 0, repaired later
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int hv = (tid < l) ? hist[(kk * m + mm) * l + tid] : 0;
-  const unsigned bal = __ballot_sync(0xffffffffu, hv != 0);
-  if (lane == 0) s_wc[warp] = __popc(bal);
-  __syncthreads();
-  int off = 0, nnz = 0;
-#pragma unroll
-  for (int w = 0; w < 8; ++w) {
-    off += (w < warp) ? s_wc[w] : 0;
-    nnz += s_wc[w];
-  }
-  if (hv != 0) {
-    const int pos = off + __popc(bal & ((1u << lane) - 1u));
-    s_s[pos] = tid;
-    s_h[pos] = (double)hv;
-  }
-  if (tid == 0) atomicAdd(&acc[0], (unsigned long long)nnz);
-  __syncthreads();
-  const double inf = __longlong_as_double(0x7ff0000000000000LL);
-  if (t32) {
-    // fp32 filter: every term h*t >= 0 carries relative error <= 2u (count and table
-    // conversion) plus one FMA rounding, so a gap above 4(nnz+3)u32 proves the
-    // exact-arithmetic argmin.
-    const float* tf = t32 + (size_t)mm * l * l;
-    float vf = __int_as_float(0x7f800000);
-    if (tid < l) {
-      // 8 independent partial sums keep 8 table loads in flight per thread
-      float part[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-      int j = 0;
-      for (; j + 8 <= nnz; j += 8) {
-#pragma unroll
-        for (int q = 0; q < 8; ++q)
-          part[q] = __fmaf_rn((float)s_h[j + q], __ldg(&tf[(size_t)s_s[j + q] * l + tid]), part[q]);
-      }
-      for (int q = 0; j < nnz; ++j, ++q) part[q] = __fmaf_rn((float)s_h[j], __ldg(&tf[(size_t)s_s[j] * l + tid]), part[q]);
-      vf = ((part[0] + part[1]) + (part[2] + part[3])) + ((part[4] + part[5]) + (part[6] + part[7]));
-    }
-    Best bf{(double)vf, tid, inf};
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) bf = merge_best(bf, shfl_best(bf, o));
-    if (lane == 0) s_best[warp] = bf;
-    __syncthreads();
-    if (warp == 0) {
-      bf = s_best[lane & 7];
-#pragma unroll
-      for (int o = 4; o > 0; o >>= 1) bf = merge_best(bf, shfl_best(bf, o));
-      if (lane == 0) s_best[0] = bf;
-    }
-    __syncthreads();
-    bf = s_best[0];
-    const double margin32 = 4.0 * (double)(nnz + 3) * 5.9604644775390625e-08;
-    if ((bf.v2 - bf.v1) > margin32 * bf.v2) {
-      if (tid == 0) newc[kk * mp + mm] = (uint8_t)bf.l1;
-      return;
-    }
-    if (tid == 0) atomicAdd(&acc[3], 1ull);
-    __syncthreads();  // s_best is reused below
-  }
-  const double* tm = t64 + (size_t)mm * l * l;
-  double v = inf;
-  if (tid < l) {
-    v = 0.0;
-    for (int j = 0; j < nnz; ++j) v = __fma_rn(s_h[j], __ldg(&tm[(size_t)s_s[j] * l + tid]), v);
-  }
-  Best b{v, tid, __longlong_as_double(0x7ff0000000000000LL)};
+// One warp per (filled cluster k, subspace m), m-major so that concurrently running
+// warps share one subspace table.  Lane q owns candidates j = lane + 32*i (i < 8).
+// Stage 1 (fp32, table t32): every term h*t >= 0 carries relative error <= 2u (count
+// and table conversion) plus one FMA rounding, so a top-2 gap above 4(nnz+3)u32
+// proves the exact-arithmetic argmin.  Stage 2 (fp64): any summation order of the
+// nnz products is within (nnz+1)u of the exact sum, a gap above 4(nnz+2)u proves it.
+// Stage 3 (double-double): near ties; values within 2^-100 relative tie -> lowest j.
+constexpr int kVoteWarps = 8;
+
+__device__ __forceinline__ void warp_best(Best& b) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) b = merge_best(b, shfl_best(b, o));
-  if (lane == 0) s_best[warp] = b;
-  __syncthreads();
-  if (warp == 0) {
-    b = s_best[lane & 7];
-#pragma unroll
-    for (int o = 4; o > 0; o >>= 1) b = merge_best(b, shfl_best(b, o));
-    if (lane == 0) s_best[0] = b;
+}
+
+__global__ void __launch_bounds__(32 * kVoteWarps) vote_kernel(const int32_t* __restrict__ hist,
+                                                               const int32_t* __restrict__ counts, int64_t k, int m,
+                                                               int l, int mp, const double* __restrict__ t64,
+                                                               const float* __restrict__ t32,
+                                                               uint8_t* __restrict__ newc,
+                                                               unsigned long long* __restrict__ acc) {
+  __shared__ int s_s[kVoteWarps][kMaxL];
+  __shared__ int s_h[kVoteWarps][kMaxL];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t gw = (int64_t)blockIdx.x * kVoteWarps + warp;
+  if (gw >= k * m) return;
+  const int mm = (int)(gw / k);
+  const int64_t kk = gw - (int64_t)mm * k;
+  if (counts[kk] == 0) return;  // empty: left 0, repaired later
+  int* ss = s_s[warp];
+  int* sh = s_h[warp];
+  const int32_t* hrow = hist + (kk * m + mm) * l;
+  int nnz = 0;
+  for (int base = 0; base < l; base += 32) {
+    const int s = base + lane;
+    const int h = (s < l) ? hrow[s] : 0;
+    const unsigned bal = __ballot_sync(0xffffffffu, h != 0);
+    if (h) {
+      const int pos = nnz + __popc(bal & ((1u << lane) - 1u));
+      ss[pos] = s;
+      sh[pos] = h;
+    }
+    nnz += __popc(bal);
   }
-  __syncthreads();
-  b = s_best[0];
-  // Any summation order of nnz nonnegative products is within (nnz+1)u of the exact
-  // sum; a relative gap above 4(nnz+2)u proves the exact (and the reference's) argmin.
-  const double margin = 4.0 * (double)(nnz + 2) * ldexp(1.0, -53);
-  const bool cert = (b.v2 - b.v1) > margin * b.v2;
-  if (cert) {
-    if (tid == 0) newc[kk * mp + mm] = (uint8_t)b.l1;
-    return;
+  __syncwarp();
+  if (lane == 0) atomicAdd(&acc[0], (unsigned long long)nnz);
+  const double inf = __longlong_as_double(0x7ff0000000000000LL);
+  if (t32) {
+    const float* tf = t32 + (size_t)mm * l * l;
+    float v[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = 0.0f;
+    for (int j = 0; j < nnz; ++j) {
+      const float h = (float)sh[j];
+      const float* row = tf + (size_t)ss[j] * l;
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        if (lane + 32 * i < l) v[i] = __fmaf_rn(h, __ldg(&row[lane + 32 * i]), v[i]);
+    }
+    Best b{inf, 0, inf};
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      if (lane + 32 * i < l) b = merge_best(b, Best{(double)v[i], lane + 32 * i, inf});
+    warp_best(b);
+    const double margin32 = 4.0 * (double)(nnz + 3) * 5.9604644775390625e-08;
+    if ((b.v2 - b.v1) > margin32 * b.v2) {
+      if (lane == 0) newc[kk * mp + mm] = (uint8_t)b.l1;
+      return;
+    }
+    if (lane == 0) atomicAdd(&acc[3], 1ull);
+  }
+  const double* td = t64 + (size_t)mm * l * l;
+  {
+    double v[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = 0.0;
+    for (int j = 0; j < nnz; ++j) {
+      const double h = (double)sh[j];
+      const double* row = td + (size_t)ss[j] * l;
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        if (lane + 32 * i < l) v[i] = __fma_rn(h, __ldg(&row[lane + 32 * i]), v[i]);
+    }
+    Best b{inf, 0, inf};
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      if (lane + 32 * i < l) b = merge_best(b, Best{v[i], lane + 32 * i, inf});
+    warp_best(b);
+    const double margin = 4.0 * (double)(nnz + 2) * ldexp(1.0, -53);
+    if ((b.v2 - b.v1) > margin * b.v2) {
+      if (lane == 0) newc[kk * mp + mm] = (uint8_t)b.l1;
+      return;
+    }
   }
   // near tie: double-double sums (exact products via FMA, compensated additions)
-  DD d{__longlong_as_double(0x7ff0000000000000LL), 0.0, tid};
-  if (tid < l) {
+  DD d{inf, 0.0, 0x7fffffff};
+  for (int i = 0; i < 8; ++i) {
+    const int c = lane + 32 * i;
+    if (c >= l) break;
     double hi = 0.0, lo = 0.0;
     for (int j = 0; j < nnz; ++j) {
-      const double t = __ldg(&tm[(size_t)s_s[j] * l + tid]);
-      const double p = __dmul_rn(s_h[j], t);
-      const double pe = __fma_rn(s_h[j], t, -p);
+      const double h = (double)sh[j];
+      const double t = __ldg(&td[(size_t)ss[j] * l + c]);
+      const double p = __dmul_rn(h, t);
+      const double pe = __fma_rn(h, t, -p);
       double s, e;
       two_sum(hi, p, s, e);
       e = __dadd_rn(e, __dadd_rn(lo, pe));
       hi = __dadd_rn(s, e);
       lo = __dsub_rn(e, __dsub_rn(hi, s));
     }
-    d.hi = hi;
-    d.lo = lo;
+    const DD cand{hi, lo, c};
+    if (dd_less(cand, d)) d = cand;
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -211,13 +209,8 @@ __global__ void __launch_bounds__(256) vote_kernel(const int32_t* __restrict__ h
     od.l = __shfl_xor_sync(0xffffffffu, d.l, o);
     if (dd_less(od, d)) d = od;
   }
-  if (lane == 0) s_dd[warp] = d;
-  __syncthreads();
-  if (tid == 0) {
-    DD w = s_dd[0];
-    for (int i = 1; i < 8; ++i)
-      if (dd_less(s_dd[i], w)) w = s_dd[i];
-    newc[kk * mp + mm] = (uint8_t)w.l;
+  if (lane == 0) {
+    newc[kk * mp + mm] = (uint8_t)d.l;
     atomicAdd(&acc[1], 1ull);
   }
 }
@@ -645,7 +638,8 @@ extern "C" int pqk_vote_device(const int32_t* d_hist, const int32_t* d_counts, i
   unsigned long long* acc = reinterpret_cast<unsigned long long*>(d_stats + 16);
   PQK_CUDA_TRY(cudaMemsetAsync(acc, 0, 4 * sizeof(unsigned long long), stream));
   PQK_CUDA_TRY(cudaMemsetAsync(d_new_centers, 0, (size_t)k * mp, stream));
-  vote_kernel<<<(unsigned)(k * m), 256, 0, stream>>>(d_hist, d_counts, k, m, l, mp, d_t64, d_t32, d_new_centers, acc);
+  vote_kernel<<<(unsigned)((k * m + kVoteWarps - 1) / kVoteWarps), 32 * kVoteWarps, 0, stream>>>(
+      d_hist, d_counts, k, m, l, mp, d_t64, d_t32, d_new_centers, acc);
   PQK_LAUNCH_CHECK("vote_kernel");
   empties_kernel<<<(unsigned)((k + 1023) / 1024), 1024, 0, stream>>>(d_counts, k, acc);
   PQK_LAUNCH_CHECK("empties_kernel");

@@ -35,6 +35,9 @@ CONFIGS = {
     # name: (n_per_gpu, k, m, l, dim)
     "c2": dict(n=1_000_000, k=10_000, m=4, l=256, dim=128, workload="config2 SIFT-like N=1e6/GPU K=1e4 M=4 L=256"),
     "c1": dict(n=100_000, k=1_000, m=4, l=256, dim=128, workload="config1 mixture N=1e5 K=1e3 M=4 L=256"),
+    # config 4's per-GPU shard at 8 GPUs: 1e9/8 SIFT-like codes, K=1e5 (chunked tables stream from HBM)
+    "c4": dict(n=125_000_000, k=100_000, m=4, l=256, dim=128, gpu_data=True,
+               workload="config4 shard SIFT-like N=1.25e8/GPU K=1e5 M=4 L=256"),
 }
 SEED = 20260419
 
@@ -51,6 +54,18 @@ def make_vectors(cfg_name: str, n: int, rank: int) -> np.ndarray:
     if cfg_name == "c1":
         return synth.mixture(n, 128, 1000, synth.stage_seed(SEED, 100 + rank))
     return synth.sift_like(n, synth.stage_seed(SEED, 100 + rank))
+
+
+def sift_like_gpu(n: int, seed: int, dev, dim: int = 128, blocks: int = 8):
+    """Device-side SIFT-like generator (config 4 chunks), same recipe as synth.sift_like."""
+    import torch
+
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(seed)
+    alpha = torch.full((n, blocks, dim // blocks), 0.6, dtype=torch.float32, device=dev)
+    g = torch._standard_gamma(alpha, generator=gen) * 30.0
+    g = g * (512.0 / g.norm(dim=2, keepdim=True).clamp_min(1e-12))
+    return g.round_().clamp_(0, 255).reshape(n, dim).contiguous()
 
 
 def make_codebook(cfg_name: str, m: int, l_count: int) -> np.ndarray:
@@ -229,14 +244,37 @@ def main() -> None:
     t0 = time.perf_counter()
     book = make_codebook(cfgn, m, l_count)
     tables = build_distance_tables(PQCodebook(book)).tables
-    vectors = make_vectors(cfgn, n_loc, rank)
+    mp = _lib.padded_m(m)
+    enc_ms = 0.0
     with torch.cuda.device(dev):
         stats_enc = torch.zeros(_lib.STATS_LEN, dtype=torch.int64, device=dev)
-        vec_dev = torch.from_numpy(vectors).to(dev)
-        cw_dev = torch.from_numpy(book).to(dev)
-        codes_dev = engine.encode_device(vec_dev, cw_dev, m, l_count, dev, stride=_lib.padded_m(m), stats=stats_enc)
-        del vec_dev
+        cw_dev = torch.from_numpy(np.array(book)).to(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if cfg.get("gpu_data"):
+            # billion-scale shard: vectors generated on device per seeded chunk, encoded in place
+            codes_dev = torch.empty((n_loc, mp), dtype=torch.uint8, device=dev)
+            chunk = 1 << 20
+            for s in range(0, n_loc, chunk):
+                e = min(n_loc, s + chunk)
+                vec = sift_like_gpu(e - s, synth.stage_seed(SEED, 1000 + rank * 100_000 + s // chunk), dev)
+                e0.record()
+                codes_dev[s:e] = engine.encode_device(vec, cw_dev, m, l_count, dev, stride=mp, stats=stats_enc)
+                e1.record()
+                torch.cuda.synchronize(dev)
+                enc_ms += e0.elapsed_time(e1)
+                del vec
+        else:
+            vectors = make_vectors(cfgn, n_loc, rank)
+            vec_dev = torch.from_numpy(vectors).to(dev)
+            e0.record()
+            codes_dev = engine.encode_device(vec_dev, cw_dev, m, l_count, dev, stride=mp, stats=stats_enc)
+            e1.record()
+            torch.cuda.synchronize(dev)
+            enc_ms = e0.elapsed_time(e1)
+            del vec_dev
         codes_host = engine.download_codes(codes_dev, m)
+        enc_flagged = int(stats_enc[_lib.STAT_ENCODE_FLAGGED].item())
+        del codes_dev
     log(f"[bench] rank {rank}: workload ready in {time.perf_counter() - t0:.1f}s")
 
     offset, length = shard_bounds(n_total, world, rank)
@@ -357,6 +395,17 @@ def main() -> None:
         "clocks": clk,
         "gpu_launches": int(launches),
     }
+    # PQ encoder (set-up of the workload, timed with events): HBM roofline of code streaming
+    enc_bytes = n_loc * (4 * cfg["dim"] + m)
+    hbm_peak = 6545.3
+    try:
+        hbm_peak = float(json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"])
+    except Exception:
+        pass
+    out["encode"] = {"vectors": n_loc, "ms": enc_ms, "vectors_per_s": n_loc / (enc_ms / 1e3),
+                     "hbm_gbs": enc_bytes / (enc_ms / 1e3) / 1e9,
+                     "hbm_frac": enc_bytes / (enc_ms / 1e3) / 1e9 / hbm_peak,
+                     "flagged_pairs": enc_flagged, "kernel": "encode_kernel (SIMT fp32 filter + fp64 certificate)"}
 
     # ---- e2e through the C-ABI host entry (host buffers, H2D/D2H inside) ------------
     if not args.no_e2e and world == 1:

@@ -73,6 +73,10 @@ struct HostCtx {
   };
   Buf raw, codes, centers_raw, centers, t64, t32, labels, sd, ws, stats, hist, counts, newc, rws, vec, cw, obj, objws,
       plan;
+  // cached numpy-summation plan for the last n (uploaded into `plan`)
+  int64_t plan_n = -1, plan_nleaves = 0, plan_nnodes = 0;
+  size_t plan_o_len = 0, plan_o_na = 0, plan_o_nb = 0;
+  std::vector<int64_t> plan_depth_start;
 };
 
 static HostCtx g_ctx[64];
@@ -132,6 +136,7 @@ static int upload_codes(HostCtx* c, HostCtx::Buf& rawb, HostCtx::Buf& dst, const
 }
 
 static bool validate_codes_host(const uint8_t* codes, int64_t n, int m, int l) {
+  if (l >= 256) return true;  // every uint8 is a valid subindex
   const size_t cnt = (size_t)n * m;
   for (size_t i = 0; i < cnt; ++i)
     if (codes[i] >= l) return false;
@@ -168,13 +173,16 @@ extern "C" int pqk_device_info(int32_t device, int32_t* sm_count, int32_t* smem_
 
 extern "C" int pqk_table_scale(const double* t, int64_t count, int32_t* exp2_out, int32_t* fp64_only_out) {
   if (!t || count < 0 || !exp2_out || !fp64_only_out) return fail(PQK_EINVAL, "pqk_table_scale: bad arguments");
+  // branch-free reduction (vectorises): bad counts NaN / negative / infinite entries
   double mx = 0.0, mn = INFINITY;
+  int64_t bad = 0;
   for (int64_t i = 0; i < count; ++i) {
     const double v = t[i];
-    if (!(v >= 0.0) || std::isinf(v)) return fail(PQK_EINVAL, "table entries must be finite and non-negative");
-    if (v > mx) mx = v;
-    if (v > 0.0 && v < mn) mn = v;
+    bad += !(v >= 0.0 && v <= 1.7976931348623157e308);
+    mx = v > mx ? v : mx;
+    mn = (v > 0.0 && v < mn) ? v : mn;
   }
+  if (bad) return fail(PQK_EINVAL, "table entries must be finite and non-negative");
   *exp2_out = 0;
   *fp64_only_out = 0;
   if (mx == 0.0) return PQK_OK;
@@ -313,22 +321,35 @@ extern "C" int pqk_lloyd_step_host(const uint8_t* codes, int64_t n, int32_t m, c
   PQK_TRY(ensure(c->newc, (size_t)k * mp));
   const size_t rwsb = pqk_repair_workspace_bytes(n, k);
   PQK_TRY(ensure(c->rws, rwsb));
-  // objective plan
-  int64_t nleaves = 0, nnodes = 0;
-  int32_t ndepth = 0;
-  PQK_TRY(pqk_pairwise_plan_size(n, &nleaves, &ndepth, &nnodes));
-  std::vector<int64_t> leaf_off(nleaves), depth_start(ndepth + 1);
-  std::vector<int32_t> leaf_len(nleaves), na(nnodes), nb(nnodes);
-  PQK_TRY(pqk_pairwise_plan_build(n, leaf_off.data(), leaf_len.data(), depth_start.data(), na.data(), nb.data()));
-  const size_t o_len = align_up(nleaves * sizeof(int64_t), 256);
-  const size_t o_na = o_len + align_up(nleaves * sizeof(int32_t), 256);
-  const size_t o_nb = o_na + align_up(nnodes * sizeof(int32_t), 256);
-  PQK_TRY(ensure(c->plan, o_nb + nnodes * sizeof(int32_t)));
+  // objective plan (depends on n only; built and uploaded once per n)
+  if (c->plan_n != n) {
+    int64_t nl = 0, nn = 0;
+    int32_t nd = 0;
+    PQK_TRY(pqk_pairwise_plan_size(n, &nl, &nd, &nn));
+    std::vector<int64_t> leaf_off(nl), depth_start(nd + 1);
+    std::vector<int32_t> leaf_len(nl), na(nn), nb(nn);
+    PQK_TRY(pqk_pairwise_plan_build(n, leaf_off.data(), leaf_len.data(), depth_start.data(), na.data(), nb.data()));
+    c->plan_o_len = align_up(nl * sizeof(int64_t), 256);
+    c->plan_o_na = c->plan_o_len + align_up(nl * sizeof(int32_t), 256);
+    c->plan_o_nb = c->plan_o_na + align_up(nn * sizeof(int32_t), 256);
+    PQK_TRY(ensure(c->plan, c->plan_o_nb + nn * sizeof(int32_t)));
+    char* p = (char*)c->plan.p;
+    PQK_CUDA_TRY(cudaMemcpyAsync(p, leaf_off.data(), nl * sizeof(int64_t), cudaMemcpyHostToDevice, c->stream));
+    PQK_CUDA_TRY(cudaMemcpyAsync(p + c->plan_o_len, leaf_len.data(), nl * sizeof(int32_t), cudaMemcpyHostToDevice,
+                                 c->stream));
+    PQK_CUDA_TRY(cudaMemcpyAsync(p + c->plan_o_na, na.data(), nn * sizeof(int32_t), cudaMemcpyHostToDevice, c->stream));
+    PQK_CUDA_TRY(cudaMemcpyAsync(p + c->plan_o_nb, nb.data(), nn * sizeof(int32_t), cudaMemcpyHostToDevice, c->stream));
+    PQK_CUDA_TRY(cudaStreamSynchronize(c->stream));  // host vectors go out of scope
+    c->plan_n = n;
+    c->plan_nleaves = nl;
+    c->plan_nnodes = nn;
+    c->plan_depth_start = depth_start;
+  }
+  const int64_t nleaves = c->plan_nleaves, nnodes = c->plan_nnodes;
+  const int32_t ndepth = (int32_t)c->plan_depth_start.size() - 1;
+  const int64_t* depth_start_h = c->plan_depth_start.data();
   char* pb = (char*)c->plan.p;
-  PQK_CUDA_TRY(cudaMemcpyAsync(pb, leaf_off.data(), nleaves * sizeof(int64_t), cudaMemcpyHostToDevice, c->stream));
-  PQK_CUDA_TRY(cudaMemcpyAsync(pb + o_len, leaf_len.data(), nleaves * sizeof(int32_t), cudaMemcpyHostToDevice, c->stream));
-  PQK_CUDA_TRY(cudaMemcpyAsync(pb + o_na, na.data(), nnodes * sizeof(int32_t), cudaMemcpyHostToDevice, c->stream));
-  PQK_CUDA_TRY(cudaMemcpyAsync(pb + o_nb, nb.data(), nnodes * sizeof(int32_t), cudaMemcpyHostToDevice, c->stream));
+  const size_t o_len = c->plan_o_len, o_na = c->plan_o_na, o_nb = c->plan_o_nb;
   const size_t owsb = pqk_objective_workspace_bytes(nleaves, nnodes);
   PQK_TRY(ensure(c->objws, owsb));
   PQK_TRY(ensure(c->obj, 2 * sizeof(double)));
@@ -339,7 +360,7 @@ extern "C" int pqk_lloyd_step_host(const uint8_t* codes, int64_t n, int32_t m, c
                             (const double*)c->t64.p, (const float*)c->t32.p, fp64_only, c->ws.p, wsb,
                             (uint32_t*)c->labels.p, (double*)c->sd.p, dstats, c->stream));
   PQK_TRY(pqk_objective_device((const double*)c->sd.p, n, nleaves, ndepth, (const int64_t*)pb,
-                               (const int32_t*)(pb + o_len), depth_start.data(), (const int32_t*)(pb + o_na),
+                               (const int32_t*)(pb + o_len), depth_start_h, (const int32_t*)(pb + o_na),
                                (const int32_t*)(pb + o_nb), c->objws.p, owsb, (double*)c->obj.p, c->stream));
   PQK_TRY(pqk_histogram_device((const uint8_t*)c->codes.p, n, m, l, (const uint32_t*)c->labels.p, k,
                                (int32_t*)c->hist.p, (int32_t*)c->counts.p, c->stream));
@@ -385,5 +406,7 @@ extern "C" int pqk_host_release(int32_t device) {
   cudaStreamDestroy(c.stream);
   c.stream = nullptr;
   c.init = false;
+  c.plan_n = -1;
+  c.plan_depth_start.clear();
   return PQK_OK;
 }

@@ -253,7 +253,7 @@ def main() -> None:
         if cfg.get("gpu_data"):
             # billion-scale shard: vectors generated on device per seeded chunk, encoded in place
             codes_dev = torch.empty((n_loc, mp), dtype=torch.uint8, device=dev)
-            chunk = 1 << 20
+            chunk = 1 << 23  # 8 Mi vectors (4 GiB fp32) per encode call
             for s in range(0, n_loc, chunk):
                 e = min(n_loc, s + chunk)
                 vec = sift_like_gpu(e - s, synth.stage_seed(SEED, 1000 + rank * 100_000 + s // chunk), dev)

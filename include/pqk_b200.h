@@ -171,6 +171,11 @@ int pqk_lloyd_step_host(const uint8_t* codes, int64_t n, int32_t m, const uint8_
 /* Release the cached per-device context of the host entry points. */
 int pqk_host_release(int32_t device);
 
+/* ---- diagnostics -------------------------------------------------------------- */
+/* tcgen05 self-test: C (128 x 256, fp32) = A (128 x k, fp16, row-major) * B (256 x k,
+ * fp16, row-major)^T through UMMA descriptors, TMEM and tcgen05.ld (k % 16 == 0). */
+int pqk_tc_selftest(const void* d_a_f16, const void* d_b_f16, float* d_c, int32_t k, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

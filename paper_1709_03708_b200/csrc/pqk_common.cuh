@@ -92,7 +92,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred p;\n"
       "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 10000000;\n\t"  // suspend-time hint (ns)
       "@!p bra WAIT_%=;\n\t}" ::"r"(addr),
       "r"(parity)
       : "memory");
@@ -117,6 +117,13 @@ __device__ __forceinline__ float4 lds128(uint32_t addr) {
 
 // Exact float64 accumulate without FMA contraction: acc + t rounded once (numpy's `acc += t`).
 __device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
+
+// np.argmin order: a NaN is the minimum (the first NaN wins), otherwise value then index.
+__device__ __forceinline__ bool argmin_less(double a, int ia, double b, int ib) {
+  const bool na = a != a, nb = b != b;
+  if (na || nb) return na && (!nb || ia < ib);
+  return a < b || (a == b && ia < ib);
+}
 
 // 32-bit mixing hash for center-code dedup.
 __device__ __forceinline__ uint32_t mix32(uint32_t h) {

@@ -18,6 +18,10 @@
 
 namespace pqk {
 
+// pqk_encode_tc.cu: tensor-core encoder; *used = false when the shape is not covered.
+int encode_tc_try(const float* d_x, int64_t n, int d, const float* d_cw, int m, int l, uint8_t* d_codes, int stride,
+                  unsigned long long* flagged_out, cudaStream_t stream, bool* used);
+
 
 template <int MAXD>
 __global__ void __launch_bounds__(128) encode_kernel(const float* __restrict__ vec, int64_t n, int d,
@@ -80,13 +84,15 @@ __global__ void __launch_bounds__(128) encode_kernel(const float* __restrict__ v
   // an absolute term for squares flushed below the normal range.
   const double gamma = (double)(dsub + 4) * 5.9604644775390625e-08;  // 2^-24
   const double absl = (double)dsub * 2.350988701644575e-38;          // 2^-125
-  bool cert = (l == 1);
-  if (!cert && b1 <= fmax_ && b2 <= fmax_) cert = (double)b2 > ((double)b1 + absl) * (1.0 + 4.0 * gamma);
-  else if (!cert && b1 <= fmax_ && !(b2 <= fmax_)) cert = false;
+  // certified only with a finite winner and a finite, clearly separated runner-up
+  // (l == 1: a single finite candidate); non-finite inputs go to the exact path
+  bool cert = (l == 1) && b1 <= fmax_;
+  if (l > 1 && b1 <= fmax_ && b2 <= fmax_) cert = (double)b2 > ((double)b1 + absl) * (1.0 + 4.0 * gamma);
   if (!cert) {
-    // exact: float64 sequential sum, separate multiply and add (scipy cdist order)
+    // exact: float64 sequential sum, separate multiply and add (scipy cdist order),
+    // np.argmin order (first NaN wins, else lowest index among equal values)
     double best = __longlong_as_double(0x7ff0000000000000LL);
-    int bl = 0;
+    int bl = 0x7fffffff;
     const float* cbg = cb;
     for (int c = 0; c < l; ++c) {
       const float* cc = cbg + (size_t)c * dsub;
@@ -95,7 +101,7 @@ __global__ void __launch_bounds__(128) encode_kernel(const float* __restrict__ v
         const double df = __dsub_rn((double)x[j], (double)__ldg(&cc[j]));
         acc = __dadd_rn(acc, __dmul_rn(df, df));
       }
-      if (acc < best) {
+      if (argmin_less(acc, c, best, bl)) {
         best = acc;
         bl = c;
       }
@@ -121,6 +127,22 @@ extern "C" int pqk_encode_device(const float* d_vectors, int64_t n, int32_t d, c
   unsigned long long* flagged = reinterpret_cast<unsigned long long*>(d_stats + 20);
   PQK_CUDA_TRY(cudaMemsetAsync(flagged, 0, sizeof(unsigned long long), stream));
   if (code_stride > m) PQK_CUDA_TRY(cudaMemsetAsync(d_codes, 0, (size_t)n * code_stride, stream));
+  // tcgen05 path for the shapes it covers (dsub in {16,32,64}, operands fit in smem);
+  // PQK_ENCODE_SIMT=1 forces the SIMT kernel (used by tests to cross-check both paths)
+  static const bool force_simt = [] {
+    const char* e = getenv("PQK_ENCODE_SIMT");
+    return e && e[0] == '1';
+  }();
+  bool used_tc = false;
+  if (!force_simt) {
+    const int rc = encode_tc_try(d_vectors, n, d, d_codewords, m, l, d_codes, code_stride, flagged, stream, &used_tc);
+    if (rc != PQK_OK) return rc;
+  }
+  if (used_tc) {
+    PQK_CUDA_TRY(cudaMemcpyAsync(d_stats + PQK_STAT_ENCODE_FLAGGED, flagged, sizeof(int64_t),
+                                 cudaMemcpyDeviceToDevice, stream));
+    return PQK_OK;
+  }
   dim3 grid((unsigned)((n + 127) / 128), (unsigned)m);
   const size_t smem = (size_t)l * dsub * sizeof(float);
   if (dsub <= 8) {

@@ -1,0 +1,114 @@
+"""Tensor-core encoder (tcgen05, fp16 hi/lo split + certificate + fp64 fallback)
+against the oracle (pq.py:205-231 semantics: fp64 sequential (x-c)^2, lowest index
+on ties).  Shapes with dsub in {16, 32, 64} take the tcgen05 path."""
+
+import numpy as np
+import pytest
+
+from helpers import random_codebook
+
+pytestmark = pytest.mark.gpu
+
+
+def _encode(cw, x):
+    import paper_1709_03708_b200 as pqk
+
+    return pqk.encode(pqk.PQCodebook(cw), x)
+
+
+@pytest.mark.parametrize("m,sub,l_count,n", [(4, 32, 256, 5000), (8, 16, 256, 3001), (2, 64, 256, 1000),
+                                              (1, 32, 100, 777), (4, 16, 7, 129), (3, 32, 256, 1)])
+def test_tc_encode_random(oracle, m, sub, l_count, n):
+    cw = random_codebook(m, l_count, sub, seed=m * 100 + sub + l_count)
+    x = np.random.default_rng(n).normal(size=(n, m * sub)).astype(np.float32)
+    np.testing.assert_array_equal(_encode(cw, x), oracle.encode(cw, x))
+
+
+def test_tc_encode_integer_data_and_ties(oracle):
+    """SIFT-like integer vectors (x exactly fp16: the lo-x pass is skipped) and exact
+    ties from duplicated codewords and vectors placed on codewords."""
+    rng = np.random.default_rng(3)
+    x = np.clip(np.rint(rng.gamma(0.6, 30.0, size=(4096, 128))), 0, 255).astype(np.float32)
+    cw = x[rng.choice(4096, 256, replace=False)].reshape(256, 4, 32).transpose(1, 0, 2).copy()
+    cw[:, 17] = cw[:, 3]  # duplicated codeword: ties must go to index 3
+    got = _encode(cw, x)
+    np.testing.assert_array_equal(got, oracle.encode(cw, x))
+
+
+@pytest.mark.parametrize("scale", [1e-30, 1e-6, 1e6, 1e30])
+def test_tc_encode_extreme_scales(oracle, scale):
+    cw = (random_codebook(4, 256, 32, seed=9) * scale).astype(np.float32)
+    x = (np.random.default_rng(1).normal(size=(700, 128)) * scale).astype(np.float32)
+    np.testing.assert_array_equal(_encode(cw, x), oracle.encode(cw, x))
+
+
+def test_tc_encode_config1_golden():
+    """Reference encode output on BASELINE config 1 vectors (tests/golden/config1.npz)."""
+    from golden_io import load
+
+    g = load("config1")
+    np.testing.assert_array_equal(_encode(g["codebook"], g["vectors_head"]), g["codes_head"])
+
+
+@pytest.mark.parametrize("bad", [np.nan, np.inf])
+def test_encode_non_finite_vectors_follow_np_argmin(oracle, bad):
+    """np.argmin over cdist rows: a NaN distance is the minimum (first NaN wins)."""
+    cw = random_codebook(4, 256, 32, seed=2)
+    x = np.random.default_rng(4).normal(size=(300, 128)).astype(np.float32)
+    x[5, 3] = bad
+    x[77, 100] = bad
+    np.testing.assert_array_equal(_encode(cw, x), oracle.encode(cw, x))
+
+
+_SIMT_SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+import paper_1709_03708_b200 as pqk
+d = np.load(sys.argv[2])
+np.save(sys.argv[3], pqk.encode(pqk.PQCodebook(d["cw"]), d["x"]))
+"""
+
+
+def test_tc_encode_many_tiles_matches_simt_path(tmp_path):
+    """~11 tiles x 4 subspaces per CTA (buffer reuse across items): the tcgen05 path must
+    equal the SIMT certified path (run in a subprocess with PQK_ENCODE_SIMT=1), and the
+    fp64 fallback must stay rare."""
+    import os
+    import subprocess
+    import sys
+
+    import torch
+
+    from paper_1709_03708_b200 import _lib, engine
+
+    rng = np.random.default_rng(11)
+    n = 200_000
+    cw = random_codebook(4, 256, 32, seed=12)
+    x = rng.normal(size=(n, 128)).astype(np.float32)
+    x[: n // 2] = np.rint(x[: n // 2] * 20)  # half integer-valued (2-pass), half general (3-pass)
+    dev = engine.device_of()
+    stats = torch.zeros(_lib.STATS_LEN, dtype=torch.int64, device=dev)
+    tc_codes = engine.encode_device(torch.from_numpy(x).to(dev), torch.from_numpy(cw).to(dev), 4, 256, dev,
+                                    stride=4, stats=stats).cpu().numpy()
+    flagged = int(stats[_lib.STAT_ENCODE_FLAGGED].item())
+    np.savez(tmp_path / "in.npz", cw=cw, x=x)
+    env = dict(os.environ, PQK_ENCODE_SIMT="1")
+    root = str(__import__("pathlib").Path(__file__).resolve().parents[1])
+    subprocess.run([sys.executable, "-c", _SIMT_SCRIPT, root, str(tmp_path / "in.npz"), str(tmp_path / "out.npy")],
+                   check=True, env=env)
+    np.testing.assert_array_equal(tc_codes, np.load(tmp_path / "out.npy"))
+    assert flagged < n * 4 * 1e-3, flagged  # the stats slot counts every uncertified pair
+
+
+def test_tc_encode_sift_like_flag_rate():
+    """SIFT-like data (BASELINE configs 2/4): the certificate must cover almost every pair."""
+    import torch
+
+    from paper_1709_03708_b200 import _lib, engine, synth
+
+    x = synth.sift_like(100_000, 5)
+    cw = synth.train_codebook_fast(synth.sift_like(20_000, 6), 4, 256, iterations=3, seed=1)
+    dev = engine.device_of()
+    stats = torch.zeros(_lib.STATS_LEN, dtype=torch.int64, device=dev)
+    engine.encode_device(torch.from_numpy(x).to(dev), torch.from_numpy(cw).to(dev), 4, 256, dev, stride=4, stats=stats)
+    assert int(stats[_lib.STAT_ENCODE_FLAGGED].item()) < 100_000 * 4 * 1e-3

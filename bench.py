@@ -36,7 +36,10 @@ CONFIGS = {
     "c2": dict(n=1_000_000, k=10_000, m=4, l=256, dim=128, workload="config2 SIFT-like N=1e6/GPU K=1e4 M=4 L=256"),
     "c1": dict(n=100_000, k=1_000, m=4, l=256, dim=128, workload="config1 mixture N=1e5 K=1e3 M=4 L=256"),
     # config 4's per-GPU shard at 8 GPUs: 1e9/8 SIFT-like codes, K=1e5 (chunked tables stream from HBM)
-    "c4": dict(n=125_000_000, k=100_000, m=4, l=256, dim=128, gpu_data=True,
+    # config 5's per-GPU shard at 8 GPUs: 1e8/8 mixture codes with M=16 (8-D subspaces), K=1e5
+    "c5": dict(n=12_500_000, k=100_000, m=16, l=256, dim=128, gpu_data="mixture",
+               workload="config5 shard mixture N=1.25e7/GPU K=1e5 M=16 L=256"),
+    "c4": dict(n=125_000_000, k=100_000, m=4, l=256, dim=128, gpu_data="sift",
                workload="config4 shard SIFT-like N=1.25e8/GPU K=1e5 M=4 L=256"),
 }
 SEED = 20260419
@@ -68,11 +71,25 @@ def sift_like_gpu(n: int, seed: int, dev, dim: int = 128, blocks: int = 8):
     return g.round_().clamp_(0, 255).reshape(n, dim).contiguous()
 
 
+def mixture_gpu(n: int, seed: int, dev, dim: int = 128, components: int = 100_000, sigma: float = 5.0):
+    """Device-side config-5 mixture: means U[0,100]^dim (fixed seed), sigma 5, uniform components."""
+    import torch
+
+    g = torch.Generator(device=dev)
+    g.manual_seed(SEED)
+    means = torch.rand((components, dim), generator=g, device=dev) * 100.0
+    g.manual_seed(seed)
+    lab = torch.randint(0, components, (n,), generator=g, device=dev)
+    return (means[lab] + sigma * torch.randn((n, dim), generator=g, device=dev)).contiguous()
+
+
 def make_codebook(cfg_name: str, m: int, l_count: int) -> np.ndarray:
     from paper_1709_03708_b200 import synth
 
     if cfg_name == "c1":
         sample = synth.mixture(20_000, 128, 1000, synth.stage_seed(SEED, 1))
+    elif cfg_name == "c5":
+        sample = synth.mixture(100_000, 128, 100_000, synth.stage_seed(SEED, 1))
     else:
         sample = synth.sift_like(100_000, synth.stage_seed(SEED, 1))
     return synth.train_codebook_fast(sample, m, l_count, iterations=8, seed=synth.stage_seed(SEED, 2))
@@ -213,6 +230,7 @@ def main() -> None:
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--dist", action="store_true", help="sharded NCCL driver even with one rank")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "b200" else args.warmup
     if args.impl == "reference":
@@ -231,8 +249,11 @@ def main() -> None:
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+    use_dist = world > 1 or args.dist
+    if use_dist:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29517")
+        dist.init_process_group("nccl", device_id=dev, rank=rank, world_size=world)
     lib = _lib.load()
 
     cfgn = args.config
@@ -256,7 +277,8 @@ def main() -> None:
             chunk = 1 << 23  # 8 Mi vectors (4 GiB fp32) per encode call
             for s in range(0, n_loc, chunk):
                 e = min(n_loc, s + chunk)
-                vec = sift_like_gpu(e - s, synth.stage_seed(SEED, 1000 + rank * 100_000 + s // chunk), dev)
+                cseed = synth.stage_seed(SEED, 1000 + rank * 100_000 + s // chunk)
+                vec = (mixture_gpu(e - s, cseed, dev) if cfg["gpu_data"] == "mixture" else sift_like_gpu(e - s, cseed, dev))
                 e0.record()
                 codes_dev[s:e] = engine.encode_device(vec, cw_dev, m, l_count, dev, stride=mp, stats=stats_enc)
                 e1.record()
@@ -280,8 +302,8 @@ def main() -> None:
     offset, length = shard_bounds(n_total, world, rank)
     assert length == n_loc, (length, n_loc)
     backend = GpuShardBackend(codes_host, offset, tables, k, device=local)
-    drv = DistributedLloyd(backend, n_total, k, m) if world > 1 else None
-    if world > 1:
+    drv = DistributedLloyd(backend, n_total, k, m) if use_dist else None
+    if use_dist:
         centers0 = drv.init_centers(SEED, codes_host)
     else:
         rng = np.random.default_rng(SEED)
@@ -300,7 +322,7 @@ def main() -> None:
         return eng.new_centers.clone(), st
 
     def step(cur):
-        if world == 1:
+        if not use_dist:
             return step_single(cur)
         st, nxt, _ = drv.iteration(cur, None)
         return nxt, eng.stats_host()
@@ -323,7 +345,7 @@ def main() -> None:
         with ClockSampler(local) as clocks:
             for _ in range(args.steps):
                 flush.fill_(1)
-                if world > 1:
+                if use_dist:
                     dist.barrier()
                 torch.cuda.synchronize(dev)
                 e0 = torch.cuda.Event(enable_timing=True)
@@ -342,7 +364,7 @@ def main() -> None:
     lib.pqk_set_profile_events(None, None)
 
     total_ms = float(np.sum(step_ms))
-    if world > 1:
+    if use_dist:
         t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
@@ -408,7 +430,7 @@ def main() -> None:
                      "flagged_pairs": enc_flagged, "kernel": "encode_kernel (SIMT fp32 filter + fp64 certificate)"}
 
     # ---- e2e through the C-ABI host entry (host buffers, H2D/D2H inside) ------------
-    if not args.no_e2e and world == 1:
+    if not args.no_e2e and not use_dist:
         import ctypes as C
 
         pin_codes = torch.from_numpy(codes_host).pin_memory()
@@ -471,7 +493,7 @@ def main() -> None:
         out["cpu_baseline"] = cpu_baseline_sample(codes_host, centers0, tables, n_total)
     if rank == 0:
         print(json.dumps(out), flush=True)
-    if world > 1:
+    if use_dist:
         dist.barrier()
         dist.destroy_process_group()
 

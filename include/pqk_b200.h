@@ -154,6 +154,16 @@ int pqk_encode_device(const float* d_vectors, int64_t n, int32_t d, const float*
                       int32_t m, int32_t l, uint8_t* d_codes, int32_t code_stride,
                       int64_t* d_stats, void* stream);
 
+/* Codebook training (pq.py:127-152, one Lloyd step of _lloyd_subspace on subspace
+ * columns [col0, col0+dsub) of fp32 points (n, d)): labels, counts, per-(codeword, dim)
+ * sums in point-index order, centers[filled] = sums / counts (fp64, in place), and —
+ * only when some codeword is empty (count in d_stats[PQK_STAT_EMPTY]) — the
+ * reference's `own` = np.sum((x - c[label])**2, axis=1) for the host-side reseed. */
+size_t pqk_train_workspace_bytes(int64_t n, int32_t dsub);
+int pqk_train_step_device(const float* d_x, int64_t n, int32_t d, int32_t col0, int32_t dsub, double* d_centers,
+                          int32_t l, int32_t* d_labels, double* d_sums, int32_t* d_counts, double* d_own,
+                          void* d_ws, size_t ws_bytes, int64_t* d_stats, void* stream);
+
 /* ---- host-buffer entry points (the reference-facing plugin boundary) ---------- */
 /* AssignStrategy (clustering.py:200): labels (and optionally sd_sq) for host codes. */
 int pqk_assign_host(const uint8_t* codes, int64_t n, int32_t m, const uint8_t* centers, int64_t k,

@@ -229,6 +229,51 @@ def encode(codewords: np.ndarray, vectors: np.ndarray) -> np.ndarray:
     return out
 
 
+def _nearest_f64(points: np.ndarray, centers: np.ndarray) -> np.ndarray:
+    """pq.py:114-116 with scipy cdist("sqeuclidean") restated: sequential (x-c)*(x-c) sums."""
+    acc = np.zeros((len(points), len(centers)), dtype=np.float64)
+    for d in range(points.shape[1]):
+        diff = points[:, None, d] - centers[None, :, d]
+        acc += diff * diff
+    return np.argmin(acc, axis=1)
+
+
+def _lloyd_subspace(sub: np.ndarray, num_codewords: int, iterations: int, rng) -> np.ndarray:
+    """pq.py:127-152: float64 Lloyd with farthest-point reseed of empty codewords."""
+    points = sub.astype(np.float64)
+    n = len(points)
+    centers = points[rng.choice(n, size=num_codewords, replace=False)].copy()
+    for _ in range(iterations):
+        labels = _nearest_f64(points, centers)
+        counts = np.bincount(labels, minlength=num_codewords)
+        sums = np.stack([np.bincount(labels, weights=points[:, d], minlength=num_codewords)
+                         for d in range(points.shape[1])], axis=1)  # pq.py:119-124
+        filled = counts > 0
+        centers[filled] = sums[filled] / counts[filled, None]
+        if not filled.all():
+            own = np.sum((points - centers[labels]) ** 2, axis=1)
+            for slot in np.flatnonzero(~filled):
+                far = int(np.argmax(own))
+                centers[slot] = points[far]
+                labels[far] = slot
+                own[far] = -np.inf
+    return centers
+
+
+def train_codebook(train_vectors: np.ndarray, num_subspaces: int, num_codewords: int, iterations: int = 20,
+                   seed: int = 0) -> np.ndarray:
+    """pq.py:155-202 (one Generator shared across subspaces); returns (M, L, D/M) float32."""
+    vectors = np.asarray(train_vectors, dtype=np.float32)
+    n, dim = vectors.shape
+    sub_dim = dim // num_subspaces
+    rng = np.random.default_rng(seed)
+    books = np.empty((num_subspaces, num_codewords, sub_dim), dtype=np.float32)
+    for m in range(num_subspaces):
+        sub = vectors[:, m * sub_dim : (m + 1) * sub_dim]
+        books[m] = _lloyd_subspace(sub, num_codewords, iterations, rng).astype(np.float32)
+    return books
+
+
 def build_distance_tables(codewords: np.ndarray) -> np.ndarray:
     """pq.py:254-268: sequential fp64 squared distances between codewords."""
     m_count, l_count, sub = codewords.shape

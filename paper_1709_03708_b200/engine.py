@@ -437,6 +437,52 @@ def encode_host(codewords: np.ndarray, vectors: np.ndarray, *, device=None, stri
         return out.cpu().numpy()
 
 
+def train_codebook_host(vectors: np.ndarray, m: int, l: int, iterations: int, seed: int, *, device=None) -> np.ndarray:
+    """Per-subspace Lloyd k-means on the GPU, bit-identical to pq.train_codebook (pq.py:127-202).
+
+    Initial codewords come from the same host Generator draws as the reference; each
+    Lloyd step runs in pqk_train_step_device; empty codewords are re-seeded on the
+    farthest points (lowest index first) chosen by the device top-E select.
+    """
+    dev = device_of(device)
+    lib = _lib.load()
+    vectors = np.ascontiguousarray(vectors, dtype=np.float32)
+    n, d = vectors.shape
+    sub = d // m
+    rng = np.random.default_rng(seed)
+    books = np.empty((m, l, sub), dtype=np.float32)
+    with torch.cuda.device(dev):
+        s = _stream(dev)
+        x = torch.from_numpy(vectors).to(dev)
+        labels = torch.empty(n, dtype=torch.int32, device=dev)
+        sums = torch.empty(l * sub, dtype=torch.float64, device=dev)
+        counts = torch.empty(l, dtype=torch.int32, device=dev)
+        own = torch.empty(n, dtype=torch.float64, device=dev)
+        ws_bytes = int(lib.pqk_train_workspace_bytes(n, sub))
+        ws = _empty(ws_bytes, dev)
+        stats = torch.zeros(STATS_LEN, dtype=torch.int64, device=dev)
+        rws_bytes = int(lib.pqk_repair_workspace_bytes(n, l))
+        rws = _empty(rws_bytes, dev)
+        keys = torch.empty(l, dtype=torch.int64, device=dev)
+        index = torch.empty(l, dtype=torch.int64, device=dev)
+        for mm in range(m):
+            idx = rng.choice(n, size=l, replace=False)
+            centers = torch.from_numpy(vectors[idx, mm * sub : (mm + 1) * sub].astype(np.float64)).to(dev).contiguous()
+            for _ in range(iterations):
+                call("pqk_train_step_device", _ptr(x), n, d, mm * sub, sub, _ptr(centers), l, _ptr(labels), _ptr(sums),
+                     _ptr(counts), _ptr(own), _ptr(ws), ws_bytes, _ptr(stats), s)
+                e = int(stats[_lib.STAT_EMPTY].item())
+                if e:
+                    # pq.py:145-151: empty slots (ascending) take the farthest points
+                    call("pqk_repair_candidates_device", _ptr(own), n, 0, e, _ptr(rws), rws_bytes, _ptr(keys),
+                         _ptr(index), s)
+                    slots = torch.from_numpy(np.flatnonzero(counts.cpu().numpy() == 0)).to(dev)
+                    far = index[:e]
+                    centers[slots] = x[far, mm * sub : (mm + 1) * sub].double()
+            books[mm] = centers.cpu().numpy().astype(np.float32)
+    return books
+
+
 def encode_device(vec_dev, cw_dev, m: int, l: int, dev, stride: int | None = None, stats=None):
     n, d = int(vec_dev.shape[0]), int(vec_dev.shape[1])
     stride = m if stride is None else stride

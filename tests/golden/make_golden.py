@@ -245,10 +245,27 @@ def make_tables_and_mean():
     save("tables_mean", **arrays)
 
 
+def make_train():
+    """Reference train_codebook (pq.py:155-202), incl. empty-codeword reseeds."""
+    arrays = {}
+    rng = np.random.default_rng(77)
+    x0 = rng.normal(size=(2000, 16)).astype(np.float32)
+    arrays.update(t0_x=x0, t0_book=train_codebook(x0, 4, 32, iterations=5, seed=3).codewords,
+                  t0_args=np.array([4, 32, 5, 3]))
+    # many duplicated rows: codewords go empty and are re-seeded on the farthest points
+    rows = rng.normal(size=(40, 12)).astype(np.float32) * 3
+    x1 = rows[rng.integers(0, 40, size=300)]
+    arrays.update(t1_x=x1, t1_book=train_codebook(x1, 2, 64, iterations=6, seed=5).codewords,
+                  t1_args=np.array([2, 64, 6, 5]))
+    x2 = (rng.normal(size=(1500, 64)) * 10).astype(np.float32)
+    arrays.update(t2_x=x2, t2_book=train_codebook(x2, 1, 256, iterations=3, seed=9).codewords,
+                  t2_args=np.array([1, 256, 3, 9]))
+    arrays["ncases"] = np.array(3)
+    save("train", **arrays)
+
+
 if __name__ == "__main__":
-    make_assign()
-    make_fit()
-    make_encode()
-    make_vote()
-    make_tables_and_mean()
-    make_config1()
+    makers = {"assign": make_assign, "fit": make_fit, "encode": make_encode, "vote": make_vote,
+              "tables_mean": make_tables_and_mean, "config1": make_config1, "train": make_train}
+    for name in sys.argv[1:] or list(makers):  # default: regenerate every fixture
+        makers[name]()

@@ -94,3 +94,12 @@ def test_objective_tree_golden():
         assert O.pairwise_sum(np.sqrt(x)) / n == mean[0]
         assert O.pairwise_sum(x) / n == mean[1]
         assert O.objective(x) == (mean[0], mean[1])
+
+
+def test_train_codebook_golden():
+    """Oracle restatement of pq.train_codebook vs the reference's own codewords."""
+    g = load("train")
+    for i in range(int(g["ncases"])):
+        m, l_count, it, seed = (int(v) for v in g[f"t{i}_args"])
+        got = O.train_codebook(g[f"t{i}_x"], m, l_count, iterations=it, seed=seed)
+        assert got.tobytes() == g[f"t{i}_book"].tobytes(), i

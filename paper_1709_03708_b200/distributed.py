@@ -72,12 +72,6 @@ class GpuShardBackend:
     def sync(self) -> None:
         torch.cuda.current_stream(self.dev).synchronize()
 
-    def objective_sums(self) -> np.ndarray:
-        if self.n == 0:
-            return np.zeros(2)
-        self.eng.objective()
-        return self.eng.obj.cpu().numpy()
-
     def histogram(self):
         self.eng.histogram()
         return self.eng.hist, self.eng.counts
@@ -89,11 +83,30 @@ class GpuShardBackend:
     def counts_host(self) -> np.ndarray:
         return self.eng.counts.cpu().numpy()
 
+    def objective_tensor(self):
+        """(sum sqrt(sd), sum sd) of the local subtree, float64 on the device (no host sync)."""
+        if self.n == 0:
+            return torch.zeros(2, dtype=torch.float64, device=self.dev)
+        self.eng.objective()
+        return self.eng.obj
+
     def local_candidates(self, e: int):
+        """Local top-e (sd desc, global index asc) padded to exactly e entries, on the device:
+        keys (int64 bit patterns of sd), global index (int64; padding = int64 max), code rows."""
         keys, index = self.eng.repair_candidates(e)
-        local = (index - self.offset).clamp_(min=0)
-        rows = self.eng.codes[local][:, : self.m] if len(index) else torch.empty((0, self.m), dtype=torch.uint8)
-        return keys.cpu().numpy().view(np.uint64), index.cpu().numpy(), rows.cpu().numpy()
+        got = len(index)
+        pk = torch.zeros(e, dtype=torch.int64, device=self.dev)
+        pi = torch.full((e,), np.iinfo(np.int64).max, dtype=torch.int64, device=self.dev)
+        pr = torch.zeros((e, self.m), dtype=torch.uint8, device=self.dev)
+        if got:
+            pk[:got] = keys
+            pi[:got] = index
+            pr[:got] = self.eng.codes[(index - self.offset).clamp_(min=0)][:, : self.m]
+        return pk, pi, pr
+
+    @property
+    def tensor_device(self):
+        return self.dev
 
     def apply_repair(self, empty: np.ndarray, rows: np.ndarray) -> None:
         if len(empty):
@@ -109,9 +122,6 @@ class GpuShardBackend:
 
     def labels_host(self) -> np.ndarray:
         return self.eng.labels_host()
-
-    def collective_device(self):
-        return self.dev
 
 
 def _allgather_obj(values, group) -> list:
@@ -153,16 +163,23 @@ class DistributedLloyd:
             rows.update(p)
         return np.stack([rows[int(i)] for i in idx]).astype(np.uint8)
 
+    def _gather(self, t: "torch.Tensor") -> "torch.Tensor":
+        """all_gather of a fixed-shape tensor (NCCL on GPUs, gloo on CPU) -> (world, *shape)."""
+        if self.world == 1:
+            return t.unsqueeze(0)
+        out = [torch.empty_like(t) for _ in range(self.world)]
+        dist.all_gather(out, t.contiguous(), group=self.group)
+        return torch.stack(out)
+
     def iteration(self, centers_dev, previous: float | None) -> tuple[StepStats, object, bool]:
         """One Lloyd iteration; returns (stats, next centers, stopped)."""
         t0 = time.perf_counter()
         self.b.assign(centers_dev)
         self.b.sync()
         assign_seconds = time.perf_counter() - t0
-        sums = self.b.objective_sums()
-        parts = _allgather_obj((float(sums[0]), float(sums[1])), self.group)
-        s1 = tree_combine(self.n_total, [p[0] for p in parts])
-        s2 = tree_combine(self.n_total, [p[1] for p in parts])
+        parts = self._gather(self.b.objective_tensor()).cpu().numpy()
+        s1 = tree_combine(self.n_total, list(parts[:, 0]))
+        s2 = tree_combine(self.n_total, list(parts[:, 1]))
         objective = float(np.float64(s1) / self.n_total)
         objective_sq = float(np.float64(s2) / self.n_total)
         if previous is not None and objective == previous:
@@ -177,9 +194,11 @@ class DistributedLloyd:
         if empty_n:
             counts_h = self.b.counts_host()
             empty = np.flatnonzero(counts_h == 0)
-            cand = self.b.local_candidates(empty_n)
-            allc = _allgather_obj(cand, self.group)
-            _, _, rows = merge_candidates(allc, empty_n)
+            pk, pi, pr = self.b.local_candidates(empty_n)
+            gk = self._gather(pk).cpu().numpy().reshape(-1).view(np.uint64)
+            gi = self._gather(pi).cpu().numpy().reshape(-1)
+            gr = self._gather(pr).cpu().numpy().reshape(-1, self.m)
+            _, _, rows = merge_candidates([(gk, gi, gr)], empty_n)
             self.b.apply_repair(empty, rows)
         nxt = self.b.take_new_centers()
         self.b.sync()

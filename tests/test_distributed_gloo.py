@@ -44,10 +44,10 @@ class CpuShardBackend:
     def sync(self):
         pass
 
-    def objective_sums(self):
+    def objective_tensor(self):
         if self.n == 0:
-            return np.zeros(2)
-        return np.array([np.add.reduce(np.sqrt(self.sd)), np.add.reduce(self.sd)])
+            return torch.zeros(2, dtype=torch.float64)
+        return torch.tensor([np.add.reduce(np.sqrt(self.sd)), np.add.reduce(self.sd)], dtype=torch.float64)
 
     def histogram(self):
         h = self.O.histogram(self.codes, self.labels, self.k, self.l).astype(np.int32)
@@ -77,7 +77,13 @@ class CpuShardBackend:
         keys = self.sd.view(np.uint64)
         idx = np.arange(self.n) + self.offset
         order = np.lexsort((idx, ~keys))[:e]
-        return keys[order], idx[order], self.codes[order - 0]
+        pk = np.zeros(e, np.uint64)
+        pi = np.full(e, np.iinfo(np.int64).max, np.int64)
+        pr = np.zeros((e, self.m), np.uint8)
+        pk[: len(order)] = keys[order]
+        pi[: len(order)] = idx[order]
+        pr[: len(order)] = self.codes[order]
+        return torch.from_numpy(pk.view(np.int64)), torch.from_numpy(pi), torch.from_numpy(pr)
 
     def apply_repair(self, empty, rows):
         self.new[empty] = rows

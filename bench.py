@@ -114,26 +114,29 @@ class ClockSampler:
         self._stop = threading.Event()
         self._thread = None
 
-    def _poll(self):
+    def _sample(self):
         import pynvml
 
-        pynvml.nvmlInit()
-        h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
-        self.max_mhz = float(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM))
-        masks = {k: getattr(pynvml, v) for k, v in self.REASONS.items()}
-        while not self._stop.is_set():
-            self.sm.append(float(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)))
-            r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
-            for k, mask in masks.items():
-                if r & mask:
-                    self.reasons.add(k)
-            self._stop.wait(0.005)
-        pynvml.nvmlShutdown()
+        self.sm.append(float(pynvml.nvmlDeviceGetClockInfo(self._h, pynvml.NVML_CLOCK_SM)))
+        r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+        for k, mask in self._masks.items():
+            if r & mask:
+                self.reasons.add(k)
+
+    def _poll(self):
+        while True:  # at least one sample even for a region shorter than the period
+            self._sample()
+            if self._stop.wait(0.005):
+                break
 
     def __enter__(self):
         try:
-            import pynvml  # noqa: F401
+            import pynvml
 
+            pynvml.nvmlInit()  # before the region starts: init costs tens of ms
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = float(pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM))
+            self._masks = {k: getattr(pynvml, v) for k, v in self.REASONS.items()}
             self._thread = threading.Thread(target=self._poll, daemon=True)
             self._thread.start()
         except Exception:
@@ -144,6 +147,9 @@ class ClockSampler:
         self._stop.set()
         if self._thread:
             self._thread.join(timeout=2)
+            import pynvml
+
+            pynvml.nvmlShutdown()
 
     def summary(self) -> dict:
         return {"sm_mhz": float(np.median(self.sm)) if self.sm else None, "sm_max_mhz": self.max_mhz,
@@ -276,6 +282,11 @@ def main() -> None:
         stats_enc = torch.zeros(_lib.STATS_LEN, dtype=torch.int64, device=dev)
         cw_dev = torch.from_numpy(np.array(book)).to(dev)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        # untimed warm-up call: module load, tensor-map entry point, per-device workspace
+        warm = torch.zeros((4096, cfg["dim"]), dtype=torch.float32, device=dev)
+        engine.encode_device(warm, cw_dev, m, l_count, dev, stride=mp)
+        torch.cuda.synchronize(dev)
+        del warm
         if cfg.get("gpu_data"):
             # billion-scale shard: vectors generated on device per seeded chunk, encoded in place
             codes_dev = torch.empty((n_loc, mp), dtype=torch.uint8, device=dev)

@@ -304,11 +304,16 @@ def main() -> None:
         else:
             vectors = make_vectors(cfgn, n_loc, rank)
             vec_dev = torch.from_numpy(vectors).to(dev)
-            e0.record()
             codes_dev = engine.encode_device(vec_dev, cw_dev, m, l_count, dev, stride=mp, stats=stats_enc)
-            e1.record()
             torch.cuda.synchronize(dev)
-            enc_ms = e0.elapsed_time(e1)
+            times = []
+            for _ in range(3):  # timed repeats (the first call above sized the workspace)
+                e0.record()
+                engine.encode_device(vec_dev, cw_dev, m, l_count, dev, stride=mp)
+                e1.record()
+                torch.cuda.synchronize(dev)
+                times.append(e0.elapsed_time(e1))
+            enc_ms = min(times)
             del vec_dev
         codes_host = engine.download_codes(codes_dev, m)
         enc_flagged = int(stats_enc[_lib.STAT_ENCODE_FLAGGED].item())

@@ -72,23 +72,31 @@ extern "C" int pqk_tc_selftest(const void* d_a, const void* d_b, float* d_c, int
 // ===========================================================================
 // Tensor-core PQ encoder (pq.py:205-231 on tcgen05).
 //
-// For subspace m and a tile of 128 vectors: S = X_m C_m^T (128 x 256) on the tensor
-// cores, g_l = ||c_l||^2 - 2 x.c_l, code = argmin_l g_l (= argmin ||x - c_l||^2).
-// Exactness: x and c are scaled by powers of two into fp16 range and split as
-// v = hi + lo (fp16 each, ~22 significant bits); S = hi.hi + hi.lo + lo.hi in fp32
-// (the lo.hi pass is skipped for tiles whose x are exactly fp16, e.g. integer SIFT
-// data).  The epilogue keeps best and runner-up per row and certifies the winner
-// when their gap exceeds a rigorous bound on the split/accumulation error; other
-// (vector, subspace) pairs are re-decided by the exact float64 sequential sum
-// (scipy cdist order) in encode_exact_kernel.
+// Each CTA owns one subspace m (blockIdx.x % M) and walks 128-vector tiles.  For a
+// tile, one accumulator of 128 x 256 fp32 in TMEM receives
+//
+//   D_rj = s^2 |x_r|^2 - 2 s^2 x_r.c_j + s^2 |c_j|^2    (= s^2 |x_r - c_j|^2)
+//
+// entirely from tcgen05.mma: the x and -2c operands are scaled by one power of two s
+// per subspace and split v = hi + lo into fp16 pairs (hi.hi + hi.lo [+ lo.hi when the
+// tile's x are not exactly fp16]); s^2|c_j|^2 and the row's s^2|x_r|^2 enter through
+// 16 extra K columns of the hi pass (three fp16 parts each, times an exact power of
+// two).  The epilogue therefore has no per-distance floating-point work: a key is
+// the accumulator's bits with the low 6 bits replaced by the column (one LOP3),
+// compared as signed int32 so that the (rare) negative values produced by rounding
+// next to a zero distance still sort below every positive value.  Best and runner-up
+// keys give a certificate: the winner is certified when the runner-up exceeds it by
+// more than twice a rigorous bound on |computed - exact| (split, skipped lo.lo term,
+// tensor-core accumulation).  Uncertified (vector, subspace) pairs are re-decided by
+// the exact float64 sequential sum (scipy cdist order) in encode_exact_kernel.
 //
 // Warp roles (persistent, one CTA per SM, 576 threads):
-//   warp 0  TMA producer: 2-D tensor-map loads of X[128 rows x KP] per (tile, m)
-//   warp 1  TMEM allocator + single-thread tcgen05.mma issuer (2 accumulators of
-//           128 x 256 fp32 = all 512 TMEM columns, double-buffered)
-//   warps 2-17 transform (fp32 -> fp16 hi/lo in the UMMA K-major layout) and
-//           epilogue (tcgen05.ld, argmin, certificate, code store); warp w reads
-//           TMEM lanes 32*(w%4).. and columns [64*h, 64*h+64), h = (w-2)/4.
+//   warp 0   TMA producer: 2-D tensor-map loads of X[128 rows x dsub] per tile
+//   warp 1   TMEM allocator + single-thread tcgen05.mma issuer (2 accumulators of
+//            128 x 256 fp32 = all 512 TMEM columns, double-buffered)
+//   warps 2-17 transform (fp32 -> scaled fp16 hi/lo + extension columns in the UMMA
+//            K-major layout) and epilogue (tcgen05.ld, keys, argmin, certificate);
+//            warp w reads TMEM lanes 32*(w%4).. and columns [64h, 64h+64), h=(w-2)/4.
 // ===========================================================================
 #include <cuda.h>
 #include <cudaTypedefs.h>
@@ -100,24 +108,52 @@ namespace enc {
 
 constexpr int kRows = 128;
 constexpr int kN = 256;
-constexpr int kXStages = 3;
-constexpr int kWorkWarps = 16;  // transform + epilogue warps (4 per SM sub-partition)
-constexpr int kThreads = (2 + kWorkWarps) * 32;
+constexpr int kExt = 16;       // extension K columns of the hi pass
+constexpr int kEpiWarps = 8;   // 2 per TMEM lane quadrant: one per accumulator
+constexpr int kTrWarps = 8;    // transform warps (16 rows each)
+constexpr int kThreads = (2 + kEpiWarps + kTrWarps) * 32;
+constexpr int kChunk = 32;     // epilogue columns per tcgen05.ld pair
+constexpr float kX2Limit = 1073741824.0f;  // 2^30: |s x|^2 bound for the fp16 extension parts
+
+// per-subspace constants written by encode_prep_kernel (floats)
+enum { CST_S = 0, CST_ACN = 1, CST_CB = 2, CST_CN = 3, CST_S1C = 4, CST_VALID = 5, CST_LEN = 8 };
+
+template <int KP>
+struct Geo {
+  static constexpr int KE = KP + kExt;
+  static constexpr int XST = KP >= 64 ? 2 : 3;  // X stages
+  static constexpr bool SWZ = KP >= 32;         // X tile loaded with the 128-byte swizzle
+  static constexpr int B_HI = kN * KE * 2;
+  static constexpr int B_LO = kN * KP * 2;
+  static constexpr int B_BYTES = B_HI + B_LO;
+  static constexpr int A_HI = kRows * KE * 2;
+  static constexpr int A_LO = kRows * KP * 2;
+  static constexpr int A_BYTES = A_HI + A_LO;
+  static constexpr int X_STAGE = kRows * KP * 4;  // 128 x dsub floats (dsub <= KP)
+  static constexpr int OFF_X = B_BYTES;           // multiple of 1024 (swizzled TMA destination)
+  static constexpr int OFF_A = OFF_X + XST * X_STAGE;
+  static constexpr int OFF_STATS = OFF_A + 2 * A_BYTES;        // float4 [4][128]
+  static constexpr int OFF_LO = OFF_STATS + 4 * kRows * 16;    // int [2][kTrWarps]
+  static constexpr int OFF_CST = OFF_LO + 2 * kTrWarps * 4;    // float [8]
+  static constexpr int OFF_BAR = OFF_CST + CST_LEN * 4;        // uint64 [24]
+  static constexpr int OFF_TBASE = OFF_BAR + 24 * 8;
+  static constexpr int SMEM = OFF_TBASE + 16 + 1024;           // + alignment slack
+};
 
 struct EncParams {
-  const float* x;
-  const float* cw;
-  const uint8_t* bprep;  // [M][2][256 x KP] fp16, UMMA K-major
-  const float* cnc;      // [M][256]  s_c * ||c||^2 (+inf for padding rows)
-  const float* cstat;    // [M][4]    C2, C1, CN (scaled), s_c
+  const uint8_t* bprep;  // [M][B_BYTES]: hi+ext (256 x KE) then lo (256 x KP), fp16 K-major
+  const float* cst;      // [M][CST_LEN]
   int64_t n;
-  int d, m, l, ks;
+  int m, ks;
   uint8_t* codes;
   int stride;
-  uint32_t* flags;
-  unsigned int* counters;  // [0] flagged, [1] overflow
+  uint32_t* flags;         // [M][flag_cap] uncertified rows per subspace
+  unsigned int* counters;  // [0] flagged total, [1] overflow, [2 + m] per-subspace count
   uint32_t flag_cap;
-  int ntiles;
+  int ntiles;        // 128-row tiles
+  int tstride;       // CTAs per subspace
+  uint32_t keymask;  // ~31u, a run-time value so that key packing is one LOP3
+  uint32_t one;      // 1
 };
 
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
@@ -128,62 +164,122 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
       : "memory");
 }
 
-__device__ __forceinline__ void named_bar(int id, int count) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+__device__ __forceinline__ int imin3(int a, int b, int c) { return min(a, min(b, c)); }
+__device__ __forceinline__ uint32_t umin3(uint32_t a, uint32_t b, uint32_t c) { return min(a, min(b, c)); }
+
+__device__ __forceinline__ uint32_t pack_h2(__half a, __half b) {
+  return (uint32_t)__half_as_ushort(a) | ((uint32_t)__half_as_ushort(b) << 16);
 }
 
-template <int KP>
-__host__ __device__ constexpr size_t smem_bytes(int m) {
-  return (size_t)m * 2 * kN * KP * 2          // B hi/lo
-         + (size_t)kXStages * kRows * KP * 4  // X stages
-         + (size_t)2 * 2 * kRows * KP * 2     // A hi/lo, double-buffered
-         + (size_t)m * kN * 4 + (size_t)m * 16  // cnc, cstat
-         + (size_t)4 * kRows * 16              // row stats, 4 buffers
-         + (size_t)3 * kRows * 16              // column-quarter merge
-         + 2 * kWorkWarps * 4 + 16 * 8 + 16;   // lo flags, barriers, tmem base
+// 32 columns (two tcgen05.ld x16) into r[0..31]
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%32];\n\t"
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%33];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr), "r"(taddr + 16u));
+}
+
+// tcgen05.wait::ld with the destination registers as operands, so that no use of them
+// can be scheduled before the wait
+__device__ __forceinline__ void tmem_wait32(uint32_t (&r)[32]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
+                 "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]),
+                 "+r"(r[15]), "+r"(r[16]), "+r"(r[17]), "+r"(r[18]), "+r"(r[19]), "+r"(r[20]), "+r"(r[21]),
+                 "+r"(r[22]), "+r"(r[23]), "+r"(r[24]), "+r"(r[25]), "+r"(r[26]), "+r"(r[27]), "+r"(r[28]),
+                 "+r"(r[29]), "+r"(r[30]), "+r"(r[31])
+               :
+               : "memory");
+}
+
+// x * one + y on the FMA pipe (one = 1 at run time: keeps ptxas from fusing the add
+// into an ALU VIADDMNMX, the epilogue being ALU-bound)
+__device__ __forceinline__ uint32_t imad(uint32_t x, uint32_t one, uint32_t y) {
+  uint32_t r;
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(x), "r"(one), "r"(y));
+  return r;
+}
+
+// minimum of 32 values as a depth-4 tree of 3-input minima (independent operations for
+// instruction-level parallelism: one warp per row block must keep the ALU pipe busy)
+__device__ __forceinline__ int tree_min32(const uint32_t (&k)[32]) {
+  int t[11];
+#pragma unroll
+  for (int i = 0; i < 10; ++i) t[i] = imin3((int)k[3 * i], (int)k[3 * i + 1], (int)k[3 * i + 2]);
+  t[10] = min((int)k[30], (int)k[31]);
+  const int u0 = imin3(t[0], t[1], t[2]), u1 = imin3(t[3], t[4], t[5]), u2 = imin3(t[6], t[7], t[8]);
+  const int u3 = min(t[9], t[10]);
+  return imin3(u0, u1, min(u2, u3));
+}
+__device__ __forceinline__ uint32_t tree_umin32(const uint32_t (&k)[32]) {
+  uint32_t t[11];
+#pragma unroll
+  for (int i = 0; i < 10; ++i) t[i] = umin3(k[3 * i], k[3 * i + 1], k[3 * i + 2]);
+  t[10] = min(k[30], k[31]);
+  const uint32_t u0 = umin3(t[0], t[1], t[2]), u1 = umin3(t[3], t[4], t[5]), u2 = umin3(t[6], t[7], t[8]);
+  const uint32_t u3 = min(t[9], t[10]);
+  return umin3(u0, u1, min(u2, u3));
+}
+
+// best (signed key) and runner-up of 32 raw accumulator words of one row; keys carry the
+// column within the chunk in their low 5 bits
+__device__ __forceinline__ void chunk_best(uint32_t (&k)[32], uint32_t kmask, uint32_t one, int& bc, int& rc) {
+#pragma unroll
+  for (int j = 0; j < 32; ++j) k[j] = (k[j] & kmask) | (uint32_t)j;
+  bc = tree_min32(k);
+  // runner-up: keys are unique, so min over (k - (b + 1)) mod 2^32 maps the winner to
+  // 0xffffffff and every other key to k - b - 1, in signed-key order
+  const uint32_t nbp = ~(uint32_t)bc;  // -(b + 1)
+#pragma unroll
+  for (int j = 0; j < 32; ++j) k[j] = imad(k[j], one, nbp);
+  rc = (int)(tree_umin32(k) - nbp);
 }
 
 template <int KP>
 __global__ void __launch_bounds__(kThreads, 1) encode_tc_kernel(const __grid_constant__ CUtensorMap tmap,
                                                                 const EncParams p) {
-  extern __shared__ __align__(1024) uint8_t smem[];
-  constexpr int A_PART = kRows * KP * 2;
-  constexpr int B_PART = kN * KP * 2;
-  constexpr int X_STAGE = kRows * KP * 4;
-  const int M = p.m;
-  const uint32_t bytesB = (uint32_t)M * 2 * B_PART;
+  using G = Geo<KP>;
+  constexpr int KE = G::KE;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sB = smem;
-  uint8_t* sX = smem + bytesB;
-  uint8_t* sA = sX + kXStages * X_STAGE;
-  float* s_cnc = reinterpret_cast<float*>(sA + 2 * 2 * A_PART);
-  float* s_cstat = s_cnc + M * kN;
-  float4* s_stats = reinterpret_cast<float4*>(s_cstat + M * 4);
-  float4* s_merge = s_stats + 4 * kRows;                     // [3][128]
-  int* s_lo = reinterpret_cast<int*>(s_merge + 3 * kRows);    // [2][kWorkWarps]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(s_lo + 2 * kWorkWarps);
-  uint64_t* xfull = bars;
-  uint64_t* xempty = bars + 3;
-  uint64_t* afull = bars + 6;
-  uint64_t* aempty = bars + 8;
-  uint64_t* tfull = bars + 10;
-  uint64_t* tempty = bars + 12;
-  uint64_t* bload = bars + 14;
-  uint32_t* s_tbase = reinterpret_cast<uint32_t*>(bars + 16);
+  uint8_t* sX = smem + G::OFF_X;
+  uint8_t* sA = smem + G::OFF_A;
+  float4* s_stats = reinterpret_cast<float4*>(smem + G::OFF_STATS);
+  int* s_lo = reinterpret_cast<int*>(smem + G::OFF_LO);
+  float* s_cst = reinterpret_cast<float*>(smem + G::OFF_CST);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + G::OFF_BAR);
+  uint64_t* xfull = bars;        // [3]
+  uint64_t* xempty = bars + 3;   // [3]
+  uint64_t* afull = bars + 6;    // [2]
+  uint64_t* aempty = bars + 8;   // [2]
+  uint64_t* tfull = bars + 10;   // [2][2]: accumulator, column half
+  uint64_t* tempty = bars + 14;  // [2][2]
+  uint64_t* bload = bars + 18;
+  uint32_t* s_tbase = reinterpret_cast<uint32_t*>(smem + G::OFF_TBASE);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int my_tiles = (p.ntiles > (int)blockIdx.x) ? (p.ntiles - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x : 0;
-  const int items = my_tiles * M;
+  const int m = (int)blockIdx.x % p.m;
+  const int t0 = (int)blockIdx.x / p.m;
+  const int items = t0 < p.ntiles ? (p.ntiles - t0 + p.tstride - 1) / p.tstride : 0;
+  const int ks = p.ks;
 
   if (tid == 0) {
-    for (int i = 0; i < kXStages; ++i) {
+    for (int i = 0; i < G::XST; ++i) {
       mbar_init(&xfull[i], 1);
-      mbar_init(&xempty[i], kWorkWarps);
+      mbar_init(&xempty[i], kTrWarps);
     }
     for (int i = 0; i < 2; ++i) {
-      mbar_init(&afull[i], kWorkWarps);
+      mbar_init(&afull[i], kTrWarps);
       mbar_init(&aempty[i], 1);
+    }
+    for (int i = 0; i < 4; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], kWorkWarps);
+      mbar_init(&tempty[i], kEpiWarps / 2);
     }
     mbar_init(bload, 1);
     fence_mbar_init();
@@ -194,241 +290,292 @@ __global__ void __launch_bounds__(kThreads, 1) encode_tc_kernel(const __grid_con
   tc::fence_after();
   const uint32_t tbase = *s_tbase;
 
-  // codebook operands and statistics, once per CTA
+  // this subspace's operands and constants, once per CTA
   if (tid == 0) {
-    const uint32_t cbytes = (uint32_t)M * kN * 4, sbytes = (uint32_t)M * 16;
-    mbar_arrive_expect_tx(bload, bytesB + cbytes + sbytes);
-    for (uint32_t off = 0; off < bytesB; off += 32768)
-      bulk_g2s(sB + off, p.bprep + off, min(32768u, bytesB - off), bload);
-    bulk_g2s(s_cnc, p.cnc, cbytes, bload);
-    bulk_g2s(s_cstat, p.cstat, sbytes, bload);
+    const uint8_t* src = p.bprep + (size_t)m * G::B_BYTES;
+    mbar_arrive_expect_tx(bload, (uint32_t)G::B_BYTES + CST_LEN * 4);
+    for (uint32_t off = 0; off < (uint32_t)G::B_BYTES; off += 32768)
+      bulk_g2s(sB + off, src + off, min(32768u, (uint32_t)G::B_BYTES - off), bload);
+    bulk_g2s(s_cst, p.cst + (size_t)m * CST_LEN, CST_LEN * 4, bload);
   }
   mbar_wait(bload, 0);
 
   if (warp == 0) {
     // ---------------- TMA producer ----------------
     if (lane == 0) {
+      const uint32_t xbytes = (uint32_t)(kRows * ks * 4);
       for (int w = 0; w < items; ++w) {
-        const int t = (int)blockIdx.x + (w / M) * (int)gridDim.x, m = w % M;
-        const int xs = w % kXStages;
-        const uint32_t ph = (uint32_t)((w / kXStages) & 1);
-        mbar_wait(&xempty[xs], ph ^ 1u);
-        mbar_arrive_expect_tx(&xfull[xs], X_STAGE);
-        tma_load_2d(sX + xs * X_STAGE, &tmap, m * KP, t * kRows, &xfull[xs]);
+        const int t = t0 + w * p.tstride;
+        const int xs = w % G::XST;
+        mbar_wait(&xempty[xs], (uint32_t)(((w / G::XST) & 1) ^ 1));
+        mbar_arrive_expect_tx(&xfull[xs], xbytes);
+        uint8_t* dst = sX + xs * G::X_STAGE;
+        if (KP == 64) {  // two 32-float swizzled boxes
+          tma_load_2d(dst, &tmap, m * ks, t * kRows, &xfull[xs]);
+          tma_load_2d(dst + kRows * 128, &tmap, m * ks + 32, t * kRows, &xfull[xs]);
+        } else {
+          tma_load_2d(dst, &tmap, m * ks, t * kRows, &xfull[xs]);
+        }
       }
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer ----------------
     if (lane == 0) {
-      const uint32_t idesc = tc::idesc_f16_f32(kRows, kN);
-      const uint32_t sbo = (uint32_t)(KP / 8) * 128;
+      // two N = 128 halves per accumulator, each released separately by the epilogue, so
+      // that the next item's first half runs while the epilogue still reads the second
+      const uint32_t idesc = tc::idesc_f16_f32(kRows, kN / 2);
+      constexpr uint32_t sboE = (uint32_t)(KE / 8) * 128, sboP = (uint32_t)(KP / 8) * 128;
+      const uint32_t b_hi0 = smem_u32(sB), b_lo0 = smem_u32(sB + G::B_HI);
       for (int w = 0; w < items; ++w) {
-        const int m = w % M, ab = w & 1;
+        const int ab = w & 1;
         const uint32_t ph = (uint32_t)((w >> 1) & 1);
-        mbar_wait(&afull[ab], ph);
-        mbar_wait(&tempty[ab], ph ^ 1u);
+        mbar_wait_spin(&afull[ab], ph);
         tc::fence_after();
         int lo_any = 0;
 #pragma unroll
-        for (int j = 0; j < kWorkWarps; ++j) lo_any |= s_lo[ab * kWorkWarps + j];
-        const uint32_t a_hi = smem_u32(sA + (ab * 2 + 0) * A_PART), a_lo = smem_u32(sA + (ab * 2 + 1) * A_PART);
-        const uint32_t b_hi = smem_u32(sB + (m * 2 + 0) * B_PART), b_lo = smem_u32(sB + (m * 2 + 1) * B_PART);
-        const uint32_t tacc = tbase + (uint32_t)ab * kN;
-        uint32_t acc = 0;
+        for (int j = 0; j < kTrWarps; ++j) lo_any |= s_lo[ab * kTrWarps + j];
+        const uint32_t a_hi = smem_u32(sA + ab * G::A_BYTES), a_lo = a_hi + G::A_HI;
 #pragma unroll
-        for (int s = 0; s < KP / 16; ++s) {
-          tc::mma_f16(tacc, tc::smem_desc(a_hi + s * 256, 128, sbo), tc::smem_desc(b_hi + s * 256, 128, sbo), idesc, acc);
-          acc = 1;
-        }
-#pragma unroll
-        for (int s = 0; s < KP / 16; ++s)
-          tc::mma_f16(tacc, tc::smem_desc(a_hi + s * 256, 128, sbo), tc::smem_desc(b_lo + s * 256, 128, sbo), idesc, 1);
-        if (lo_any) {
+        for (int hf = 0; hf < 2; ++hf) {
+          mbar_wait_spin(&tempty[2 * ab + hf], ph ^ 1u);
+          tc::fence_after();
+          const uint32_t tacc = tbase + (uint32_t)ab * kN + (uint32_t)hf * (kN / 2);
+          const uint32_t b_hi = b_hi0 + (uint32_t)hf * 16u * sboE, b_lo = b_lo0 + (uint32_t)hf * 16u * sboP;
+          // hi . hi, hi . lo, [lo . hi], then the |c|^2 / |x|^2 extension block last, so that
+          // the large extension terms enter the accumulator in a single instruction
 #pragma unroll
           for (int s = 0; s < KP / 16; ++s)
-            tc::mma_f16(tacc, tc::smem_desc(a_lo + s * 256, 128, sbo), tc::smem_desc(b_hi + s * 256, 128, sbo), idesc, 1);
+            tc::mma_f16(tacc, tc::smem_desc(a_hi + s * 256, 128, sboE), tc::smem_desc(b_hi + s * 256, 128, sboE), idesc,
+                        s > 0 ? 1u : 0u);
+#pragma unroll
+          for (int s = 0; s < KP / 16; ++s)
+            tc::mma_f16(tacc, tc::smem_desc(a_hi + s * 256, 128, sboE), tc::smem_desc(b_lo + s * 256, 128, sboP), idesc,
+                        1u);
+          if (lo_any) {
+#pragma unroll
+            for (int s = 0; s < KP / 16; ++s)
+              tc::mma_f16(tacc, tc::smem_desc(a_lo + s * 256, 128, sboP), tc::smem_desc(b_hi + s * 256, 128, sboE),
+                          idesc, 1u);
+          }
+          tc::mma_f16(tacc, tc::smem_desc(a_hi + (KP / 16) * 256, 128, sboE),
+                      tc::smem_desc(b_hi + (KP / 16) * 256, 128, sboE), idesc, 1u);
+          tc::commit(&tfull[2 * ab + hf]);
         }
         tc::commit(&aempty[ab]);
-        tc::commit(&tfull[ab]);
+      }
+    }
+  } else if (warp < 2 + kEpiWarps) {
+    // ---------------- epilogue warps: whole rows of one accumulator ----------------
+    const int ew = warp - 2;
+    const int q = warp & 3;   // TMEM lane quadrant (warp % 4)
+    const int e = ew >> 2;    // accumulator / item parity
+    const int er = 32 * q + lane;
+    const uint32_t kmask = p.keymask, kone = p.one;
+    // tensor-core accumulation model: an MMA instruction adds 16 products to the
+    // accumulator with error <= 17 * 2^-23 * max(|addend|); the main passes (2 KP/16
+    // instructions, 3 KP/16 for a row whose x is not exactly fp16: adding the exact zeros
+    // of lo . hi leaves an accumulator unchanged) have every addend and partial sum bounded
+    // by P, the extension instruction (7 nonzero addends) by P + |c|^2 + |x|^2
+    const float eps_main2 = (float)(17 * 2 * KP / 16) * 1.1920928955078125e-07f;
+    const float eps_main3 = (float)(17 * 3 * KP / 16) * 1.1920928955078125e-07f;
+    const float eps_ext = 7.0f * 1.1920928955078125e-07f;
+    const float cb = s_cst[CST_CB], cnm = s_cst[CST_CN], s1c = s_cst[CST_S1C];
+    for (int w = e; w < items; w += 2) {
+      const int t = t0 + w * p.tstride;
+      const uint32_t ph = (uint32_t)((w >> 1) & 1);
+      mbar_wait(&tfull[2 * e], ph);
+      tc::fence_after();
+      const float4 st = s_stats[(w & 3) * kRows + er];  // x2u, |s x|, ok
+      const uint32_t tacc = tbase + (uint32_t)e * kN + ((uint32_t)(32 * q) << 16);
+      int B = 0x7fffffff, R = 0x7fffffff, Bi = 0;
+      uint32_t ka[32], kb[32];
+      tmem_ld32(tacc, ka);
+#pragma unroll
+      for (int c = 0; c < kN / kChunk; c += 2) {
+        tmem_wait32(ka);
+        tmem_ld32(tacc + (uint32_t)((c + 1) * kChunk), kb);
+        int bc, rc;
+        chunk_best(ka, kmask, kone, bc, rc);
+        if ((bc & ~31) < (B & ~31)) {  // strictly smaller value: ties keep the earlier chunk
+          R = min(B, rc);
+          B = bc;
+          Bi = c;
+        } else {
+          R = min(R, bc);
+        }
+        tmem_wait32(kb);
+        if (c + 2 == kN / kChunk / 2 || c + 2 == kN / kChunk) {  // a column half fully read
+          tc::fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty[2 * e + (c + 2 == kN / kChunk ? 1 : 0)]);
+        }
+        if (c + 2 < kN / kChunk) {
+          if (c + 2 == kN / kChunk / 2) {
+            mbar_wait(&tfull[2 * e + 1], ph);
+            tc::fence_after();
+          }
+          tmem_ld32(tacc + (uint32_t)((c + 2) * kChunk), ka);
+        }
+        chunk_best(kb, kmask, kone, bc, rc);
+        if ((bc & ~31) < (B & ~31)) {
+          R = min(B, rc);
+          B = bc;
+          Bi = c + 1;
+        } else {
+          R = min(R, bc);
+        }
+      }
+      const int64_t n = (int64_t)t * kRows + er;
+      if (n < p.n) {
+        // keys dropped 5 mantissa bits: the value lies within 32 ulp <= 2^-18 |v| of the key
+        // value, above it for v >= 0 and below it for v < 0
+        const float wv = __int_as_float(B & ~31), rv = __int_as_float(R & ~31);
+        const float w_hi = wv >= 0.f ? wv * 1.00000762939453125f : wv;  // 1 + 2^-17
+        const float r_lo = rv >= 0.f ? rv : rv * 1.00000762939453125f;
+        // rigorous bound on |computed - exact| of any D_rj (see header)
+        const float P = st.y * cb * 1.001f;  // >= sum |split products|
+        const float E = (st.w != 0.f ? eps_main3 : eps_main2) * P + eps_ext * (P + cnm + st.x) * 1.001f                  //
+                        + 4.76837158203125e-07f * P                                          // 4 * 2^-23
+                        + 2.98023223876953125e-08f * (sqrtf((float)KP) * st.y + s1c)          // 2^-25
+                        + 9.313225746154785e-10f * (cnm + st.x)                               // 2^-30
+                        + 1e-3f;
+        const bool cert = st.z != 0.f && (r_lo - w_hi) > 2.0f * E * 1.0001f;
+        if (cert) {
+          p.codes[n * p.stride + m] = (uint8_t)(kChunk * Bi + (B & 31));
+        } else {
+          atomicAdd(&p.counters[0], 1u);
+          const unsigned f = atomicAdd(&p.counters[2 + m], 1u);
+          if (f < p.flag_cap)
+            p.flags[(size_t)m * p.flag_cap + f] = (uint32_t)n;
+          else
+            p.counters[1] = 1u;
+        }
       }
     }
   } else {
-    // ---------------- transform + epilogue warps ----------------
-    const int ww = warp - 2;
-    constexpr int TPR = 4;                                   // transform: threads per row
-    constexpr int VPT = KP / TPR;                            // floats per thread
-    const int tr = (kRows / kWorkWarps) * ww + lane / TPR;  // 8 rows per warp
-    const int th = lane % TPR;
-    const int q = warp & 3, h = ww >> 2;                     // epilogue: TMEM lane quadrant, column quarter
-    const int er = 32 * q + lane;
-    const float eps = (float)(KP + 11) * 2.384185791015625e-07f;  // (KP+11) * 2^-22
-
-    auto transform = [&](int w) {
-      const int ab = w & 1, xs = w % kXStages;
-      mbar_wait(&xfull[xs], (uint32_t)((w / kXStages) & 1));
-      const float* xr = reinterpret_cast<const float*>(sX + xs * X_STAGE) + tr * KP + th * VPT;
-      float v[VPT];
+    // ---------------- transform warps: 16 rows each, 2 passes of 8 ----------------
+    const int tw = warp - 2 - kEpiWarps;
+    constexpr int VPT = KP / 4;  // columns per thread; 4 threads per row (lanes r, r+8, r+16, r+24)
+    const int th = lane >> 3;
+    const float sc = s_cst[CST_S];
+    const __half acn = __float2half_rn(s_cst[CST_ACN]);
+    const bool valid = s_cst[CST_VALID] != 0.f;
+    const bool has_x = th * VPT < ks;  // dsub = 8 < KP = 16: the upper half is zero padding
+    for (int w = 0; w < items; ++w) {
+      const int ab = w & 1, xs = w % G::XST;
+      mbar_wait(&xfull[xs], (uint32_t)((w / G::XST) & 1));
+      float v[2][VPT];
 #pragma unroll
-      for (int j = 0; j < VPT; j += 4) {
-        const float4 f = *reinterpret_cast<const float4*>(xr + j);
-        v[j] = f.x;
-        v[j + 1] = f.y;
-        v[j + 2] = f.z;
-        v[j + 3] = f.w;
+      for (int ps = 0; ps < 2; ++ps) {
+        const int r = 16 * tw + 8 * ps + (lane & 7);
+        const uint8_t* xb = sX + xs * G::X_STAGE;
+        if (G::SWZ) {
+          // 128-byte rows of 8 x 16-byte chunks, chunk index XOR (row % 8)
+#pragma unroll
+          for (int cc = 0; cc < VPT / 4; ++cc) {
+            const int chunk = th * (VPT / 4) + cc;  // 16-byte chunk of the row
+            const int half = chunk >> 3, ch = chunk & 7;
+            const float4 f = *reinterpret_cast<const float4*>(xb + half * (kRows * 128) + r * 128 + ((ch ^ (r & 7)) << 4));
+            v[ps][4 * cc] = f.x;
+            v[ps][4 * cc + 1] = f.y;
+            v[ps][4 * cc + 2] = f.z;
+            v[ps][4 * cc + 3] = f.w;
+          }
+        } else if (has_x) {
+          const float* xr = reinterpret_cast<const float*>(xb) + r * ks + th * VPT;
+#pragma unroll
+          for (int j = 0; j < VPT; j += 4) {
+            const float4 f = *reinterpret_cast<const float4*>(xr + j);
+            v[ps][j] = f.x;
+            v[ps][j + 1] = f.y;
+            v[ps][j + 2] = f.z;
+            v[ps][j + 3] = f.w;
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < VPT; ++j) v[ps][j] = 0.f;
+        }
       }
-      float amax = 0.f;
-#pragma unroll
-      for (int j = 0; j < VPT; ++j) amax = fmaxf(amax, fabsf(v[j]));
-      amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, 1));
-      amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, 2));  // every lane has consumed its loads
+      __syncwarp();
       if (lane == 0) mbar_arrive(&xempty[xs]);
-      int ex = 0;
-      const bool fin = amax > 0.f && amax <= 3.4e38f;
-      if (fin) frexpf(amax, &ex);
-      const float scale = fin ? ldexpf(1.0f, 14 - ex) : 1.0f;
-      uint32_t hw[VPT / 2], lw[VPT / 2];
-      float x2 = 0.f, x1 = 0.f;
-      int lo_nz = 0;
+      uint32_t hw[2][VPT / 2], lw[2][VPT / 2];
+      float x2[2];
+      uint32_t lo_nz = 0, lo_row[2];
 #pragma unroll
-      for (int j = 0; j < VPT; j += 2) {
-        const float s0 = v[j] * scale, s1 = v[j + 1] * scale;
-        const __half h0 = __float2half_rn(s0), h1 = __float2half_rn(s1);
-        const __half l0 = __float2half_rn(s0 - __half2float(h0)), l1 = __float2half_rn(s1 - __half2float(h1));
-        lo_nz |= ((__half_as_ushort(l0) | __half_as_ushort(l1)) & 0x7fff) != 0;
-        hw[j / 2] = __half_as_ushort(h0) | ((uint32_t)__half_as_ushort(h1) << 16);
-        lw[j / 2] = __half_as_ushort(l0) | ((uint32_t)__half_as_ushort(l1) << 16);
-        x2 = fmaf(s0, s0, fmaf(s1, s1, x2));
-        x1 += fabsf(s0) + fabsf(s1);
+      for (int ps = 0; ps < 2; ++ps) {
+        float acc = 0.f;
+        uint32_t lr = 0;
+#pragma unroll
+        for (int j = 0; j < VPT; j += 2) {
+          const float a0 = v[ps][j] * sc, a1 = v[ps][j + 1] * sc;
+          const __half2 hh = __floats2half2_rn(a0, a1);
+          const float2 hf = __half22float2(hh);
+          const __half2 ll = __floats2half2_rn(a0 - hf.x, a1 - hf.y);
+          hw[ps][j / 2] = *reinterpret_cast<const uint32_t*>(&hh);
+          lw[ps][j / 2] = *reinterpret_cast<const uint32_t*>(&ll);
+          lr |= lw[ps][j / 2];
+          acc = fmaf(a0, a0, fmaf(a1, a1, acc));
+        }
+        acc += __shfl_xor_sync(0xffffffffu, acc, 8);
+        acc += __shfl_xor_sync(0xffffffffu, acc, 16);
+        x2[ps] = acc;
+        lr &= 0x7fff7fffu;
+        lr |= __shfl_xor_sync(0xffffffffu, lr, 8);
+        lr |= __shfl_xor_sync(0xffffffffu, lr, 16);
+        lo_row[ps] = lr;
+        lo_nz |= lr;
       }
-      x2 += __shfl_xor_sync(0xffffffffu, x2, 1);
-      x2 += __shfl_xor_sync(0xffffffffu, x2, 2);
-      x1 += __shfl_xor_sync(0xffffffffu, x1, 1);
-      x1 += __shfl_xor_sync(0xffffffffu, x1, 2);
-      const unsigned bal = __ballot_sync(0xffffffffu, lo_nz);
+      const unsigned bal = __ballot_sync(0xffffffffu, lo_nz != 0);
       mbar_wait(&aempty[ab], (uint32_t)(((w >> 1) & 1) ^ 1));
-      uint8_t* ahi = sA + (ab * 2 + 0) * A_PART;
-      uint8_t* alo = sA + (ab * 2 + 1) * A_PART;
+      uint8_t* ahi = sA + ab * G::A_BYTES;
+      uint8_t* alo = ahi + G::A_HI;
 #pragma unroll
-      for (int c = 0; c < VPT / 8; ++c) {
-        const int k = th * VPT + 8 * c;
-        *reinterpret_cast<uint4*>(ahi + tc::kmajor_off(tr, k, KP)) =
-            make_uint4(hw[4 * c], hw[4 * c + 1], hw[4 * c + 2], hw[4 * c + 3]);
-        *reinterpret_cast<uint4*>(alo + tc::kmajor_off(tr, k, KP)) =
-            make_uint4(lw[4 * c], lw[4 * c + 1], lw[4 * c + 2], lw[4 * c + 3]);
+      for (int ps = 0; ps < 2; ++ps) {
+        const int r = 16 * tw + 8 * ps + (lane & 7);
+        // |s x|^2 rounded up (fp32 sum of KP products: relative error < (KP+4) 2^-24)
+        const float x2u = x2[ps] * (1.0f + (float)(KP + 8) * 5.9604644775390625e-08f);
+        const bool ok = valid && (x2u < kX2Limit);  // false for NaN / inf / out-of-range rows
+        if (!ok) {
+#pragma unroll
+          for (int j = 0; j < VPT / 2; ++j) hw[ps][j] = lw[ps][j] = 0u;
+        }
+#pragma unroll
+        for (int c = 0; c < VPT / 8; ++c) {
+          const int k = th * VPT + 8 * c;
+          *reinterpret_cast<uint4*>(ahi + tc::kmajor_off(r, k, KE)) =
+              make_uint4(hw[ps][4 * c], hw[ps][4 * c + 1], hw[ps][4 * c + 2], hw[ps][4 * c + 3]);
+          *reinterpret_cast<uint4*>(alo + tc::kmajor_off(r, k, KP)) =
+              make_uint4(lw[ps][4 * c], lw[ps][4 * c + 1], lw[ps][4 * c + 2], lw[ps][4 * c + 3]);
+        }
+        if (VPT % 8) {  // KP = 16: 4 columns per thread, half a core-matrix row
+          const int k = th * VPT;
+          *reinterpret_cast<uint2*>(ahi + tc::kmajor_off(r, k, KE)) = make_uint2(hw[ps][0], hw[ps][1]);
+          *reinterpret_cast<uint2*>(alo + tc::kmajor_off(r, k, KP)) = make_uint2(lw[ps][0], lw[ps][1]);
+        }
+        if (th == 0) {
+          // extension columns: [acn x3, |s x|^2 parts (x 2^15), 2^15 (padding codewords), 0...]
+          const float xv = ok ? x2u * 3.0517578125e-05f : 0.f;  // 2^-15, exact
+          const __half x_h = __float2half_rn(xv);
+          const float r1 = xv - __half2float(x_h);
+          const __half x_m = __float2half_rn(r1);
+          const __half x_l = __float2half_rn(r1 - __half2float(x_m));
+          const __half p15 = __float2half_rn(32768.f);
+          const __half z = __float2half_rn(0.f);
+          *reinterpret_cast<uint4*>(ahi + tc::kmajor_off(r, KP, KE)) =
+              make_uint4(pack_h2(acn, acn), pack_h2(acn, x_h), pack_h2(x_m, x_l), pack_h2(p15, z));
+          *reinterpret_cast<uint4*>(ahi + tc::kmajor_off(r, KP + 8, KE)) = make_uint4(0u, 0u, 0u, 0u);
+          // |s x| rounded up: sqrt.approx has relative error < 2^-21
+          float xn;
+          asm("sqrt.approx.f32 %0, %1;" : "=f"(xn) : "f"(x2u));
+          // 4 stats buffers: transform(w + 4) waits for MMA(w + 2), which waits for every
+          // epilogue warp of parity w to have read item w's stats
+          s_stats[(w & 3) * kRows + r] = make_float4(x2u, xn * 1.000002f, ok ? 1.f : 0.f, lo_row[ps] ? 1.f : 0.f);
+        }
       }
-      if (VPT % 8) {  // KP = 16: 4 floats per thread, half a 16-byte chunk
-        const int k = th * VPT;
-        *reinterpret_cast<uint2*>(ahi + tc::kmajor_off(tr, k, KP)) = make_uint2(hw[0], hw[1]);
-        *reinterpret_cast<uint2*>(alo + tc::kmajor_off(tr, k, KP)) = make_uint2(lw[0], lw[1]);
-      }
-      // 4 stats buffers: a warp can run at most 3 items ahead of the slowest epilogue
-      // reader (MMA(w+2) waits for every warp's tempty arrival of item w)
-      if (th == 0) s_stats[(w & 3) * kRows + tr] = make_float4(scale, sqrtf(x2) * 1.00001f, x1 * 1.00001f, 0.f);
-      if (lane == 0) s_lo[ab * kWorkWarps + ww] = (bal != 0);
+      if (lane == 0) s_lo[ab * kTrWarps + tw] = (bal != 0);
       tc::fence_proxy_async();
       __syncwarp();
       if (lane == 0) mbar_arrive(&afull[ab]);
-    };
-
-    auto epilogue = [&](int w) {
-      const int m = w % M, ab = w & 1;
-      const int t = (int)blockIdx.x + (w / M) * (int)gridDim.x;
-      mbar_wait(&tfull[ab], (uint32_t)((w >> 1) & 1));
-      tc::fence_after();
-      const float4 st = s_stats[(w & 3) * kRows + er];
-      const float4 cs = *reinterpret_cast<const float4*>(s_cstat + 4 * m);  // C2, C1, CN, s_c
-      const float sr = st.x, x2 = st.y, x1 = st.z;
-      // rigorous bound on |computed - exact| of g = s_r s_c (|c|^2 - 2 x.c) (see header)
-      const float dS = eps * x2 * cs.x + 2.98023223876953125e-08f * (x1 + cs.y);  // 2^-25
-      const float big = sr * cs.z + x2 * cs.x;
-      const float dg = 2.0f * dS + 1.1920928955078125e-07f * big;                // 2^-23
-      const float margin = 2.0f * dg * 1.001f + 1e-12f * big;
-      // e'_l = s_c |x - c_l|^2 = cnc_l - (2/s_r) S'_l + s_c |x|^2 >= 0 (offset widened by the
-      // error bound so that every computed e' is nonnegative: its bits then order as uint)
-      const float nsr = -2.0f / sr;
-      const float off = cs.w * (x2 * x2) / (sr * sr) * 1.0001f + 2.0f * dg / sr;
-      const float* cn = s_cnc + m * kN + 64 * h;
-      uint32_t k[64];
-      const uint32_t tacc = tbase + (uint32_t)ab * kN + 64u * h + ((uint32_t)(32 * q) << 16);
-      {
-        uint32_t r0[16], r1[16], r2[16], r3[16];
-        tc::tmem_ld16(tacc + 0, r0);
-        tc::tmem_ld16(tacc + 16, r1);
-        tc::tmem_ld16(tacc + 32, r2);
-        tc::tmem_ld16(tacc + 48, r3);
-        tc::tmem_wait_ld();
-#pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          k[j] = r0[j];
-          k[16 + j] = r1[j];
-          k[32 + j] = r2[j];
-          k[48 + j] = r3[j];
-        }
-      }
-      tc::fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[ab]);
-      // keys: e' bits with the low 6 mantissa bits replaced by the column (one LOP3 each)
-#pragma unroll
-      for (int j = 0; j < 64; ++j) {
-        const float e = fmaf(__uint_as_float(k[j]), nsr, cn[j]) + off;
-        k[j] = (__float_as_uint(e) & ~63u) | (uint32_t)j;
-      }
-      uint32_t b = k[0];
-#pragma unroll
-      for (int j = 1; j + 1 < 64; j += 2) b = min(b, min(k[j], k[j + 1]));
-      b = min(b, k[63]);
-      // runner-up key: keys are unique, so min over (k - (b + 1)) mod 2^32 maps the winner
-      // to 0xffffffff and every other key k to k - b - 1 (order preserved)
-      const uint32_t bp = b + 1u;
-      uint32_t rr = 0xffffffffu;
-#pragma unroll
-      for (int j = 0; j < 64; j += 2) rr = min(rr, min(k[j] - bp, k[j + 1] - bp));
-      rr += bp;
-      // merge the four column quarters of each row (warps sharing quadrant q)
-      if (h > 0) s_merge[(h - 1) * kRows + er] = make_float4(__uint_as_float(b), __uint_as_float(rr), 0.f, 0.f);
-      named_bar(1 + q, 128);
-      if (h == 0) {
-        uint32_t wb = b, wr = rr;
-        int wh = 0;
-        float other = __int_as_float(0x7f800000);  // min lower bound of losing quarters' winners
-#pragma unroll
-        for (int u = 1; u < 4; ++u) {
-          const float4 o = s_merge[(u - 1) * kRows + er];
-          const uint32_t ob = __float_as_uint(o.x);
-          if ((ob & ~63u) < (wb & ~63u)) {  // strictly smaller value: ties keep the lower quarter
-            other = fminf(other, __uint_as_float(wb & ~63u));
-            wb = ob;
-            wr = __float_as_uint(o.y);
-            wh = u;
-          } else {
-            other = fminf(other, __uint_as_float(ob & ~63u));
-          }
-        }
-        const int64_t n = (int64_t)t * kRows + er;
-        if (n < p.n) {
-          const float w_hi = __uint_as_float((wb & ~63u) | 63u);
-          const float r_lo = fminf(__uint_as_float(wr & ~63u), other);
-          // e' values are g/s_r units; a non-finite row makes the margin NaN/inf
-          const bool cert = (r_lo - w_hi) * sr > margin;
-          if (cert) {
-            p.codes[n * p.stride + m] = (uint8_t)(64 * wh + (int)(wb & 63u));
-          } else {
-            const unsigned f = atomicAdd(&p.counters[0], 1u);
-            if (f < p.flag_cap)
-              p.flags[f] = (uint32_t)(n * M + m);
-            else
-              p.counters[1] = 1u;
-          }
-        }
-      }
-      named_bar(1 + q, 128);  // s_merge is reused by the next item
-    };
-
-    if (items > 0) transform(0);
-    for (int w = 0; w < items; ++w) {
-      if (w + 1 < items) transform(w + 1);
-      epilogue(w);
     }
   }
   tc::fence_before();
@@ -439,103 +586,193 @@ __global__ void __launch_bounds__(kThreads, 1) encode_tc_kernel(const __grid_con
   }
 }
 
-// Codebook preparation: one block of 256 threads per subspace.
+// Codebook preparation: one block of 256 threads (one per codeword slot) per subspace.
+// B = -2 s c split into fp16 hi/lo (K-major, zero-padded to KP), extension row
+// [cn parts, 2^15 x3, padding, 0...] with cn = s^2 |c|^2 / acn in three fp16 parts, and
+// the constants of the epilogue's error bound.
 template <int KP>
 __global__ void __launch_bounds__(256) encode_prep_kernel(const float* __restrict__ cw, int m, int l, int ks,
-                                                         uint8_t* __restrict__ bprep, float* __restrict__ cnc,
-                                                         float* __restrict__ cstat) {
+                                                         uint8_t* __restrict__ bprep, float* __restrict__ cst) {
+  using G = Geo<KP>;
+  constexpr int KE = G::KE;
   __shared__ float red[8];
-  __shared__ float s_scale;
+  __shared__ int bad[8];
+  __shared__ double redd[8];
+  __shared__ float s_sc;
+  __shared__ int s_bad;
+  __shared__ double s_cn;
   const int mm = blockIdx.x, row = threadIdx.x, lane = row & 31, warp = row >> 5;
-  const float* c = cw + ((size_t)mm * l + row) * ks;
+  const bool real = row < l;
+  const float* c = cw + ((size_t)mm * l + (real ? row : 0)) * ks;
   float amax = 0.f;
-  if (row < l)
-    for (int k = 0; k < ks; ++k) amax = fmaxf(amax, fabsf(c[k]));
-  for (int o = 16; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
-  if (lane == 0) red[warp] = amax;
+  int nonfinite = 0;
+  if (real)
+    for (int k = 0; k < ks; ++k) {
+      const float a = fabsf(c[k]);
+      nonfinite |= !(a <= 3.4028234663852886e38f);
+      amax = fmaxf(amax, a);
+    }
+  for (int o = 16; o > 0; o >>= 1) {
+    amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+    nonfinite |= __shfl_xor_sync(0xffffffffu, nonfinite, o);
+  }
+  if (lane == 0) {
+    red[warp] = amax;
+    bad[warp] = nonfinite;
+  }
   __syncthreads();
   if (row == 0) {
     float a = 0.f;
-    for (int i = 0; i < 8; ++i) a = fmaxf(a, red[i]);
+    int b = 0;
+    for (int i = 0; i < 8; ++i) {
+      a = fmaxf(a, red[i]);
+      b |= bad[i];
+    }
     int ex = 0;
-    if (a > 0.f) frexpf(a, &ex);
-    s_scale = a > 0.f ? ldexpf(1.0f, 14 - ex) : 1.0f;
+    if (a > 0.f && !b) frexpf(a, &ex);  // a in [2^(ex-1), 2^ex)
+    // |s c| < 2^8: vectors up to ~2^8 x the codebook's range stay inside the fp16
+    // operand and |s x|^2 < 2^30 extension ranges (others take the exact path)
+    s_sc = (a > 0.f && !b) ? ldexpf(1.0f, 8 - ex) : 1.0f;
+    s_bad = b;
   }
   __syncthreads();
-  const float sc = s_scale;
-  uint8_t* bh = bprep + (size_t)(mm * 2 + 0) * kN * KP * 2;
-  uint8_t* bl = bprep + (size_t)(mm * 2 + 1) * kN * KP * 2;
-  double nn = 0.0;
-  float c2 = 0.f, c1 = 0.f;
+  const float sc = s_sc;
+  const bool cb_ok = !s_bad;
+  uint8_t* bh = bprep + (size_t)mm * G::B_BYTES;
+  uint8_t* bl = bh + G::B_HI;
+  double cn = 0.0, nb2 = 0.0, s1 = 0.0;
   for (int k = 0; k < KP; ++k) {
-    const float v = (row < l && k < ks) ? c[k] * sc : 0.f;
-    const __half hi = __float2half_rn(v);
-    const __half lo = __float2half_rn(v - __half2float(hi));
-    *reinterpret_cast<__half*>(bh + tc::kmajor_off(row, k, KP)) = hi;
+    const float cv = (real && cb_ok && k < ks) ? c[k] * sc : 0.f;  // exact (power-of-two scale)
+    const float bv = -2.0f * cv;
+    const __half hi = __float2half_rn(bv);
+    const __half lo = __float2half_rn(bv - __half2float(hi));
+    *reinterpret_cast<__half*>(bh + tc::kmajor_off(row, k, KE)) = hi;
     *reinterpret_cast<__half*>(bl + tc::kmajor_off(row, k, KP)) = lo;
-    if (row < l && k < ks) {
-      const double cd = (double)c[k];
-      nn += cd * cd;
-    }
-    c2 = fmaf(v, v, c2);
-    c1 += fabsf(v);
+    cn += (double)cv * (double)cv;
+    nb2 += (double)bv * (double)bv;
+    s1 += fabs((double)bv);
   }
-  const float cn = row < l ? (float)(nn * (double)sc) : __int_as_float(0x7f800000);
-  cnc[mm * kN + row] = cn;
-  // block maxima of C2, C1, CN over real rows
-  float v2 = row < l ? sqrtf(c2) * 1.00001f : 0.f, v1 = row < l ? c1 * 1.00001f : 0.f, vn = row < l ? cn : 0.f;
+  // block maximum of cn -> acn = 2^a with cn / acn < 2^15 (cn < KP 2^16 <= 2^22: a <= 8)
+  double cmx = cn;
+  for (int o = 16; o > 0; o >>= 1) cmx = fmax(cmx, __shfl_xor_sync(0xffffffffu, cmx, o));
+  if (lane == 0) redd[warp] = cmx;
+  __syncthreads();
+  if (row == 0) {
+    double a = 0.0;
+    for (int i = 0; i < 8; ++i) a = fmax(a, redd[i]);
+    s_cn = a;
+  }
+  __syncthreads();
+  int ea = 0;
+  if (s_cn >= 16384.0) {
+    frexp(s_cn, &ea);  // s_cn < 2^ea
+    ea -= 14;          // s_cn / 2^ea < 2^14
+  }
+  const double acn = ldexp(1.0, ea);
+  const double cv = cn / acn;
+  const __half c_h = __double2half(cv);
+  const double r1 = cv - (double)__half2float(c_h);
+  const __half c_m = __double2half(r1);
+  const __half c_l = __double2half(r1 - (double)__half2float(c_m));
+  const __half p15 = __float2half_rn(32768.f);
+  const __half pad = __float2half_rn(real ? 0.f : 65504.f);
+  const __half z = __float2half_rn(0.f);
+  *reinterpret_cast<uint4*>(bh + tc::kmajor_off(row, KP, KE)) =
+      make_uint4(pack_h2(c_h, c_m), pack_h2(c_l, p15), pack_h2(p15, p15), pack_h2(pad, z));
+  *reinterpret_cast<uint4*>(bh + tc::kmajor_off(row, KP + 8, KE)) = make_uint4(0u, 0u, 0u, 0u);
+  // block maxima of |B_j|, cn_j, sum |B_j| over real rows
+  float vb = real ? (float)sqrt(nb2) : 0.f, vc = real ? (float)cn : 0.f, v1 = real ? (float)s1 : 0.f;
   for (int o = 16; o > 0; o >>= 1) {
-    v2 = fmaxf(v2, __shfl_xor_sync(0xffffffffu, v2, o));
+    vb = fmaxf(vb, __shfl_xor_sync(0xffffffffu, vb, o));
+    vc = fmaxf(vc, __shfl_xor_sync(0xffffffffu, vc, o));
     v1 = fmaxf(v1, __shfl_xor_sync(0xffffffffu, v1, o));
-    vn = fmaxf(vn, __shfl_xor_sync(0xffffffffu, vn, o));
   }
-  __shared__ float r2[8], r1[8], rn[8];
+  __shared__ float rb[8], rc[8], r1s[8];
   if (lane == 0) {
-    r2[warp] = v2;
-    r1[warp] = v1;
-    rn[warp] = vn;
+    rb[warp] = vb;
+    rc[warp] = vc;
+    r1s[warp] = v1;
   }
   __syncthreads();
   if (row == 0) {
-    float a = 0.f, b = 0.f, d = 0.f;
+    float a = 0.f, b2 = 0.f, d = 0.f;
     for (int i = 0; i < 8; ++i) {
-      a = fmaxf(a, r2[i]);
-      b = fmaxf(b, r1[i]);
-      d = fmaxf(d, rn[i]);
+      a = fmaxf(a, rb[i]);
+      b2 = fmaxf(b2, rc[i]);
+      d = fmaxf(d, r1s[i]);
     }
-    cstat[4 * mm + 0] = a;
-    cstat[4 * mm + 1] = b;
-    cstat[4 * mm + 2] = d * 1.00001f;
-    cstat[4 * mm + 3] = sc;  // s_c: the epilogue's |x|^2 offset
+    float* o = cst + (size_t)mm * CST_LEN;
+    o[CST_S] = sc;
+    o[CST_ACN] = (float)acn;
+    o[CST_CB] = a * 1.0001f;
+    o[CST_CN] = b2 * 1.0001f;
+    o[CST_S1C] = d * 1.0001f;
+    o[CST_VALID] = cb_ok ? 1.f : 0.f;
+    o[6] = 0.f;
+    o[7] = 0.f;
   }
 }
 
-// Exact float64 decision for the pairs the certificate did not cover; one warp per pair.
-__global__ void encode_exact_kernel(const float* __restrict__ x, int64_t n, int d, const float* __restrict__ cw, int m,
-                                    int l, int ks, const uint32_t* __restrict__ flags,
-                                    const unsigned int* __restrict__ counters, uint32_t flag_cap,
-                                    uint8_t* __restrict__ codes, int stride) {
-  const int lane = threadIdx.x & 31;
-  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+// Exact float64 decision for the (row, subspace) pairs the certificate did not cover.
+// Block (x, m) holds subspace m's codebook in shared memory (row stride ks + 1: lanes
+// reading different codewords hit different banks); one warp per flagged row, each
+// lane owning codewords lane, lane + 32, ...; float64 (x - c)^2 summed sequentially
+// without FMA (scipy cdist order), np.argmin order (first NaN, else lowest index).
+__global__ void __launch_bounds__(256) encode_exact_kernel(const float* __restrict__ x, int64_t n, int d,
+                                                          const float* __restrict__ cw, int m, int l, int ks,
+                                                          const uint32_t* __restrict__ flags,
+                                                          const unsigned int* __restrict__ counters, uint32_t flag_cap,
+                                                          uint8_t* __restrict__ codes, int stride) {
+  extern __shared__ float s_cb[];
+  const int mm = blockIdx.y;
   const bool all = counters[1] != 0;
-  const int64_t total = all ? n * m : (int64_t)min(counters[0], flag_cap);
-  for (int64_t w = gw; w < total; w += nw) {
-    const int64_t pair = all ? w : (int64_t)flags[w];
-    const int64_t row = pair / m;
-    const int mm = (int)(pair - row * m);
+  const int64_t total = all ? n : (int64_t)min(counters[2 + mm], flag_cap);
+  if (total == 0 || (int64_t)blockIdx.x * 8 >= total) return;
+  const int sp = ks + 1;
+  const float* cb = cw + (size_t)mm * l * ks;
+  for (int i0 = threadIdx.x; i0 < l * ks; i0 += 8 * blockDim.x) {  // 8 loads in flight per thread
+    float v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int i = i0 + u * blockDim.x;
+      v[u] = i < l * ks ? __ldg(cb + i) : 0.f;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int i = i0 + u * blockDim.x;
+      if (i < l * ks) s_cb[(i / ks) * sp + (i % ks)] = v[u];
+    }
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int64_t i = (int64_t)blockIdx.x * 8 + warp; i < total; i += (int64_t)gridDim.x * 8) {
+    const int64_t row = all ? i : (int64_t)flags[(size_t)mm * flag_cap + i];
     const float* xv = x + row * d + (size_t)mm * ks;
+    const float x0 = lane < ks ? xv[lane] : 0.f, x1 = lane + 32 < ks ? xv[lane + 32] : 0.f;
+    double acc[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc[u] = 0.0;
+    // codewords c >= l alias codeword l - 1 (same distance, larger index: never chosen)
+    int cbase[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) cbase[u] = min(lane + 32 * u, l - 1) * sp;
+    for (int k = 0; k < ks; ++k) {
+      const double xk = (double)__shfl_sync(0xffffffffu, k < 32 ? x0 : x1, k & 31);
+      double df[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) df[u] = __dsub_rn(xk, (double)s_cb[cbase[u] + k]);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) df[u] = __dmul_rn(df[u], df[u]);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) acc[u] = __dadd_rn(acc[u], df[u]);
+    }
     double best = __longlong_as_double(0x7ff0000000000000LL);
     int bl = 0x7fffffff;
-    for (int c = lane; c < l; c += 32) {
-      const float* cv = cw + ((size_t)mm * l + c) * ks;
-      double acc = 0.0;
-      for (int k = 0; k < ks; ++k) {
-        const double df = __dsub_rn((double)xv[k], (double)cv[k]);
-        acc = __dadd_rn(acc, __dmul_rn(df, df));
-      }
-      if (argmin_less(acc, c, best, bl)) {
-        best = acc;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int c = lane + 32 * u;
+      if (argmin_less(acc[u], c, best, bl)) {
+        best = acc[u];
         bl = c;
       }
     }
@@ -580,19 +817,19 @@ PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
 }
 
 template <int KP>
-int launch_encode_tc(const float* d_x, int64_t n, int d, const float* d_cw, int m, int l, uint8_t* d_codes, int stride,
-                     unsigned long long* flagged_out, cudaStream_t stream) {
+int launch_encode_tc(const float* d_x, int64_t n, int d, const float* d_cw, int m, int l, int ks, uint8_t* d_codes,
+                     int stride, unsigned long long* flagged_out, cudaStream_t stream) {
   using namespace enc;
+  using G = Geo<KP>;
   const DevInfo& di = dev_info();
-  const size_t smem = smem_bytes<KP>(m);
   int dev = 0;
   cudaGetDevice(&dev);
   EncWS& ws = g_encws[dev & 63];
   std::lock_guard<std::mutex> lock(ws.mu);
-  const size_t b_bytes = (size_t)m * 2 * kN * KP * 2;
-  const uint32_t cap = (uint32_t)std::min<int64_t>(n * m, (int64_t)(n * m) / 64 + 65536);
-  const size_t need = align_up(b_bytes, 256) + align_up((size_t)m * kN * 4, 256) + align_up((size_t)m * 16, 256) +
-                      align_up((size_t)cap * 4, 256) + 256;
+  const size_t b_bytes = (size_t)m * G::B_BYTES;
+  const uint32_t cap = (uint32_t)std::min<int64_t>(n, n / 128 + 4096);  // flagged rows per subspace
+  const size_t need = align_up(b_bytes, 256) + align_up((size_t)m * CST_LEN * 4, 256) +
+                      align_up((size_t)m * cap * 4, 256) + align_up((size_t)(m + 2) * 4, 256);
   if (ws.bytes < need) {
     if (ws.p) cudaFree(ws.p);
     ws.p = nullptr;
@@ -602,49 +839,51 @@ int launch_encode_tc(const float* d_x, int64_t n, int d, const float* d_cw, int 
   }
   char* base = static_cast<char*>(ws.p);
   uint8_t* bprep = reinterpret_cast<uint8_t*>(base);
-  float* cnc = reinterpret_cast<float*>(base + align_up(b_bytes, 256));
-  float* cstat = reinterpret_cast<float*>(reinterpret_cast<char*>(cnc) + align_up((size_t)m * kN * 4, 256));
-  uint32_t* flags = reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(cstat) + align_up((size_t)m * 16, 256));
-  unsigned int* counters = reinterpret_cast<unsigned int*>(reinterpret_cast<char*>(flags) + align_up((size_t)cap * 4, 256));
+  float* cst = reinterpret_cast<float*>(base + align_up(b_bytes, 256));
+  uint32_t* flags = reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(cst) + align_up((size_t)m * CST_LEN * 4, 256));
+  unsigned int* counters =
+      reinterpret_cast<unsigned int*>(reinterpret_cast<char*>(flags) + align_up((size_t)m * cap * 4, 256));
 
   CUtensorMap map;
   auto encoder = tensor_map_encoder();
   if (!encoder) return fail(PQK_ECUDA, "cuTensorMapEncodeTiled unavailable");
   const cuuint64_t dims[2] = {(cuuint64_t)d, (cuuint64_t)n};
   const cuuint64_t strides[1] = {(cuuint64_t)d * 4};
-  const cuuint32_t box[2] = {(cuuint32_t)KP, (cuuint32_t)kRows};
+  const cuuint32_t box[2] = {(cuuint32_t)std::min(ks, 32), (cuuint32_t)kRows};
   const cuuint32_t estr[2] = {1, 1};
   const CUresult cr = encoder(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(d_x), dims, strides, box,
-                              estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                              estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                              ks >= 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (cr != CUDA_SUCCESS) return fail(PQK_ECUDA, "cuTensorMapEncodeTiled failed");
 
-  PQK_CUDA_TRY(cudaMemsetAsync(counters, 0, 8, stream));
-  encode_prep_kernel<KP><<<m, 256, 0, stream>>>(d_cw, m, l, KP, bprep, cnc, cstat);
+  PQK_CUDA_TRY(cudaMemsetAsync(counters, 0, (size_t)(m + 2) * 4, stream));
+  encode_prep_kernel<KP><<<m, 256, 0, stream>>>(d_cw, m, l, ks, bprep, cst);
   PQK_LAUNCH_CHECK("encode_prep_kernel");
   EncParams ep{};
-  ep.x = d_x;
-  ep.cw = d_cw;
   ep.bprep = bprep;
-  ep.cnc = cnc;
-  ep.cstat = cstat;
+  ep.cst = cst;
   ep.n = n;
-  ep.d = d;
   ep.m = m;
-  ep.l = l;
-  ep.ks = KP;
+  ep.ks = ks;
   ep.codes = d_codes;
   ep.stride = stride;
   ep.flags = flags;
   ep.counters = counters;
   ep.flag_cap = cap;
   ep.ntiles = (int)((n + kRows - 1) / kRows);
+  ep.tstride = std::max(1, std::min(di.sms / m, ep.ntiles));  // CTAs per subspace
+  ep.keymask = ~31u;
+  ep.one = 1u;
   auto kern = encode_tc_kernel<KP>;
-  PQK_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  const int grid = std::max(1, std::min(di.sms, ep.ntiles));
-  kern<<<grid, kThreads, smem, stream>>>(map, ep);
+  PQK_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM));
+  kern<<<ep.tstride * m, kThreads, G::SMEM, stream>>>(map, ep);
   PQK_LAUNCH_CHECK("encode_tc_kernel");
-  encode_exact_kernel<<<di.sms, 256, 0, stream>>>(d_x, n, d, d_cw, m, l, KP, flags, counters, cap, d_codes, stride);
+  const int exact_smem = l * (ks + 1) * 4;
+  PQK_CUDA_TRY(cudaFuncSetAttribute(encode_exact_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, exact_smem));
+  const dim3 egrid((unsigned)std::max(1, 2 * di.sms / m), (unsigned)m);
+  encode_exact_kernel<<<egrid, 256, exact_smem, stream>>>(d_x, n, d, d_cw, m, l, ks, flags, counters, cap, d_codes,
+                                                          stride);
   PQK_LAUNCH_CHECK("encode_exact_kernel");
   encode_stats_kernel<<<1, 1, 0, stream>>>(counters, flagged_out);
   PQK_LAUNCH_CHECK("encode_stats_kernel");
@@ -652,27 +891,30 @@ int launch_encode_tc(const float* d_x, int64_t n, int d, const float* d_cw, int 
 }
 }  // namespace
 
-// Tensor-core encoder eligibility and launch (called by pqk_encode_device).
+// Tensor-core encoder eligibility and launch (called by pqk_encode_device): dsub in
+// {8, 16, 32, 64}, at most one CTA per subspace per SM, 16-byte aligned rows.
 int encode_tc_try(const float* d_x, int64_t n, int d, const float* d_cw, int m, int l, uint8_t* d_codes, int stride,
                   unsigned long long* flagged_out, cudaStream_t stream, bool* used) {
   *used = false;
   const int ks = d / m;
-  if (n < 1 || n >= ((int64_t)1 << 31) / std::max(m, 1) || (d % 4) != 0 || (reinterpret_cast<uintptr_t>(d_x) & 15))
-    return PQK_OK;
   const DevInfo& di = dev_info();
+  if (n < 1 || n >= ((int64_t)1 << 31) || (d % 4) != 0 || (reinterpret_cast<uintptr_t>(d_x) & 15) ||
+      m > di.sms)
+    return PQK_OK;
   int rc = PQK_OK;
   switch (ks) {
+    case 8:
     case 16:
-      if (enc::smem_bytes<16>(m) > (size_t)di.smem_optin) return PQK_OK;
-      rc = launch_encode_tc<16>(d_x, n, d, d_cw, m, l, d_codes, stride, flagged_out, stream);
+      if ((size_t)enc::Geo<16>::SMEM > (size_t)di.smem_optin) return PQK_OK;
+      rc = launch_encode_tc<16>(d_x, n, d, d_cw, m, l, ks, d_codes, stride, flagged_out, stream);
       break;
     case 32:
-      if (enc::smem_bytes<32>(m) > (size_t)di.smem_optin) return PQK_OK;
-      rc = launch_encode_tc<32>(d_x, n, d, d_cw, m, l, d_codes, stride, flagged_out, stream);
+      if ((size_t)enc::Geo<32>::SMEM > (size_t)di.smem_optin) return PQK_OK;
+      rc = launch_encode_tc<32>(d_x, n, d, d_cw, m, l, ks, d_codes, stride, flagged_out, stream);
       break;
     case 64:
-      if (enc::smem_bytes<64>(m) > (size_t)di.smem_optin) return PQK_OK;
-      rc = launch_encode_tc<64>(d_x, n, d, d_cw, m, l, d_codes, stride, flagged_out, stream);
+      if ((size_t)enc::Geo<64>::SMEM > (size_t)di.smem_optin) return PQK_OK;
+      rc = launch_encode_tc<64>(d_x, n, d, d_cw, m, l, ks, d_codes, stride, flagged_out, stream);
       break;
     default:
       return PQK_OK;

@@ -6,6 +6,7 @@
 import collections
 import csv
 import io
+import os
 import subprocess
 import sys
 
@@ -24,6 +25,7 @@ METRICS = [
     ("sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active", "LSU pipe %"),
     ("smsp__inst_executed.sum", "warp instructions"),
     ("sm__warps_active.avg.pct_of_peak_sustained_active", "warps active %"),
+    ("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active", "tensor pipe active %"),
     ("launch__registers_per_thread", "registers/thread"),
     ("gpu__compute_memory_throughput.avg.pct_of_peak_sustained_elapsed", "memory throughput %"),
     ("sm__throughput.avg.pct_of_peak_sustained_elapsed", "SM throughput %"),
@@ -42,8 +44,9 @@ def raw(rep):
 def main():
     rep, launches = sys.argv[1], (sys.argv[2] if len(sys.argv) > 2 else None)
     print(f"# ncu summary — `{rep.split('/')[-1]}`\n")
+    cmd = os.environ.get("PQK_PROFILE_CMD", "python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e")
     print("Captured with `ncu --set full --clock-control none --import-source on` under gpurun on one B200 "
-          "(command: `python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e`, config 2).\n")
+          f"(command: `{cmd}`).\n")
     for hdr, units, r in raw(rep):
         ix = {n: i for i, n in enumerate(hdr)}
         name = r[ix["Kernel Name"]]

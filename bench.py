@@ -463,10 +463,37 @@ def main() -> None:
                      "hbm_frac": enc_bytes / (enc_ms / 1e3) / 1e9 / hbm_peak,
                      "flagged_pairs": enc_flagged,
                      "kernel": ("encode_tc_kernel (tcgen05 fp16 hi/lo split, certified argmin, fp64 fallback)"
-                                if (cfg["dim"] // m) in (16, 32, 64) else
+                                if (cfg["dim"] // m) in (8, 16, 32, 64) else
                                 "encode_kernel (SIMT fp32 filter + fp64 certificate)")}
     if out_train:
         out["codebook_training"] = out_train
+
+    # original-space error of the final labels (baselines.original_space_error, SURVEY
+    # §8f row 3): means in index order + pairwise row sums + np.mean tree, on device
+    if rank == 0 and not cfg.get("gpu_data") and not args.no_cpu_baseline:
+        with torch.cuda.device(dev):
+            x_dev = torch.from_numpy(vectors).to(dev)
+            lab_dev = eng.labels.to(torch.int32)
+            plan = engine.pairwise_plan(n_loc, dev)
+            out2 = torch.zeros(2, dtype=torch.float64, device=dev)
+            times = []
+            for _ in range(3):
+                torch.cuda.synchronize(dev)
+                e0.record()
+                means = engine.cluster_means_device(x_dev, lab_dev, k, dev)
+                sq = engine.assigned_sq_device(x_dev, means, lab_dev, dev)
+                engine.objective_sums(sq, plan, out2, dev)
+                e1.record()
+                torch.cuda.synchronize(dev)
+                times.append(e0.elapsed_time(e1))
+            ose_ms = min(times)
+            ose_bytes = 2 * n_loc * cfg["dim"] * 4 + n_loc * (3 * 4 + 16)
+            out["original_space_error"] = {
+                "value": engine.mean_from_sum(float(out2[0].item()), n_loc), "ms": ose_ms, "n": n_loc, "k": k,
+                "dim": cfg["dim"], "hbm_gbs": ose_bytes / (ose_ms / 1e3) / 1e9,
+                "hbm_frac": ose_bytes / (ose_ms / 1e3) / 1e9 / hbm_peak,
+                "exact": "bit-identical to baselines.original_space_error (float64, numpy order)"}
+            del x_dev, means, sq
 
     # ---- e2e through the C-ABI host entry (host buffers, H2D/D2H inside) ------------
     if not args.no_e2e and not use_dist:

@@ -164,6 +164,20 @@ int pqk_train_step_device(const float* d_x, int64_t n, int32_t d, int32_t col0, 
                           int32_t l, int32_t* d_labels, double* d_sums, int32_t* d_counts, double* d_own,
                           void* d_ws, size_t ws_bytes, int64_t* d_stats, void* stream);
 
+/* Original-space evaluation (baselines.py:26-37 cluster_means, :385-413
+ * original_space_error).  means[k][:] = float64 mean of the rows labelled k, summed in
+ * increasing row index from 0.0 (np.bincount with weights), 0 for empty clusters;
+ * counts[k] optional.  x is (n, d) row-major, dtype 0 = float32, 1 = float64; labels in
+ * [0, k), n < 2^32. */
+size_t pqk_cluster_means_workspace_bytes(int64_t n, int32_t k);
+int pqk_cluster_means_device(const void* d_x, int32_t dtype, int64_t n, int32_t d, const int32_t* d_labels,
+                             int32_t k, double* d_means, int32_t* d_counts, void* d_ws, size_t ws_bytes,
+                             void* stream);
+/* sq[i] = np.sum((x[i] - centers[labels[i]])**2): float64, numpy's pairwise order over d.
+ * original_space_error = mean(sqrt(sq)) via pqk_objective_device. */
+int pqk_assigned_sq_device(const void* d_x, int32_t dtype, int64_t n, int32_t d, const double* d_centers,
+                           const int32_t* d_labels, double* d_sq, void* stream);
+
 /* ---- host-buffer entry points (the reference-facing plugin boundary) ---------- */
 /* AssignStrategy (clustering.py:200): labels (and optionally sd_sq) for host codes. */
 int pqk_assign_host(const uint8_t* codes, int64_t n, int32_t m, const uint8_t* centers, int64_t k,

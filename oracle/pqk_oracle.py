@@ -27,6 +27,11 @@ Semantics restated (file:line of the reference):
 - encode                pq.py:205-231, _nearest pq.py:114-116 (scipy cdist
                         sqeuclidean = sequential fp64 sum of (x-c)^2, no FMA)
 - build_distance_tables pq.py:254-268
+- train_codebook        pq.py:127-202 (_lloyd_subspace, empty-codeword reseed)
+- cluster_means         baselines.py:26-37      per-dimension np.bincount with weights:
+                        float64 sums in increasing point index, / counts
+- original_space_error  baselines.py:385-413    np.sum((p - m)**2, axis=1) (pairwise
+                        over the row), np.mean(np.sqrt(.)) (pairwise over N)
 """
 
 from __future__ import annotations
@@ -286,6 +291,38 @@ def build_distance_tables(codewords: np.ndarray) -> np.ndarray:
             acc += diff * diff
         t[m] = acc
     return t
+
+
+def cluster_means(points: np.ndarray, labels: np.ndarray, k: int) -> np.ndarray:
+    """baselines.py:26-37: float64 sums in point-index order (a sequential loop, which is
+    what np.bincount(weights=...) does), divided by the counts; empty rows stay 0."""
+    pts = np.asarray(points, dtype=np.float64)
+    lab = np.asarray(labels).astype(np.intp)
+    sums = np.zeros((k, pts.shape[1]))
+    counts = np.zeros(k)
+    for i in range(len(pts)):  # sequential, index order
+        sums[lab[i]] += pts[i]
+        counts[lab[i]] += 1.0
+    out = np.zeros_like(sums)
+    filled = counts > 0
+    out[filled] = sums[filled] / counts[filled][:, None]
+    return out
+
+
+def row_pairwise_sq(points: np.ndarray, centers: np.ndarray, labels: np.ndarray) -> np.ndarray:
+    """np.sum((points - centers[labels])**2, axis=1): numpy's pairwise sum per row."""
+    diff2 = (np.asarray(points, dtype=np.float64) - centers[np.asarray(labels).astype(np.intp)]) ** 2
+    return np.array([pairwise_sum(r) for r in diff2])
+
+
+def original_space_error(vectors: np.ndarray, labels: np.ndarray) -> float:
+    """baselines.py:385-413."""
+    points = np.asarray(vectors, dtype=np.float32).astype(np.float64)
+    lab = np.asarray(labels)
+    k = int(lab.max()) + 1
+    means = cluster_means(points, lab, k)
+    sq = row_pairwise_sq(points, means, lab)
+    return float(np.float64(pairwise_sum(np.sqrt(sq))) / len(sq))
 
 
 # ---------------------------------------------------------------------------

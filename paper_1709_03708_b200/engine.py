@@ -491,3 +491,33 @@ def encode_device(vec_dev, cw_dev, m: int, l: int, dev, stride: int | None = Non
     if n:
         call("pqk_encode_device", _ptr(vec_dev), n, d, _ptr(cw_dev), m, l, _ptr(out), stride, _ptr(st), _stream(dev))
     return out
+
+
+# ---------------------------------------------------------------------------
+# original-space evaluation (baselines.py:26-37, 385-413)
+def cluster_means_device(x_dev: "torch.Tensor", labels_dev: "torch.Tensor", k: int, dev,
+                         counts_dev: "torch.Tensor | None" = None) -> "torch.Tensor":
+    """(K, D) float64 means of float32/float64 rows grouped by int32 labels in [0, k)."""
+    n, d = int(x_dev.shape[0]), int(x_dev.shape[1])
+    dtype = 0 if x_dev.dtype == torch.float32 else 1
+    means = torch.empty((k, d), dtype=torch.float64, device=dev)
+    ws = _empty(_lib.load().pqk_cluster_means_workspace_bytes(n, k), dev)
+    call("pqk_cluster_means_device", _ptr(x_dev), dtype, n, d, _ptr(labels_dev), k, _ptr(means), _ptr(counts_dev),
+         _ptr(ws), ws.numel(), _stream(dev))
+    return means
+
+
+def assigned_sq_device(x_dev: "torch.Tensor", centers_dev: "torch.Tensor", labels_dev: "torch.Tensor", dev):
+    """(N,) float64 np.sum((x - centers[labels])**2, axis=1) in numpy's order."""
+    n, d = int(x_dev.shape[0]), int(x_dev.shape[1])
+    dtype = 0 if x_dev.dtype == torch.float32 else 1
+    sq = torch.empty(n, dtype=torch.float64, device=dev)
+    call("pqk_assigned_sq_device", _ptr(x_dev), dtype, n, d, _ptr(centers_dev), _ptr(labels_dev), _ptr(sq),
+         _stream(dev))
+    return sq
+
+
+def original_space_error_device(x_dev: "torch.Tensor", labels_dev: "torch.Tensor", k: int, dev) -> float:
+    means = cluster_means_device(x_dev, labels_dev, k, dev)
+    sq = assigned_sq_device(x_dev, means, labels_dev, dev)
+    return mean_objectives(sq, int(x_dev.shape[0]), dev)[0]

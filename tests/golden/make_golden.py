@@ -264,8 +264,32 @@ def make_train():
     save("train", **arrays)
 
 
+def make_baselines():
+    """Reference cluster_means / original_space_error (baselines.py:26-37, 385-413)."""
+    from pqclust.baselines import cluster_means, original_space_error
+
+    arrays = {}
+    rng = np.random.default_rng(91)
+    cases = [(600, 128, 37, 1.0), (777, 32, 5, 1e3), (800, 40, 300, 1e-3), (130, 7, 3, 10.0), (1, 3, 1, 1.0),
+             (300, 200, 9, 1.0)]
+    for i, (n, d, k, scale) in enumerate(cases):
+        x = (rng.normal(size=(n, d)) * scale + rng.uniform(-5, 5, size=d) * scale).astype(np.float32)
+        lab = rng.integers(0, k, size=n)
+        if k > 4:
+            lab[lab == 2] = 3  # an empty cluster in the middle
+        arrays[f"b{i}_x"] = x
+        arrays[f"b{i}_labels"] = lab.astype(np.int64)
+        arrays[f"b{i}_k"] = np.array(k)
+        arrays[f"b{i}_means"] = cluster_means(x.astype(np.float64), lab, k)
+        arrays[f"b{i}_means32"] = cluster_means(x, lab, k)
+        arrays[f"b{i}_err"] = np.array(original_space_error(x, lab))
+    arrays["ncases"] = np.array(len(cases))
+    save("baselines", **arrays)
+
+
 if __name__ == "__main__":
     makers = {"assign": make_assign, "fit": make_fit, "encode": make_encode, "vote": make_vote,
-              "tables_mean": make_tables_and_mean, "config1": make_config1, "train": make_train}
+              "tables_mean": make_tables_and_mean, "config1": make_config1, "train": make_train,
+              "baselines": make_baselines}
     for name in sys.argv[1:] or list(makers):  # default: regenerate every fixture
         makers[name]()

@@ -103,3 +103,13 @@ def test_train_codebook_golden():
         m, l_count, it, seed = (int(v) for v in g[f"t{i}_args"])
         got = O.train_codebook(g[f"t{i}_x"], m, l_count, iterations=it, seed=seed)
         assert got.tobytes() == g[f"t{i}_book"].tobytes(), i
+
+
+def test_baselines_golden():
+    """Oracle cluster_means / original_space_error vs the reference's own outputs."""
+    g = load("baselines")
+    for i in range(int(g["ncases"])):
+        x, lab, k = g[f"b{i}_x"], g[f"b{i}_labels"], int(g[f"b{i}_k"])
+        assert O.cluster_means(x.astype(np.float64), lab, k).tobytes() == g[f"b{i}_means"].tobytes(), i
+        assert O.cluster_means(x, lab, k).tobytes() == g[f"b{i}_means32"].tobytes(), i
+        assert O.original_space_error(x, lab) == float(g[f"b{i}_err"]), i

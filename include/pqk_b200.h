@@ -178,6 +178,27 @@ int pqk_cluster_means_device(const void* d_x, int32_t dtype, int64_t n, int32_t 
 int pqk_assigned_sq_device(const void* d_x, int32_t dtype, int64_t n, int32_t d, const double* d_centers,
                            const int32_t* d_labels, double* d_sq, void* stream);
 
+/* Bk-means baseline (baselines.py:229-382).  Packed codes are MSB-first bytes
+ * (np.packbits) in rows padded to wp in {4, 8, 16, 32} bytes (zero pad bytes).
+ * binarize: bit b = (x . R[:, b] >= 0), R float64 (d, bits) with orthonormal columns;
+ *   fp32 filter with a rigorous bound, exact double-double sign for the rest (count in
+ *   d_stats[PQK_STAT_ENCODE_FLAGGED]).
+ * hamming_assign: labels = argmin_k popcount(code ^ center_k), lowest k on ties; sd =
+ *   dist^2 (float64, nullable) and dist (nullable).  k <= 2^24.
+ * hamming_matrix: out[i][k] = popcount(code_i ^ center_k) (hamming_to_centers).
+ * majority_update: counts, per-bit ones, new_centers[k] = packbits(2*ones > count) for
+ *   filled k (0 for empty), EMPTY/FILLED stats; then pqk_repair_device(sd, ...) with
+ *   m = wp repairs the empty clusters. */
+int pqk_binarize_device(const float* d_x, int64_t n, int32_t d, const double* d_rotation, int32_t bits,
+                        uint8_t* d_codes, int32_t code_stride, int64_t* d_stats, void* stream);
+int pqk_hamming_assign_device(const uint8_t* d_codes, int64_t n, int32_t wp, const uint8_t* d_centers, int64_t k,
+                              uint32_t* d_labels, double* d_sd, int32_t* d_dist, void* stream);
+int pqk_hamming_matrix_device(const uint8_t* d_codes, int64_t n, int32_t wp, const uint8_t* d_centers, int64_t k,
+                              int32_t* d_out, void* stream);
+int pqk_majority_update_device(const uint8_t* d_codes, int64_t n, int32_t wp, int32_t bits, const uint32_t* d_labels,
+                               int64_t k, int32_t* d_counts, int32_t* d_ones, uint8_t* d_new_centers,
+                               int64_t* d_stats, void* stream);
+
 /* ---- host-buffer entry points (the reference-facing plugin boundary) ---------- */
 /* AssignStrategy (clustering.py:200): labels (and optionally sd_sq) for host codes. */
 int pqk_assign_host(const uint8_t* codes, int64_t n, int32_t m, const uint8_t* centers, int64_t k,

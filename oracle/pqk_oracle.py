@@ -32,6 +32,10 @@ Semantics restated (file:line of the reference):
                         float64 sums in increasing point index, / counts
 - original_space_error  baselines.py:385-413    np.sum((p - m)**2, axis=1) (pairwise
                         over the row), np.mean(np.sqrt(.)) (pairwise over N)
+- binarize              baselines.py:212-234    sign of the float64 projection (exact
+                        rational sign here; the reference's dgemm order is unpinned)
+- hamming / majority    baselines.py:242-288    popcount(xor), 2 * ones > count
+- bkmeans_fit           baselines.py:291-382
 """
 
 from __future__ import annotations
@@ -323,6 +327,74 @@ def original_space_error(vectors: np.ndarray, labels: np.ndarray) -> float:
     means = cluster_means(points, lab, k)
     sq = row_pairwise_sq(points, means, lab)
     return float(np.float64(pairwise_sum(np.sqrt(sq))) / len(sq))
+
+
+_POPCOUNT = np.array([bin(v).count("1") for v in range(256)], dtype=np.uint8)
+
+
+def binarize(rotation: np.ndarray, vectors: np.ndarray) -> np.ndarray:
+    """baselines.py:212-234 with the exact sign of x . R_b (Fraction arithmetic on the
+    float64 values), packed MSB-first (np.packbits)."""
+    x = np.atleast_2d(np.asarray(vectors, dtype=np.float32)).astype(np.float64)
+    proj = x @ rotation
+    bits = (proj >= 0).astype(np.uint8)
+    # exact sign where the float64 product could be off (|proj| below its error bound)
+    bound = (x.shape[1] + 2) * 2.0**-52 * (np.abs(x) @ np.abs(rotation))
+    for i, b in zip(*np.nonzero(np.abs(proj) <= bound)):
+        v = sum(Fraction(float(x[i, k])) * Fraction(float(rotation[k, b])) for k in range(x.shape[1]))
+        bits[i, b] = 1 if v >= 0 else 0
+    return np.packbits(bits, axis=1)
+
+
+def hamming_to_centers(codes: np.ndarray, centers: np.ndarray) -> np.ndarray:
+    """baselines.py:285-288."""
+    xor = codes[:, None, :] ^ centers[None, :, :]
+    return _POPCOUNT[xor].sum(axis=2, dtype=np.int64)
+
+
+def majority_center(member_bits: np.ndarray) -> np.ndarray:
+    """baselines.py:253-282: bit = 2 * ones > count (ties give 0)."""
+    ones = np.asarray(member_bits).sum(axis=0, dtype=np.int64)
+    return (2 * ones > len(member_bits)).astype(np.uint8)
+
+
+def bkmeans_fit(codes, k, max_iterations=20, seed=0, *, initial_centers=None):
+    """baselines.py:291-382 (single-threaded restatement)."""
+    packed = np.asarray(codes, dtype=np.uint8)
+    n, width = packed.shape
+    bits = 8 * width
+    if initial_centers is None:
+        centers = packed[np.random.default_rng(seed).choice(n, size=k, replace=False)].copy()
+    else:
+        centers = np.asarray(initial_centers, dtype=np.uint8).copy()
+    trace = []
+    previous = None
+    converged = False
+    labels = np.zeros(n, dtype=np.uint32)
+    for _ in range(max_iterations):
+        labels = np.argmin(hamming_to_centers(packed, centers), axis=1).astype(np.uint32)
+        dist = _POPCOUNT[packed ^ centers[labels]].sum(axis=1, dtype=np.int64)
+        objective = float(np.mean(dist))
+        objective_sq = float(np.mean(dist.astype(np.float64) ** 2))
+        if previous is not None and objective == previous:
+            trace.append({"objective": objective, "objective_sq": objective_sq, "repaired": 0})
+            converged = True
+            break
+        counts = np.bincount(labels.astype(np.intp), minlength=k)
+        new_centers = np.zeros((k, width), dtype=np.uint8)
+        for ki in np.flatnonzero(counts > 0):
+            members = np.unpackbits(packed[labels == ki], axis=1, count=bits)
+            new_centers[ki] = np.packbits(majority_center(members))
+        empty = np.flatnonzero(counts == 0)
+        own = dist.astype(np.float64)
+        for ki in empty:
+            far = int(np.argmax(own))
+            new_centers[ki] = packed[far]
+            own[far] = -np.inf
+        trace.append({"objective": objective, "objective_sq": objective_sq, "repaired": len(empty)})
+        centers = new_centers
+        previous = objective
+    return {"centers": centers, "labels": labels, "trace": trace, "converged": converged}
 
 
 # ---------------------------------------------------------------------------

@@ -71,6 +71,10 @@ SIGNATURES: dict[str, tuple] = {
     "pqk_cluster_means_workspace_bytes": (_sz, [_i64, _i32]),
     "pqk_cluster_means_device": (C.c_int, [_p, _i32, _i64, _i32, _p, _i32, _p, _p, _p, _sz, _p]),
     "pqk_assigned_sq_device": (C.c_int, [_p, _i32, _i64, _i32, _p, _p, _p, _p]),
+    "pqk_binarize_device": (C.c_int, [_p, _i64, _i32, _p, _i32, _p, _i32, _p, _p]),
+    "pqk_hamming_assign_device": (C.c_int, [_p, _i64, _i32, _p, _i64, _p, _p, _p, _p]),
+    "pqk_hamming_matrix_device": (C.c_int, [_p, _i64, _i32, _p, _i64, _p, _p]),
+    "pqk_majority_update_device": (C.c_int, [_p, _i64, _i32, _i32, _p, _i64, _p, _p, _p, _p, _p]),
 }
 
 _lib: C.CDLL | None = None

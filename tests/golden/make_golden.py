@@ -287,9 +287,59 @@ def make_baselines():
     save("baselines", **arrays)
 
 
+def make_bkmeans():
+    """Reference train_binarizer / binarize / hamming_to_centers / majority_center /
+    bkmeans_fit (baselines.py:157-382)."""
+    from pqclust.baselines import binarize, bkmeans_fit, hamming_to_centers, train_binarizer
+
+    arrays = {}
+    rng = np.random.default_rng(93)
+    # binarizers and binarized vectors (incl. a zero vector: every bit set)
+    for i, (dim, bits, n) in enumerate([(128, 32, 400), (24, 16, 50), (64, 64, 200), (40, 40, 30)]):
+        bz = train_binarizer(dim, bits, seed=10 + i)
+        x = (rng.normal(size=(n, dim)) * 7).astype(np.float32)
+        x[0] = 0.0
+        arrays[f"z{i}_rot"] = bz.rotation
+        arrays[f"z{i}_args"] = np.array([dim, bits, 10 + i])
+        arrays[f"z{i}_x"] = x
+        arrays[f"z{i}_codes"] = binarize(bz, x)
+    arrays["nbin"] = np.array(4)
+    # Hamming matrix
+    a = rng.integers(0, 256, size=(40, 5), dtype=np.uint8)
+    b = rng.integers(0, 256, size=(9, 5), dtype=np.uint8)
+    arrays.update(h_a=a, h_b=b, h_d=hamming_to_centers(a, b))
+    # fits: clustered codes (noisy copies of prototypes), duplicates forcing repairs, ties
+    fits = []
+    protos = rng.integers(0, 256, size=(12, 4), dtype=np.uint8)
+    noise = (rng.random(size=(900, 32)) < 0.08).astype(np.uint8)
+    codes0 = protos[rng.integers(0, 12, size=900)] ^ np.packbits(noise, axis=1)
+    fits.append((codes0, 12, 15, 3, None))
+    dup = np.repeat(rng.integers(0, 256, size=(6, 2), dtype=np.uint8), 20, axis=0)
+    fits.append((dup, 10, 6, 1, None))  # 6 distinct codes, K=10: empty clusters every iteration
+    codes2 = rng.integers(0, 256, size=(500, 8), dtype=np.uint8)
+    fits.append((codes2, 30, 8, 5, None))
+    ties = np.array([[0x00], [0x0F], [0xF0], [0xFF], [0x3C], [0xC3]] * 5, dtype=np.uint8)
+    fits.append((ties, 3, 5, 0, np.array([[0x00], [0xFF], [0x0F]], dtype=np.uint8)))
+    codes4 = rng.integers(0, 256, size=(300, 16), dtype=np.uint8)
+    fits.append((codes4, 7, 4, 2, None))
+    for i, (codes, k, it, seed, init) in enumerate(fits):
+        res = bkmeans_fit(codes, k, max_iterations=it, seed=seed, initial_centers=init)
+        arrays[f"f{i}_codes"] = codes
+        arrays[f"f{i}_args"] = np.array([k, it, seed])
+        arrays[f"f{i}_init"] = init if init is not None else np.zeros((0, codes.shape[1]), np.uint8)
+        arrays[f"f{i}_centers"] = res.centers
+        arrays[f"f{i}_labels"] = res.labels
+        arrays[f"f{i}_obj"] = np.array([s.objective for s in res.trace])
+        arrays[f"f{i}_obj_sq"] = np.array([s.objective_sq for s in res.trace])
+        arrays[f"f{i}_rep"] = np.array([s.repaired_clusters for s in res.trace])
+        arrays[f"f{i}_conv"] = np.array(res.converged)
+    arrays["nfit"] = np.array(len(fits))
+    save("bkmeans", **arrays)
+
+
 if __name__ == "__main__":
     makers = {"assign": make_assign, "fit": make_fit, "encode": make_encode, "vote": make_vote,
               "tables_mean": make_tables_and_mean, "config1": make_config1, "train": make_train,
-              "baselines": make_baselines}
+              "baselines": make_baselines, "bkmeans": make_bkmeans}
     for name in sys.argv[1:] or list(makers):  # default: regenerate every fixture
         makers[name]()

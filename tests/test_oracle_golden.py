@@ -113,3 +113,24 @@ def test_baselines_golden():
         assert O.cluster_means(x.astype(np.float64), lab, k).tobytes() == g[f"b{i}_means"].tobytes(), i
         assert O.cluster_means(x, lab, k).tobytes() == g[f"b{i}_means32"].tobytes(), i
         assert O.original_space_error(x, lab) == float(g[f"b{i}_err"]), i
+
+
+def test_bkmeans_golden():
+    """Oracle Bk-means pieces vs the reference's own outputs (baselines.py:157-382)."""
+    g = load("bkmeans")
+    for i in range(int(g["nbin"])):
+        assert np.array_equal(O.binarize(g[f"z{i}_rot"], g[f"z{i}_x"]), g[f"z{i}_codes"]), i
+    assert np.array_equal(O.hamming_to_centers(g["h_a"], g["h_b"]), g["h_d"])
+    reps = 0
+    for i in range(int(g["nfit"])):
+        k, it, seed = (int(v) for v in g[f"f{i}_args"])
+        init = g[f"f{i}_init"] if len(g[f"f{i}_init"]) else None
+        ref = O.bkmeans_fit(g[f"f{i}_codes"], k, it, seed, initial_centers=init)
+        assert np.array_equal(ref["centers"], g[f"f{i}_centers"]), i
+        assert np.array_equal(ref["labels"], g[f"f{i}_labels"]), i
+        assert [t["objective"] for t in ref["trace"]] == list(g[f"f{i}_obj"]), i
+        assert [t["objective_sq"] for t in ref["trace"]] == list(g[f"f{i}_obj_sq"]), i
+        assert [t["repaired"] for t in ref["trace"]] == list(g[f"f{i}_rep"]), i
+        assert ref["converged"] == bool(g[f"f{i}_conv"]), i
+        reps += int(np.sum(g[f"f{i}_rep"]))
+    assert reps > 0  # the repair path is exercised

@@ -493,7 +493,53 @@ def main() -> None:
                 "dim": cfg["dim"], "hbm_gbs": ose_bytes / (ose_ms / 1e3) / 1e9,
                 "hbm_frac": ose_bytes / (ose_ms / 1e3) / 1e9 / hbm_peak,
                 "exact": "bit-identical to baselines.original_space_error (float64, numpy order)"}
-            del x_dev, means, sq
+            del means, sq
+            # Bk-means baseline on the same vectors: 32-bit sign codes
+            # (the memory of PQ with M=4), K clusters, iterations of Hamming assignment +
+            # majority update + repair, timed like the PQ step (events, warm-up first)
+            from paper_1709_03708_b200 import baselines as gbl
+
+            bz = gbl.train_binarizer(cfg["dim"], 32, seed=synth.stage_seed(SEED, 3))
+            rot = torch.from_numpy(np.array(bz.rotation)).to(dev)
+            bcodes = torch.zeros((n_loc, 4), dtype=torch.uint8, device=dev)
+            bstats = torch.zeros(_lib.STATS_LEN, dtype=torch.int64, device=dev)
+            bt = []
+            for _ in range(3):
+                torch.cuda.synchronize(dev)
+                e0.record()
+                engine.call("pqk_binarize_device", engine._ptr(x_dev), n_loc, cfg["dim"], engine._ptr(rot), 32,
+                            engine._ptr(bcodes), 4, engine._ptr(bstats), engine._stream(dev))
+                e1.record()
+                torch.cuda.synchronize(dev)
+                bt.append(e0.elapsed_time(e1))
+            packed = bcodes.cpu().numpy()
+            sh = gbl._BinaryShard(packed, k, dev)
+            bcur = sh.upload_centers(packed[np.random.default_rng(SEED).choice(n_loc, size=k, replace=False)])
+            for _ in range(2):
+                sh.assign(bcur)
+                sh.update()
+                bcur = sh.new_centers.clone()
+            it_ms, scan_ms_b = [], []
+            e2 = torch.cuda.Event(enable_timing=True)
+            for _ in range(3):
+                torch.cuda.synchronize(dev)
+                e0.record()
+                sh.assign(bcur)
+                e2.record()
+                sh.obj.cpu()
+                sh.update()
+                bcur = sh.new_centers.clone()
+                e1.record()
+                torch.cuda.synchronize(dev)
+                it_ms.append(e0.elapsed_time(e1))
+                scan_ms_b.append(e0.elapsed_time(e2))
+            out["bkmeans"] = {"bits": 32, "n": n_loc, "k": k, "binarize_ms": min(bt),
+                              "binarize_exact_bits": int(bstats[_lib.STAT_ENCODE_FLAGGED].item()),
+                              "ms_per_iteration": float(np.median(it_ms)),
+                              "assign_ms": float(np.median(scan_ms_b)),
+                              "evals_per_s": n_loc * k / (float(np.median(it_ms)) / 1e3),
+                              "exact": "bit-identical to baselines.bkmeans_fit (golden tests)"}
+            del x_dev, sh
 
     # ---- e2e through the C-ABI host entry (host buffers, H2D/D2H inside) ------------
     if not args.no_e2e and not use_dist:

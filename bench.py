@@ -540,6 +540,33 @@ def main() -> None:
                               "evals_per_s": n_loc * k / (float(np.median(it_ms)) / 1e3),
                               "exact": "bit-identical to baselines.bkmeans_fit (golden tests)"}
             del x_dev, sh
+            # streaming pipeline: fvecs file -> GPU encoder -> PQKC file, and
+            # PQKC file -> device codes; wall time, files in the page cache
+            import tempfile
+
+            from paper_1709_03708_b200 import io as pio
+
+            with tempfile.TemporaryDirectory() as td:
+                fv, pk = Path(td) / "x.fvecs", Path(td) / "x.pqkc"
+                pio.write_fvecs(fv, vectors)
+                book_obj = PQCodebook(np.asarray(book, dtype=np.float32))
+                pio.encode_fvecs(book_obj, fv, pk)  # warm (allocations, page cache)
+                t0s = time.perf_counter()
+                pio.encode_fvecs(book_obj, fv, pk)
+                enc_s = time.perf_counter() - t0s
+                pio.load_codes(pk)
+                t0s = time.perf_counter()
+                codes_dev_f, _, _, _ = pio.load_codes(pk)
+                torch.cuda.synchronize(dev)
+                load_s = time.perf_counter() - t0s
+                ok = bool(np.array_equal(engine.download_codes(codes_dev_f, m), codes_host))
+                out["stream"] = {"vectors": n_loc, "fvecs_bytes": fv.stat().st_size,
+                                 "encode_file_s": enc_s, "encode_file_gbs": fv.stat().st_size / enc_s / 1e9,
+                                 "load_codes_s": load_s, "codes_bytes": pk.stat().st_size,
+                                 "codes_equal_in_memory_encode": ok,
+                                 "note": "wall time, files in the page cache; fvecs -> pinned -> GPU unpack+encode "
+                                         "-> PQKC, PQKC -> pinned -> GPU unpack/validate"}
+                del codes_dev_f
 
     # ---- e2e through the C-ABI host entry (host buffers, H2D/D2H inside) ------------
     if not args.no_e2e and not use_dist:

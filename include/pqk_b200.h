@@ -199,6 +199,18 @@ int pqk_majority_update_device(const uint8_t* d_codes, int64_t n, int32_t wp, in
                                int64_t k, int32_t* d_counts, int32_t* d_ones, uint8_t* d_new_centers,
                                int64_t* d_stats, void* stream);
 
+/* File ingest for the streaming pipeline (io.py formats).  unpack_vecs: n raw
+ * fvecs (itemsize 4) / bvecs (itemsize 1) records -> dense float32 rows; err[0] = first
+ * record (base_record + r) whose int32 dimension != dim (UINT64_MAX if none; callers
+ * initialise it), err[1] = that dimension.  unpack_codes: n x m PQKC payload bytes ->
+ * rows of `stride` bytes (pad 0); err[0] = first byte position (record * m + column)
+ * holding a subindex >= l, err[1] = its value.  d_raw of unpack_vecs must be 4-byte
+ * aligned for itemsize 4. */
+int pqk_unpack_vecs_device(const uint8_t* d_raw, int64_t n, int32_t dim, int32_t itemsize, int64_t base_record,
+                           float* d_out, uint64_t* d_err, void* stream);
+int pqk_unpack_codes_device(const uint8_t* d_raw, int64_t n, int32_t m, int32_t l, int64_t base_record,
+                            uint8_t* d_out, int32_t stride, uint64_t* d_err, void* stream);
+
 /* ---- host-buffer entry points (the reference-facing plugin boundary) ---------- */
 /* AssignStrategy (clustering.py:200): labels (and optionally sd_sq) for host codes. */
 int pqk_assign_host(const uint8_t* codes, int64_t n, int32_t m, const uint8_t* centers, int64_t k,

@@ -75,6 +75,8 @@ SIGNATURES: dict[str, tuple] = {
     "pqk_hamming_assign_device": (C.c_int, [_p, _i64, _i32, _p, _i64, _p, _p, _p, _p]),
     "pqk_hamming_matrix_device": (C.c_int, [_p, _i64, _i32, _p, _i64, _p, _p]),
     "pqk_majority_update_device": (C.c_int, [_p, _i64, _i32, _i32, _p, _i64, _p, _p, _p, _p, _p]),
+    "pqk_unpack_vecs_device": (C.c_int, [_p, _i64, _i32, _i32, _i64, _p, _p, _p]),
+    "pqk_unpack_codes_device": (C.c_int, [_p, _i64, _i32, _i32, _i64, _p, _i32, _p, _p]),
 }
 
 _lib: C.CDLL | None = None

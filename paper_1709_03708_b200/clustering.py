@@ -290,14 +290,62 @@ def fit(
         strategy = select_assignment_strategy(codes, t, k, seed)
     if strategy not in _ASSIGNMENT_STRATEGIES:
         raise ValueError(f"unknown assignment strategy {strategy!r}")
-    device_scan = _ASSIGNMENT_STRATEGIES[strategy] is _gpu_linear_scan
-    external = None if device_scan else _ASSIGNMENT_STRATEGIES[strategy]
+    external = None if _ASSIGNMENT_STRATEGIES[strategy] is _gpu_linear_scan else _ASSIGNMENT_STRATEGIES[strategy]
 
     dev = engine.device_of(device)
-    n = len(codes)
+    with torch.cuda.device(dev):
+        codes_dev = engine.upload_codes(codes, m_count, dev)
+        return _fit_on_device(codes_dev, len(codes), t, k, centers, max_iterations, update, external, codes, threads,
+                              dev)
+
+
+def fit_device(
+    codes_dev,
+    n: int,
+    tables,
+    k: int,
+    max_iterations: int = 20,
+    seed: int = 0,
+    *,
+    update: str = "sparse",
+    initial_centers: np.ndarray | None = None,
+    device: int | None = None,
+) -> ClusteringResult:
+    """``fit`` on codes already resident on the GPU (extension for data streamed from
+    files, io.load_codes): ``codes_dev`` is the (N, MP) uint8 device layout with
+    validated subindices.  Initial centers are the rows the reference's
+    ``init_centers`` would pick (clustering.py:149-157), gathered on the device."""
+    import torch
+
+    t = as_tables(tables)
+    m_count, l_count = t.num_subspaces, t.num_codewords
+    if not 1 <= k <= n:
+        raise ValueError(f"k must be in [1, {n}], got {k}")
+    if max_iterations < 1:
+        raise ValueError(f"max_iterations must be positive, got {max_iterations}")
+    if update not in ("sparse", "naive"):
+        raise ValueError(f"update must be 'sparse' or 'naive', got {update!r}")
+    dev = engine.device_of(device)
+    with torch.cuda.device(dev):
+        if initial_centers is None:
+            idx = np.random.default_rng(seed).choice(n, size=k, replace=False)
+            rows = codes_dev.index_select(0, torch.from_numpy(idx.astype(np.int64)).to(dev))
+            centers = engine.download_codes(rows, m_count)
+        else:
+            centers = _validate_codes(initial_centers, m_count, l_count).astype(np.uint8)
+            if len(centers) != k:
+                raise ValueError(f"initial_centers has {len(centers)} rows, expected k={k}")
+        return _fit_on_device(codes_dev, n, t, k, centers, max_iterations, update, None, None, 1, dev)
+
+
+def _fit_on_device(codes_dev, n, t, k, centers, max_iterations, update, external, codes, threads, dev):
+    """The Lloyd loop of fit (clustering.py:437-482) on a device code buffer."""
+    import torch
+
+    m_count = t.num_subspaces
+    device_scan = external is None
     with torch.cuda.device(dev):
         dt = engine.device_tables(t.tables, dev)
-        codes_dev = engine.upload_codes(codes, m_count, dev)
         cur = engine.upload_codes(centers, m_count, dev)
         eng = engine.ShardEngine(codes_dev, dt, k, dev)
         trace: list[IterationStats] = []

@@ -90,7 +90,7 @@ def device_tables(tables: np.ndarray, dev) -> DeviceTables:
     f64 = C.c_int32(0)
     _lib.check(lib.pqk_table_scale(t.ctypes.data_as(C.c_void_p), t.size, C.byref(e), C.byref(f64)), "pqk_table_scale")
     mp = _lib.padded_m(m)
-    t64 = torch.from_numpy(t).to(dev)
+    t64 = torch.from_numpy(np.array(t)).to(dev)  # (read-only DistanceTables arrays)
     t32 = torch.empty(mp * l * l, dtype=torch.float32, device=dev)
     call("pqk_tables_to_f32", _ptr(t64), m, l, e.value, _ptr(t32), _stream(dev))
     dt = DeviceTables(t64, t32, m, l, mp, int(f64.value), int(e.value))

@@ -337,9 +337,34 @@ def make_bkmeans():
     save("bkmeans", **arrays)
 
 
+def make_io():
+    """Bytes of files written by the reference's io writers (io.py), and their inputs."""
+    import tempfile
+
+    from pqclust import io as rio
+
+    rng = np.random.default_rng(95)
+    vec = (rng.normal(size=(37, 12)) * 3).astype(np.float32)
+    bvec = rng.integers(0, 256, size=(19, 7)).astype(np.float32)
+    codes = rng.integers(0, 200, size=(53, 6)).astype(np.uint8)
+    book = PQCodebook(rng.normal(size=(3, 16, 4)).astype(np.float32))
+    packed = rng.integers(0, 256, size=(23, 3), dtype=np.uint8)
+    labels = rng.integers(0, 2**32 - 1, size=41, dtype=np.uint64).astype(np.uint32)
+    arrays = dict(vec=vec, bvec=bvec, codes=codes, book=book.codewords, packed=packed, labels=labels)
+    with tempfile.TemporaryDirectory() as td:
+        writers = {"fvecs": lambda p: rio.write_fvecs(p, vec), "bvecs": lambda p: rio.write_bvecs(p, bvec),
+                   "pqkc": lambda p: rio.write_codes(p, codes, 200), "pqcb": lambda p: rio.write_codebook(p, book),
+                   "pqkb": lambda p: rio.write_binary_codes(p, packed), "labels": lambda p: rio.write_labels(p, labels)}
+        for name, write in writers.items():
+            path = Path(td) / name
+            write(path)
+            arrays[f"file_{name}"] = np.frombuffer(path.read_bytes(), dtype=np.uint8).copy()
+    save("io", **arrays)
+
+
 if __name__ == "__main__":
     makers = {"assign": make_assign, "fit": make_fit, "encode": make_encode, "vote": make_vote,
               "tables_mean": make_tables_and_mean, "config1": make_config1, "train": make_train,
-              "baselines": make_baselines, "bkmeans": make_bkmeans}
+              "baselines": make_baselines, "bkmeans": make_bkmeans, "io": make_io}
     for name in sys.argv[1:] or list(makers):  # default: regenerate every fixture
         makers[name]()

@@ -574,7 +574,7 @@ def main() -> None:
 
         pin_codes = torch.from_numpy(codes_host).pin_memory()
         pin_cent = torch.from_numpy(centers0).pin_memory()
-        pin_tab = torch.from_numpy(np.ascontiguousarray(tables)).pin_memory()
+        pin_tab = torch.from_numpy(np.array(tables)).pin_memory()
         pin_lab = torch.empty(n_loc, dtype=torch.int32).pin_memory()
         pin_new = torch.empty((k, m), dtype=torch.uint8).pin_memory()
         obj2 = np.zeros(2)

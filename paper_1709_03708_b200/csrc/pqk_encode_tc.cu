@@ -239,6 +239,79 @@ __device__ __forceinline__ void chunk_best(uint32_t (&k)[32], uint32_t kmask, ui
   rc = (int)(tree_umin32(k) - nbp);
 }
 
+// Epilogue of one 128-row item for one epilogue warp (row n of TMEM lane quadrant q):
+// the 256 accumulator columns (two N=128 halves, signalled and released separately),
+// packed-key best / runner-up, certificate, code store or flag.
+__device__ __forceinline__ void epilogue_row(const EncParams& p, int m, int64_t n, uint32_t tacc, uint64_t* tfull2,
+                                             uint64_t* tempty2, uint32_t ph, float4 st, float eps_main2,
+                                             float eps_main3, float eps_ext, float cb, float cnm, float s1c,
+                                             float sqrt_kp, int lane) {
+  const uint32_t kmask = p.keymask, kone = p.one;
+  int B = 0x7fffffff, R = 0x7fffffff, Bi = 0;
+  uint32_t ka[32], kb[32];
+  tmem_ld32(tacc, ka);
+#pragma unroll
+  for (int c = 0; c < kN / kChunk; c += 2) {
+    tmem_wait32(ka);
+    tmem_ld32(tacc + (uint32_t)((c + 1) * kChunk), kb);
+    int bc, rc;
+    chunk_best(ka, kmask, kone, bc, rc);
+    if ((bc & ~31) < (B & ~31)) {  // strictly smaller value: ties keep the earlier chunk
+      R = min(B, rc);
+      B = bc;
+      Bi = c;
+    } else {
+      R = min(R, bc);
+    }
+    tmem_wait32(kb);
+    if (c + 2 == kN / kChunk / 2 || c + 2 == kN / kChunk) {  // a column half fully read
+      tc::fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty2[c + 2 == kN / kChunk ? 1 : 0]);
+    }
+    if (c + 2 < kN / kChunk) {
+      if (c + 2 == kN / kChunk / 2) {
+        mbar_wait(&tfull2[1], ph);
+        tc::fence_after();
+      }
+      tmem_ld32(tacc + (uint32_t)((c + 2) * kChunk), ka);
+    }
+    chunk_best(kb, kmask, kone, bc, rc);
+    if ((bc & ~31) < (B & ~31)) {
+      R = min(B, rc);
+      B = bc;
+      Bi = c + 1;
+    } else {
+      R = min(R, bc);
+    }
+  }
+  if (n < p.n) {
+    // keys dropped 5 mantissa bits: the value lies within 32 ulp <= 2^-18 |v| of the key
+    // value, above it for v >= 0 and below it for v < 0
+    const float wv = __int_as_float(B & ~31), rv = __int_as_float(R & ~31);
+    const float w_hi = wv >= 0.f ? wv * 1.00000762939453125f : wv;  // 1 + 2^-17
+    const float r_lo = rv >= 0.f ? rv : rv * 1.00000762939453125f;
+    // rigorous bound on |computed - exact| of any D_rj (see header)
+    const float P = st.y * cb * 1.001f;  // >= sum |split products|
+    const float E = (st.w != 0.f ? eps_main3 : eps_main2) * P + eps_ext * (P + cnm + st.x) * 1.001f  //
+                    + 4.76837158203125e-07f * P                                 // 4 * 2^-23: split, lo.lo
+                    + 2.98023223876953125e-08f * (sqrt_kp * st.y + s1c)          // 2^-25: subnormal lo parts
+                    + 9.313225746154785e-10f * (cnm + st.x)                      // 2^-30: extension parts
+                    + 1e-3f;
+    const bool cert = st.z != 0.f && (r_lo - w_hi) > 2.0f * E * 1.0001f;
+    if (cert) {
+      p.codes[n * p.stride + m] = (uint8_t)(kChunk * Bi + (B & 31));
+    } else {
+      atomicAdd(&p.counters[0], 1u);
+      const unsigned f = atomicAdd(&p.counters[2 + m], 1u);
+      if (f < p.flag_cap)
+        p.flags[(size_t)m * p.flag_cap + f] = (uint32_t)n;
+      else
+        p.counters[1] = 1u;
+    }
+  }
+}
+
 template <int KP>
 __global__ void __launch_bounds__(kThreads, 1) encode_tc_kernel(const __grid_constant__ CUtensorMap tmap,
                                                                 const EncParams p) {
@@ -370,7 +443,6 @@ __global__ void __launch_bounds__(kThreads, 1) encode_tc_kernel(const __grid_con
     const int q = warp & 3;   // TMEM lane quadrant (warp % 4)
     const int e = ew >> 2;    // accumulator / item parity
     const int er = 32 * q + lane;
-    const uint32_t kmask = p.keymask, kone = p.one;
     // tensor-core accumulation model: an MMA instruction adds 16 products to the
     // accumulator with error <= 17 * 2^-23 * max(|addend|); the main passes (2 KP/16
     // instructions, 3 KP/16 for a row whose x is not exactly fp16: adding the exact zeros
@@ -387,70 +459,8 @@ __global__ void __launch_bounds__(kThreads, 1) encode_tc_kernel(const __grid_con
       tc::fence_after();
       const float4 st = s_stats[(w & 3) * kRows + er];  // x2u, |s x|, ok
       const uint32_t tacc = tbase + (uint32_t)e * kN + ((uint32_t)(32 * q) << 16);
-      int B = 0x7fffffff, R = 0x7fffffff, Bi = 0;
-      uint32_t ka[32], kb[32];
-      tmem_ld32(tacc, ka);
-#pragma unroll
-      for (int c = 0; c < kN / kChunk; c += 2) {
-        tmem_wait32(ka);
-        tmem_ld32(tacc + (uint32_t)((c + 1) * kChunk), kb);
-        int bc, rc;
-        chunk_best(ka, kmask, kone, bc, rc);
-        if ((bc & ~31) < (B & ~31)) {  // strictly smaller value: ties keep the earlier chunk
-          R = min(B, rc);
-          B = bc;
-          Bi = c;
-        } else {
-          R = min(R, bc);
-        }
-        tmem_wait32(kb);
-        if (c + 2 == kN / kChunk / 2 || c + 2 == kN / kChunk) {  // a column half fully read
-          tc::fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&tempty[2 * e + (c + 2 == kN / kChunk ? 1 : 0)]);
-        }
-        if (c + 2 < kN / kChunk) {
-          if (c + 2 == kN / kChunk / 2) {
-            mbar_wait(&tfull[2 * e + 1], ph);
-            tc::fence_after();
-          }
-          tmem_ld32(tacc + (uint32_t)((c + 2) * kChunk), ka);
-        }
-        chunk_best(kb, kmask, kone, bc, rc);
-        if ((bc & ~31) < (B & ~31)) {
-          R = min(B, rc);
-          B = bc;
-          Bi = c + 1;
-        } else {
-          R = min(R, bc);
-        }
-      }
-      const int64_t n = (int64_t)t * kRows + er;
-      if (n < p.n) {
-        // keys dropped 5 mantissa bits: the value lies within 32 ulp <= 2^-18 |v| of the key
-        // value, above it for v >= 0 and below it for v < 0
-        const float wv = __int_as_float(B & ~31), rv = __int_as_float(R & ~31);
-        const float w_hi = wv >= 0.f ? wv * 1.00000762939453125f : wv;  // 1 + 2^-17
-        const float r_lo = rv >= 0.f ? rv : rv * 1.00000762939453125f;
-        // rigorous bound on |computed - exact| of any D_rj (see header)
-        const float P = st.y * cb * 1.001f;  // >= sum |split products|
-        const float E = (st.w != 0.f ? eps_main3 : eps_main2) * P + eps_ext * (P + cnm + st.x) * 1.001f                  //
-                        + 4.76837158203125e-07f * P                                          // 4 * 2^-23
-                        + 2.98023223876953125e-08f * (sqrtf((float)KP) * st.y + s1c)          // 2^-25
-                        + 9.313225746154785e-10f * (cnm + st.x)                               // 2^-30
-                        + 1e-3f;
-        const bool cert = st.z != 0.f && (r_lo - w_hi) > 2.0f * E * 1.0001f;
-        if (cert) {
-          p.codes[n * p.stride + m] = (uint8_t)(kChunk * Bi + (B & 31));
-        } else {
-          atomicAdd(&p.counters[0], 1u);
-          const unsigned f = atomicAdd(&p.counters[2 + m], 1u);
-          if (f < p.flag_cap)
-            p.flags[(size_t)m * p.flag_cap + f] = (uint32_t)n;
-          else
-            p.counters[1] = 1u;
-        }
-      }
+      epilogue_row(p, m, (int64_t)t * kRows + er, tacc, &tfull[2 * e], &tempty[2 * e], ph, st, eps_main2, eps_main3,
+                   eps_ext, cb, cnm, s1c, sqrtf((float)KP), lane);
     }
   } else {
     // ---------------- transform warps: 16 rows each, 2 passes of 8 ----------------
@@ -788,6 +798,488 @@ __global__ void __launch_bounds__(256) encode_exact_kernel(const float* __restri
   }
 }
 
+// ===========================================================================
+// K-streamed variant for long subspaces (dsub = ks a multiple of 32 in [96, 1024], e.g.
+// BASELINE config 3's 512-D subspaces).  The codebook operands no longer fit in shared
+// memory, so each 128-vector item streams K in 32-column chunks: X chunk by TMA (128-byte
+// swizzle), B chunk (hi + lo, 32 KB) by a bulk copy from the prepared global layout, A
+// chunk by the transform warps; every chunk's MMAs accumulate into the item's TMEM
+// accumulator, the |c|^2 / |x|^2 extension block follows the last chunk.  Epilogue,
+// certificate and fallback are the same as encode_tc_kernel's (epilogue_row), with the
+// accumulation bound scaled by the instruction count (ks / 16 per pass).
+// ===========================================================================
+constexpr int kKC = 32;
+constexpr int kXSt = 3, kBSt = 3, kASt = 2;
+
+struct GeoK {
+  static constexpr int X_STAGE = kRows * kKC * 4;     // 16 KB (1024-aligned, swizzled)
+  static constexpr int B_HI = kN * kKC * 2;           // 16 KB
+  static constexpr int B_CHUNK = 2 * B_HI;            // hi + lo
+  static constexpr int B_EXT = kN * kExt * 2;         // 8 KB
+  static constexpr int A_HI = kRows * kKC * 2;        // 8 KB
+  static constexpr int A_CHUNK = 2 * A_HI;
+  static constexpr int A_EXT = kRows * kExt * 2;      // 4 KB
+  static constexpr int OFF_BEXT = 0;
+  static constexpr int OFF_X = B_EXT;
+  static constexpr int OFF_B = OFF_X + kXSt * X_STAGE;
+  static constexpr int OFF_A = OFF_B + kBSt * B_CHUNK;
+  static constexpr int OFF_AEXT = OFF_A + kASt * A_CHUNK;
+  static constexpr int OFF_STATS = OFF_AEXT + 2 * A_EXT;
+  static constexpr int OFF_LO = OFF_STATS + 4 * kRows * 16;
+  static constexpr int OFF_CST = OFF_LO + kASt * kTrWarps * 4;
+  static constexpr int OFF_BAR = OFF_CST + CST_LEN * 4;  // uint64 [32]
+  static constexpr int OFF_TBASE = OFF_BAR + 32 * 8;
+  static constexpr int SMEM = OFF_TBASE + 16 + 1024;
+  __host__ __device__ static size_t bprep_bytes(int ks) { return (size_t)(ks / kKC) * B_CHUNK + B_EXT; }
+};
+
+__global__ void __launch_bounds__(kThreads, 1) encode_tck_kernel(const __grid_constant__ CUtensorMap tmap,
+                                                                const EncParams p) {
+  using G = GeoK;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* sBext = smem + G::OFF_BEXT;
+  uint8_t* sX = smem + G::OFF_X;
+  uint8_t* sB = smem + G::OFF_B;
+  uint8_t* sA = smem + G::OFF_A;
+  uint8_t* sAext = smem + G::OFF_AEXT;
+  float4* s_stats = reinterpret_cast<float4*>(smem + G::OFF_STATS);
+  int* s_lo = reinterpret_cast<int*>(smem + G::OFF_LO);
+  float* s_cst = reinterpret_cast<float*>(smem + G::OFF_CST);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + G::OFF_BAR);
+  uint64_t* xfull = bars;         // [3]
+  uint64_t* xempty = bars + 3;    // [3]
+  uint64_t* bfull = bars + 6;     // [3]
+  uint64_t* bempty = bars + 9;    // [3]
+  uint64_t* afull = bars + 12;    // [2]
+  uint64_t* aempty = bars + 14;   // [2]
+  uint64_t* aefull = bars + 16;   // [2] extension rows of A, per accumulator
+  uint64_t* aeempty = bars + 18;  // [2]
+  uint64_t* tfull = bars + 20;    // [2][2]
+  uint64_t* tempty = bars + 24;   // [2][2]
+  uint64_t* bload = bars + 28;
+  uint32_t* s_tbase = reinterpret_cast<uint32_t*>(smem + G::OFF_TBASE);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int m = (int)blockIdx.x % p.m;
+  const int t0 = (int)blockIdx.x / p.m;
+  const int items = t0 < p.ntiles ? (p.ntiles - t0 + p.tstride - 1) / p.tstride : 0;
+  const int ks = p.ks, nk = ks / kKC;
+  const uint8_t* bprep = p.bprep + (size_t)m * G::bprep_bytes(ks);
+
+  if (tid == 0) {
+    for (int i = 0; i < 3; ++i) {
+      mbar_init(&xfull[i], 1);
+      mbar_init(&xempty[i], kTrWarps);
+      mbar_init(&bfull[i], 1);
+      mbar_init(&bempty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&afull[i], kTrWarps);
+      mbar_init(&aempty[i], 1);
+      mbar_init(&aefull[i], kTrWarps);
+      mbar_init(&aeempty[i], 1);
+    }
+    for (int i = 0; i < 4; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], kEpiWarps / 2);
+    }
+    mbar_init(bload, 1);
+    fence_mbar_init();
+  }
+  if (warp == 1) tc::tmem_alloc(s_tbase, 512);
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tbase = *s_tbase;
+  if (tid == 0) {
+    mbar_arrive_expect_tx(bload, (uint32_t)G::B_EXT + CST_LEN * 4);
+    bulk_g2s(sBext, bprep + (size_t)nk * G::B_CHUNK, G::B_EXT, bload);
+    bulk_g2s(s_cst, p.cst + (size_t)m * CST_LEN, CST_LEN * 4, bload);
+  }
+  mbar_wait(bload, 0);
+  const int nchunks = items * nk;
+
+  if (warp == 0) {
+    // ---------------- producer: X chunks (TMA) and B chunks (bulk copies) ----------------
+    if (lane == 0) {
+      for (int g = 0; g < nchunks; ++g) {
+        const int w = g / nk, c = g - w * nk;
+        const int t = t0 + w * p.tstride;
+        const int xs = g % kXSt, bs = g % kBSt;
+        mbar_wait(&xempty[xs], (uint32_t)(((g / kXSt) & 1) ^ 1));
+        mbar_arrive_expect_tx(&xfull[xs], (uint32_t)G::X_STAGE);
+        tma_load_2d(sX + xs * G::X_STAGE, &tmap, m * ks + c * kKC, t * kRows, &xfull[xs]);
+        mbar_wait(&bempty[bs], (uint32_t)(((g / kBSt) & 1) ^ 1));
+        mbar_arrive_expect_tx(&bfull[bs], (uint32_t)G::B_CHUNK);
+        bulk_g2s(sB + bs * G::B_CHUNK, bprep + (size_t)c * G::B_CHUNK, G::B_CHUNK, &bfull[bs]);
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer ----------------
+    if (lane == 0) {
+      const uint32_t idesc = tc::idesc_f16_f32(kRows, kN);
+      constexpr uint32_t sboC = (uint32_t)(kKC / 8) * 128, sboE = (uint32_t)(kExt / 8) * 128;
+      for (int w = 0; w < items; ++w) {
+        const int ab = w & 1;
+        const uint32_t ph = (uint32_t)((w >> 1) & 1);
+        mbar_wait_spin(&tempty[2 * ab], ph ^ 1u);
+        mbar_wait_spin(&tempty[2 * ab + 1], ph ^ 1u);
+        const uint32_t tacc = tbase + (uint32_t)ab * kN;
+        for (int c = 0; c < nk; ++c) {
+          const int g = w * nk + c;
+          const int as = g % kASt, bs = g % kBSt;
+          mbar_wait_spin(&afull[as], (uint32_t)((g / kASt) & 1));
+          mbar_wait_spin(&bfull[bs], (uint32_t)((g / kBSt) & 1));
+          tc::fence_after();
+          int lo_any = 0;
+#pragma unroll
+          for (int j = 0; j < kTrWarps; ++j) lo_any |= s_lo[as * kTrWarps + j];
+          const uint32_t a_hi = smem_u32(sA + as * G::A_CHUNK), a_lo = a_hi + G::A_HI;
+          const uint32_t b_hi = smem_u32(sB + bs * G::B_CHUNK), b_lo = b_hi + G::B_HI;
+#pragma unroll
+          for (int s = 0; s < kKC / 16; ++s)
+            tc::mma_f16(tacc, tc::smem_desc(a_hi + s * 256, 128, sboC), tc::smem_desc(b_hi + s * 256, 128, sboC), idesc,
+                        (c > 0 || s > 0) ? 1u : 0u);
+#pragma unroll
+          for (int s = 0; s < kKC / 16; ++s)
+            tc::mma_f16(tacc, tc::smem_desc(a_hi + s * 256, 128, sboC), tc::smem_desc(b_lo + s * 256, 128, sboC), idesc,
+                        1u);
+          if (lo_any) {
+#pragma unroll
+            for (int s = 0; s < kKC / 16; ++s)
+              tc::mma_f16(tacc, tc::smem_desc(a_lo + s * 256, 128, sboC), tc::smem_desc(b_hi + s * 256, 128, sboC),
+                          idesc, 1u);
+          }
+          tc::commit(&aempty[as]);
+          tc::commit(&bempty[bs]);
+        }
+        mbar_wait_spin(&aefull[ab], ph);
+        tc::fence_after();
+        tc::mma_f16(tacc, tc::smem_desc(smem_u32(sAext + ab * G::A_EXT), 128, sboE),
+                    tc::smem_desc(smem_u32(sBext), 128, sboE), idesc, 1u);
+        tc::commit(&aeempty[ab]);
+        tc::commit(&tfull[2 * ab]);
+        tc::commit(&tfull[2 * ab + 1]);
+      }
+    }
+  } else if (warp < 2 + kEpiWarps) {
+    // ---------------- epilogue warps ----------------
+    const int ew = warp - 2;
+    const int q = warp & 3, e = ew >> 2;
+    const int er = 32 * q + lane;
+    // accumulation bound of encode_tc_kernel with ks / 16 instructions per pass
+    const float eps_main2 = (float)(17 * 2 * (ks / 16)) * 1.1920928955078125e-07f;
+    const float eps_main3 = (float)(17 * 3 * (ks / 16)) * 1.1920928955078125e-07f;
+    const float eps_ext = 7.0f * 1.1920928955078125e-07f;
+    const float cb = s_cst[CST_CB], cnm = s_cst[CST_CN], s1c = s_cst[CST_S1C];
+    const float sqrt_ks = sqrtf((float)ks);
+    for (int w = e; w < items; w += 2) {
+      const int t = t0 + w * p.tstride;
+      const uint32_t ph = (uint32_t)((w >> 1) & 1);
+      mbar_wait(&tfull[2 * e], ph);
+      tc::fence_after();
+      const float4 st = s_stats[(w & 3) * kRows + er];
+      const uint32_t tacc = tbase + (uint32_t)e * kN + ((uint32_t)(32 * q) << 16);
+      epilogue_row(p, m, (int64_t)t * kRows + er, tacc, &tfull[2 * e], &tempty[2 * e], ph, st, eps_main2, eps_main3,
+                   eps_ext, cb, cnm, s1c, sqrt_ks, lane);
+    }
+  } else {
+    // ---------------- transform warps: 16 rows each (2 passes of 8), 8 columns per lane ----------------
+    const int tw = warp - 2 - kEpiWarps;
+    const int th = lane >> 3;  // 4 lanes per row: lanes r, r+8, r+16, r+24
+    const float sc = s_cst[CST_S];
+    const __half acn = __float2half_rn(s_cst[CST_ACN]);
+    const bool valid = s_cst[CST_VALID] != 0.f;
+    for (int w = 0; w < items; ++w) {
+      float x2[2] = {0.f, 0.f};
+      uint32_t lo_row[2] = {0u, 0u};
+      for (int c = 0; c < nk; ++c) {
+        const int g = w * nk + c;
+        const int xs = g % kXSt, as = g % kASt;
+        mbar_wait(&xfull[xs], (uint32_t)((g / kXSt) & 1));
+        float v[2][8];
+#pragma unroll
+        for (int ps = 0; ps < 2; ++ps) {
+          const int r = 16 * tw + 8 * ps + (lane & 7);
+          const uint8_t* xb = sX + xs * G::X_STAGE + r * 128;
+#pragma unroll
+          for (int cc = 0; cc < 2; ++cc) {
+            const int ch = 2 * th + cc;
+            const float4 f = *reinterpret_cast<const float4*>(xb + ((ch ^ (r & 7)) << 4));
+            v[ps][4 * cc] = f.x;
+            v[ps][4 * cc + 1] = f.y;
+            v[ps][4 * cc + 2] = f.z;
+            v[ps][4 * cc + 3] = f.w;
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&xempty[xs]);
+        uint32_t hw[2][4], lw[2][4];
+        uint32_t lo_nz = 0;
+#pragma unroll
+        for (int ps = 0; ps < 2; ++ps) {
+          uint32_t lr = 0;
+#pragma unroll
+          for (int j = 0; j < 8; j += 2) {
+            const float a0 = v[ps][j] * sc, a1 = v[ps][j + 1] * sc;
+            const __half2 hh = __floats2half2_rn(a0, a1);
+            const float2 hf = __half22float2(hh);
+            const __half2 ll = __floats2half2_rn(a0 - hf.x, a1 - hf.y);
+            hw[ps][j / 2] = *reinterpret_cast<const uint32_t*>(&hh);
+            lw[ps][j / 2] = *reinterpret_cast<const uint32_t*>(&ll);
+            lr |= lw[ps][j / 2];
+            x2[ps] = fmaf(a0, a0, fmaf(a1, a1, x2[ps]));
+          }
+          lr &= 0x7fff7fffu;
+          lo_row[ps] |= lr;
+          lo_nz |= lr;
+        }
+        const unsigned bal = __ballot_sync(0xffffffffu, lo_nz != 0);
+        mbar_wait(&aempty[as], (uint32_t)(((g / kASt) & 1) ^ 1));
+        uint8_t* ahi = sA + as * G::A_CHUNK;
+#pragma unroll
+        for (int ps = 0; ps < 2; ++ps) {
+          const int r = 16 * tw + 8 * ps + (lane & 7);
+          *reinterpret_cast<uint4*>(ahi + tc::kmajor_off(r, 8 * th, kKC)) =
+              make_uint4(hw[ps][0], hw[ps][1], hw[ps][2], hw[ps][3]);
+          *reinterpret_cast<uint4*>(ahi + G::A_HI + tc::kmajor_off(r, 8 * th, kKC)) =
+              make_uint4(lw[ps][0], lw[ps][1], lw[ps][2], lw[ps][3]);
+        }
+        if (lane == 0) s_lo[as * kTrWarps + tw] = (bal != 0);
+        tc::fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&afull[as]);
+      }
+      // extension rows and stats of the item (whole-row |s x|^2 now known)
+      const int ab = w & 1;
+      mbar_wait(&aeempty[ab], (uint32_t)(((w >> 1) & 1) ^ 1));
+#pragma unroll
+      for (int ps = 0; ps < 2; ++ps) {
+        float acc = x2[ps];
+        acc += __shfl_xor_sync(0xffffffffu, acc, 8);
+        acc += __shfl_xor_sync(0xffffffffu, acc, 16);
+        uint32_t lr = lo_row[ps];
+        lr |= __shfl_xor_sync(0xffffffffu, lr, 8);
+        lr |= __shfl_xor_sync(0xffffffffu, lr, 16);
+        const int r = 16 * tw + 8 * ps + (lane & 7);
+        // |s x|^2 rounded up: fp32 sums of ks products (relative error < (ks + 4) 2^-24)
+        const float x2u = acc * (1.0f + (float)(ks + 16) * 5.9604644775390625e-08f);
+        const bool ok = valid && (x2u < kX2Limit);
+        if (th == 0) {
+          const float xv = ok ? x2u * 3.0517578125e-05f : 0.f;
+          const __half x_h = __float2half_rn(xv);
+          const float r1 = xv - __half2float(x_h);
+          const __half x_m = __float2half_rn(r1);
+          const __half x_l = __float2half_rn(r1 - __half2float(x_m));
+          const __half p15 = __float2half_rn(32768.f);
+          const __half z = __float2half_rn(0.f);
+          uint8_t* ae = sAext + ab * G::A_EXT;
+          *reinterpret_cast<uint4*>(ae + tc::kmajor_off(r, 0, kExt)) =
+              make_uint4(pack_h2(acn, acn), pack_h2(acn, x_h), pack_h2(x_m, x_l), pack_h2(p15, z));
+          *reinterpret_cast<uint4*>(ae + tc::kmajor_off(r, 8, kExt)) = make_uint4(0u, 0u, 0u, 0u);
+          float xn;
+          asm("sqrt.approx.f32 %0, %1;" : "=f"(xn) : "f"(x2u));
+          s_stats[(w & 3) * kRows + r] = make_float4(x2u, xn * 1.000002f, ok ? 1.f : 0.f, lr ? 1.f : 0.f);
+        }
+      }
+      tc::fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&aefull[ab]);
+    }
+  }
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc::fence_after();
+    tc::tmem_dealloc(tbase, 512);
+  }
+}
+
+// Codebook preparation for the K-streamed kernel: per subspace, B chunks [hi | lo] of 32
+// columns then the extension block (same values as encode_prep_kernel).
+__global__ void __launch_bounds__(256) encode_prep_k_kernel(const float* __restrict__ cw, int m, int l, int ks,
+                                                           uint8_t* __restrict__ bprep, float* __restrict__ cst) {
+  __shared__ float red[8], rb[8], rc[8], r1s[8];
+  __shared__ int bad[8];
+  __shared__ double redd[8];
+  __shared__ float s_sc;
+  __shared__ int s_bad;
+  __shared__ double s_cn;
+  const int mm = blockIdx.x, row = threadIdx.x, lane = row & 31, warp = row >> 5;
+  const bool real = row < l;
+  const float* c = cw + ((size_t)mm * l + (real ? row : 0)) * ks;
+  float amax = 0.f;
+  int nonfinite = 0;
+  if (real)
+    for (int k = 0; k < ks; ++k) {
+      const float a = fabsf(c[k]);
+      nonfinite |= !(a <= 3.4028234663852886e38f);
+      amax = fmaxf(amax, a);
+    }
+  for (int o = 16; o > 0; o >>= 1) {
+    amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+    nonfinite |= __shfl_xor_sync(0xffffffffu, nonfinite, o);
+  }
+  if (lane == 0) {
+    red[warp] = amax;
+    bad[warp] = nonfinite;
+  }
+  __syncthreads();
+  if (row == 0) {
+    float a = 0.f;
+    int b = 0;
+    for (int i = 0; i < 8; ++i) {
+      a = fmaxf(a, red[i]);
+      b |= bad[i];
+    }
+    int ex = 0;
+    if (a > 0.f && !b) frexpf(a, &ex);
+    s_sc = (a > 0.f && !b) ? ldexpf(1.0f, 8 - ex) : 1.0f;  // |s c| < 2^8
+    s_bad = b;
+  }
+  __syncthreads();
+  const float sc = s_sc;
+  const bool cb_ok = !s_bad;
+  uint8_t* base = bprep + (size_t)mm * GeoK::bprep_bytes(ks);
+  double cn = 0.0, nb2 = 0.0, s1 = 0.0;
+  for (int k = 0; k < ks; ++k) {
+    const float cv = (real && cb_ok) ? c[k] * sc : 0.f;
+    const float bv = -2.0f * cv;
+    const __half hi = __float2half_rn(bv);
+    const __half lo = __float2half_rn(bv - __half2float(hi));
+    uint8_t* chunk = base + (size_t)(k / kKC) * GeoK::B_CHUNK;
+    *reinterpret_cast<__half*>(chunk + tc::kmajor_off(row, k % kKC, kKC)) = hi;
+    *reinterpret_cast<__half*>(chunk + GeoK::B_HI + tc::kmajor_off(row, k % kKC, kKC)) = lo;
+    cn += (double)cv * (double)cv;
+    nb2 += (double)bv * (double)bv;
+    s1 += fabs((double)bv);
+  }
+  double cmx = cn;
+  for (int o = 16; o > 0; o >>= 1) cmx = fmax(cmx, __shfl_xor_sync(0xffffffffu, cmx, o));
+  if (lane == 0) redd[warp] = cmx;
+  __syncthreads();
+  if (row == 0) {
+    double a = 0.0;
+    for (int i = 0; i < 8; ++i) a = fmax(a, redd[i]);
+    s_cn = a;
+  }
+  __syncthreads();
+  int ea = 0;
+  if (s_cn >= 16384.0) {
+    frexp(s_cn, &ea);
+    ea -= 14;
+  }
+  const double acn = ldexp(1.0, ea);
+  const double cvv = cn / acn;
+  const __half c_h = __double2half(cvv);
+  const double r1 = cvv - (double)__half2float(c_h);
+  const __half c_m = __double2half(r1);
+  const __half c_l = __double2half(r1 - (double)__half2float(c_m));
+  const __half p15 = __float2half_rn(32768.f);
+  const __half pad = __float2half_rn(real ? 0.f : 65504.f);
+  const __half z = __float2half_rn(0.f);
+  uint8_t* ext = base + (size_t)(ks / kKC) * GeoK::B_CHUNK;
+  *reinterpret_cast<uint4*>(ext + tc::kmajor_off(row, 0, kExt)) =
+      make_uint4(pack_h2(c_h, c_m), pack_h2(c_l, p15), pack_h2(p15, p15), pack_h2(pad, z));
+  *reinterpret_cast<uint4*>(ext + tc::kmajor_off(row, 8, kExt)) = make_uint4(0u, 0u, 0u, 0u);
+  float vb = real ? (float)sqrt(nb2) : 0.f, vc = real ? (float)cn : 0.f, v1 = real ? (float)s1 : 0.f;
+  for (int o = 16; o > 0; o >>= 1) {
+    vb = fmaxf(vb, __shfl_xor_sync(0xffffffffu, vb, o));
+    vc = fmaxf(vc, __shfl_xor_sync(0xffffffffu, vc, o));
+    v1 = fmaxf(v1, __shfl_xor_sync(0xffffffffu, v1, o));
+  }
+  if (lane == 0) {
+    rb[warp] = vb;
+    rc[warp] = vc;
+    r1s[warp] = v1;
+  }
+  __syncthreads();
+  if (row == 0) {
+    float a = 0.f, b2 = 0.f, d = 0.f;
+    for (int i = 0; i < 8; ++i) {
+      a = fmaxf(a, rb[i]);
+      b2 = fmaxf(b2, rc[i]);
+      d = fmaxf(d, r1s[i]);
+    }
+    float* o = cst + (size_t)mm * CST_LEN;
+    o[CST_S] = sc;
+    o[CST_ACN] = (float)acn;
+    o[CST_CB] = a * 1.0001f;
+    o[CST_CN] = b2 * 1.0001f;
+    o[CST_S1C] = d * 1.0001f;
+    o[CST_VALID] = cb_ok ? 1.f : 0.f;
+    o[6] = 0.f;
+    o[7] = 0.f;
+  }
+}
+
+// Exact float64 fallback for long subspaces: the codebook streams through shared memory
+// in 32-column chunks (all warps of a block in lockstep); each lane keeps the running
+// sequential sums of its 8 codewords, so the summation order is scipy cdist's.
+__global__ void __launch_bounds__(256) encode_exact_k_kernel(const float* __restrict__ x, int64_t n, int d,
+                                                            const float* __restrict__ cw, int m, int l, int ks,
+                                                            const uint32_t* __restrict__ flags,
+                                                            const unsigned int* __restrict__ counters,
+                                                            uint32_t flag_cap, uint8_t* __restrict__ codes, int stride) {
+  __shared__ float s_cb[256 * 33];
+  const int mm = blockIdx.y;
+  const bool all = counters[1] != 0;
+  const int64_t total = all ? n : (int64_t)min(counters[2 + mm], flag_cap);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const float* cb = cw + (size_t)mm * l * ks;
+  for (int64_t i0 = (int64_t)blockIdx.x * 8; i0 < total; i0 += (int64_t)gridDim.x * 8) {
+    const int64_t i = i0 + warp;
+    const bool active = i < total;
+    const int64_t row = active ? (all ? i : (int64_t)flags[(size_t)mm * flag_cap + i]) : 0;
+    const float* xv = x + row * d + (size_t)mm * ks;
+    double acc[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc[u] = 0.0;
+    int cbase[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) cbase[u] = min(lane + 32 * u, l - 1) * 33;
+    for (int k0 = 0; k0 < ks; k0 += 32) {
+      __syncthreads();
+      for (int e = threadIdx.x; e < l * 32; e += blockDim.x) {
+        const int c = e >> 5, k = e & 31;
+        s_cb[c * 33 + k] = cb[(size_t)c * ks + k0 + k];
+      }
+      __syncthreads();
+      const float xk_lane = active ? xv[k0 + lane] : 0.f;
+      for (int k = 0; k < 32; ++k) {
+        const double xk = (double)__shfl_sync(0xffffffffu, xk_lane, k);
+        double df[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) df[u] = __dsub_rn(xk, (double)s_cb[cbase[u] + k]);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) df[u] = __dmul_rn(df[u], df[u]);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc[u] = __dadd_rn(acc[u], df[u]);
+      }
+    }
+    double best = __longlong_as_double(0x7ff0000000000000LL);
+    int bl = 0x7fffffff;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int c = lane + 32 * u;
+      if (argmin_less(acc[u], c, best, bl)) {
+        best = acc[u];
+        bl = c;
+      }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bl, o);
+      if (argmin_less(ob, oi, best, bl)) {
+        best = ob;
+        bl = oi;
+      }
+    }
+    if (active && lane == 0) codes[row * stride + mm] = (uint8_t)bl;
+  }
+}
+
 __global__ void encode_stats_kernel(const unsigned int* __restrict__ counters, unsigned long long* __restrict__ out) {
   *out += (unsigned long long)counters[0];  // pairs not certified (all re-decided in fp64)
 }
@@ -889,10 +1381,79 @@ int launch_encode_tc(const float* d_x, int64_t n, int d, const float* d_cw, int 
   PQK_LAUNCH_CHECK("encode_stats_kernel");
   return PQK_OK;
 }
+// K-streamed launch for long subspaces (ks % 32 == 0, 96 <= ks <= 1024)
+int launch_encode_tck(const float* d_x, int64_t n, int d, const float* d_cw, int m, int l, int ks, uint8_t* d_codes,
+                      int stride, unsigned long long* flagged_out, cudaStream_t stream) {
+  using namespace enc;
+  using G = GeoK;
+  const DevInfo& di = dev_info();
+  int dev = 0;
+  cudaGetDevice(&dev);
+  EncWS& ws = g_encws[dev & 63];
+  std::lock_guard<std::mutex> lock(ws.mu);
+  const size_t b_bytes = (size_t)m * G::bprep_bytes(ks);
+  const uint32_t cap = (uint32_t)std::min<int64_t>(n, n / 128 + 4096);
+  const size_t need = align_up(b_bytes, 256) + align_up((size_t)m * CST_LEN * 4, 256) +
+                      align_up((size_t)m * cap * 4, 256) + align_up((size_t)(m + 2) * 4, 256);
+  if (ws.bytes < need) {
+    if (ws.p) cudaFree(ws.p);
+    ws.p = nullptr;
+    ws.bytes = 0;
+    PQK_CUDA_TRY(cudaMalloc(&ws.p, need));
+    ws.bytes = need;
+  }
+  char* base = static_cast<char*>(ws.p);
+  uint8_t* bprep = reinterpret_cast<uint8_t*>(base);
+  float* cst = reinterpret_cast<float*>(base + align_up(b_bytes, 256));
+  uint32_t* flags = reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(cst) + align_up((size_t)m * CST_LEN * 4, 256));
+  unsigned int* counters =
+      reinterpret_cast<unsigned int*>(reinterpret_cast<char*>(flags) + align_up((size_t)m * cap * 4, 256));
+
+  CUtensorMap map;
+  auto encoder = tensor_map_encoder();
+  if (!encoder) return fail(PQK_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  const cuuint64_t dims[2] = {(cuuint64_t)d, (cuuint64_t)n};
+  const cuuint64_t strides[1] = {(cuuint64_t)d * 4};
+  const cuuint32_t box[2] = {(cuuint32_t)kKC, (cuuint32_t)kRows};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult cr = encoder(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(d_x), dims, strides, box,
+                              estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (cr != CUDA_SUCCESS) return fail(PQK_ECUDA, "cuTensorMapEncodeTiled failed");
+
+  PQK_CUDA_TRY(cudaMemsetAsync(counters, 0, (size_t)(m + 2) * 4, stream));
+  encode_prep_k_kernel<<<m, 256, 0, stream>>>(d_cw, m, l, ks, bprep, cst);
+  PQK_LAUNCH_CHECK("encode_prep_k_kernel");
+  EncParams ep{};
+  ep.bprep = bprep;
+  ep.cst = cst;
+  ep.n = n;
+  ep.m = m;
+  ep.ks = ks;
+  ep.codes = d_codes;
+  ep.stride = stride;
+  ep.flags = flags;
+  ep.counters = counters;
+  ep.flag_cap = cap;
+  ep.ntiles = (int)((n + kRows - 1) / kRows);
+  ep.tstride = std::max(1, std::min(di.sms / m, ep.ntiles));
+  ep.keymask = ~31u;
+  ep.one = 1u;
+  PQK_CUDA_TRY(cudaFuncSetAttribute(encode_tck_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM));
+  encode_tck_kernel<<<ep.tstride * m, kThreads, G::SMEM, stream>>>(map, ep);
+  PQK_LAUNCH_CHECK("encode_tck_kernel");
+  const dim3 egrid((unsigned)std::max(1, 2 * di.sms / m), (unsigned)m);
+  encode_exact_k_kernel<<<egrid, 256, 0, stream>>>(d_x, n, d, d_cw, m, l, ks, flags, counters, cap, d_codes, stride);
+  PQK_LAUNCH_CHECK("encode_exact_k_kernel");
+  encode_stats_kernel<<<1, 1, 0, stream>>>(counters, flagged_out);
+  PQK_LAUNCH_CHECK("encode_stats_kernel");
+  return PQK_OK;
+}
 }  // namespace
 
 // Tensor-core encoder eligibility and launch (called by pqk_encode_device): dsub in
-// {8, 16, 32, 64}, at most one CTA per subspace per SM, 16-byte aligned rows.
+// {8, 16, 32, 64} (operands resident in shared memory) or a multiple of 32 in [96, 1024]
+// (K-streamed), at most one CTA per subspace per SM, 16-byte aligned rows.
 int encode_tc_try(const float* d_x, int64_t n, int d, const float* d_cw, int m, int l, uint8_t* d_codes, int stride,
                   unsigned long long* flagged_out, cudaStream_t stream, bool* used) {
   *used = false;
@@ -917,7 +1478,9 @@ int encode_tc_try(const float* d_x, int64_t n, int d, const float* d_cw, int m, 
       rc = launch_encode_tc<64>(d_x, n, d, d_cw, m, l, ks, d_codes, stride, flagged_out, stream);
       break;
     default:
-      return PQK_OK;
+      // long subspaces: K-streamed kernel (codebook chunks through shared memory)
+      if (ks % enc::kKC != 0 || ks < 96 || ks > 1024 || (size_t)enc::GeoK::SMEM > (size_t)di.smem_optin) return PQK_OK;
+      rc = launch_encode_tck(d_x, n, d, d_cw, m, l, ks, d_codes, stride, flagged_out, stream);
   }
   if (rc == PQK_OK) *used = true;
   return rc;

@@ -428,7 +428,7 @@ def encode_host(codewords: np.ndarray, vectors: np.ndarray, *, device=None, stri
     with torch.cuda.device(dev):
         out = encode_device(
             torch.from_numpy(np.ascontiguousarray(vectors, dtype=np.float32)).to(dev),
-            torch.from_numpy(np.ascontiguousarray(codewords, dtype=np.float32)).to(dev),
+            torch.from_numpy(np.array(codewords, dtype=np.float32)).to(dev),  # (read-only codebooks)
             m,
             l,
             dev,

@@ -18,7 +18,9 @@ def _encode(cw, x):
 
 @pytest.mark.parametrize("m,sub,l_count,n", [(4, 32, 256, 5000), (8, 16, 256, 3001), (2, 64, 256, 1000),
                                               (1, 32, 100, 777), (4, 16, 7, 129), (3, 32, 256, 1),
-                                              (16, 8, 256, 2000), (2, 8, 33, 500), (5, 64, 256, 300)])
+                                              (16, 8, 256, 2000), (2, 8, 33, 500), (5, 64, 256, 300),
+                                              (2, 96, 256, 700), (3, 128, 100, 1300), (1, 256, 256, 400),
+                                              (2, 512, 256, 300)])
 def test_tc_encode_random(oracle, m, sub, l_count, n):
     cw = random_codebook(m, l_count, sub, seed=m * 100 + sub + l_count)
     x = np.random.default_rng(n).normal(size=(n, m * sub)).astype(np.float32)
@@ -125,3 +127,15 @@ def test_tc_encode_sift_like_flag_rate():
     stats = torch.zeros(_lib.STATS_LEN, dtype=torch.int64, device=dev)
     engine.encode_device(torch.from_numpy(x).to(dev), torch.from_numpy(cw).to(dev), 4, 256, dev, stride=4, stats=stats)
     assert int(stats[_lib.STAT_ENCODE_FLAGGED].item()) < 100_000 * 4 * 1e-3
+
+
+def test_tc_encode_config3_shape(oracle):
+    """BASELINE config 3's shape: 4096-D deep-feature-like vectors, M=8 (512-D subspaces,
+    the K-streamed tensor-core kernel), codewords drawn from the data."""
+    from paper_1709_03708_b200 import synth
+
+    x = synth.deep_like(3000, 11, components=300)
+    rng = np.random.default_rng(2)
+    cw = x[rng.choice(3000, 256, replace=False)].reshape(256, 8, 512).transpose(1, 0, 2).copy()
+    cw += rng.normal(0, 1e-3, size=cw.shape).astype(np.float32)
+    np.testing.assert_array_equal(_encode(cw, x), oracle.encode(cw, x))

@@ -40,6 +40,10 @@ CONFIGS = {
                workload="config5 shard mixture N=1.25e7/GPU K=1e5 M=16 L=256"),
     "c4": dict(n=125_000_000, k=100_000, m=4, l=256, dim=128, gpu_data="sift",
                workload="config4 shard SIFT-like N=1.25e8/GPU K=1e5 M=4 L=256"),
+    # config 3 on one GPU: 1e7 deep-feature-like 4096-D vectors generated on the device in
+    # chunks and encoded there (K-streamed tensor-core encoder, 512-D subspaces)
+    "c3": dict(n=10_000_000, k=10_000, m=8, l=256, dim=4096, gpu_data="deep",
+               workload="config3 deep-feature-like N=1e7 K=1e4 M=8 L=256 (D=4096, GPU-encoded)"),
 }
 SEED = 20260419
 
@@ -55,6 +59,10 @@ def make_vectors(cfg_name: str, n: int, rank: int) -> np.ndarray:
 
     if cfg_name == "c1":
         return synth.mixture(n, 128, 1000, synth.stage_seed(SEED, 100 + rank))
+    if cfg_name == "c5":
+        return synth.mixture(n, 128, 100_000, synth.stage_seed(SEED, 100 + rank))
+    if cfg_name == "c3":
+        return synth.deep_like(n, synth.stage_seed(SEED, 100 + rank))
     return synth.sift_like(n, synth.stage_seed(SEED, 100 + rank))
 
 
@@ -82,9 +90,25 @@ def mixture_gpu(n: int, seed: int, dev, dim: int = 128, components: int = 100_00
     return (means[lab] + sigma * torch.randn((n, dim), generator=g, device=dev)).contiguous()
 
 
+def deep_like_gpu(n: int, seed: int, dev, dim: int = 4096, components: int = 10_000, sigma: float = 0.5):
+    """Device-side config-3 vectors: ReLU(mixture of N(0,1) means, sigma 0.5), L2-normalised."""
+    import torch
+
+    g = torch.Generator(device=dev)
+    g.manual_seed(SEED)
+    means = torch.randn((components, dim), generator=g, device=dev)
+    g.manual_seed(seed)
+    lab = torch.randint(0, components, (n,), generator=g, device=dev)
+    x = (means[lab] + sigma * torch.randn((n, dim), generator=g, device=dev)).clamp_min_(0.0)
+    return (x / x.norm(dim=1, keepdim=True).clamp_min(1e-12)).contiguous()
+
+
 def make_codebook(cfg_name: str, m: int, l_count: int) -> np.ndarray:
     from paper_1709_03708_b200 import synth
 
+    if cfg_name == "c3":  # bench set-up: 4 Lloyd iterations on a 20k sample of the same distribution
+        sample = synth.deep_like(20_000, synth.stage_seed(SEED, 1))
+        return synth.train_codebook_fast(sample, m, l_count, iterations=4, seed=synth.stage_seed(SEED, 2))
     if cfg_name == "c1":
         sample = synth.mixture(20_000, 128, 1000, synth.stage_seed(SEED, 1))
     elif cfg_name == "c5":
@@ -201,9 +225,10 @@ def run_reference(args) -> None:
     cfg = CONFIGS[cfgn]
     book = make_codebook(cfgn, cfg["m"], cfg["l"])
     tables = O.build_distance_tables(book)
-    vectors = make_vectors(cfgn, cfg["n"], 0)
+    ns = min(cfg["n"], max(60_000, cfg["k"] + 10_000))  # bounded host sample of the workload's vectors
+    vectors = make_vectors(cfgn, ns, 0)
     rng = np.random.default_rng(SEED)
-    cidx = rng.choice(cfg["n"], size=cfg["k"], replace=False)
+    cidx = rng.choice(ns, size=cfg["k"], replace=False)
     centers = O.encode(book, vectors[cidx])
     codes = np.concatenate([O.encode(book, vectors[s : s + 10_000]) for s in range(0, min(cfg["n"], 50_000), 10_000)])
     vals = []
@@ -290,11 +315,12 @@ def main() -> None:
         if cfg.get("gpu_data"):
             # billion-scale shard: vectors generated on device per seeded chunk, encoded in place
             codes_dev = torch.empty((n_loc, mp), dtype=torch.uint8, device=dev)
-            chunk = 1 << 23  # 8 Mi vectors (4 GiB fp32) per encode call
+            chunk = (1 << 32) // (4 * cfg["dim"])  # 4 GiB of fp32 vectors per encode call
+            gen = {"mixture": mixture_gpu, "sift": sift_like_gpu, "deep": deep_like_gpu}[cfg["gpu_data"]]
             for s in range(0, n_loc, chunk):
                 e = min(n_loc, s + chunk)
                 cseed = synth.stage_seed(SEED, 1000 + rank * 100_000 + s // chunk)
-                vec = (mixture_gpu(e - s, cseed, dev) if cfg["gpu_data"] == "mixture" else sift_like_gpu(e - s, cseed, dev))
+                vec = gen(e - s, cseed, dev)
                 e0.record()
                 codes_dev[s:e] = engine.encode_device(vec, cw_dev, m, l_count, dev, stride=mp, stats=stats_enc)
                 e1.record()
@@ -464,6 +490,8 @@ def main() -> None:
                      "flagged_pairs": enc_flagged,
                      "kernel": ("encode_tc_kernel (tcgen05 fp16 hi/lo split, certified argmin, fp64 fallback)"
                                 if (cfg["dim"] // m) in (8, 16, 32, 64) else
+                                "encode_tck_kernel (K-streamed tcgen05, certified argmin, fp64 fallback)"
+                                if (cfg["dim"] // m) % 32 == 0 and 96 <= cfg["dim"] // m <= 1024 else
                                 "encode_kernel (SIMT fp32 filter + fp64 certificate)")}
     if out_train:
         out["codebook_training"] = out_train

@@ -1214,69 +1214,92 @@ __global__ void __launch_bounds__(256) encode_prep_k_kernel(const float* __restr
   }
 }
 
-// Exact float64 fallback for long subspaces: the codebook streams through shared memory
-// in 32-column chunks (all warps of a block in lockstep); each lane keeps the running
-// sequential sums of its 8 codewords, so the summation order is scipy cdist's.
+// Exact float64 fallback for long subspaces (the pairs the tensor-core certificate left):
+// the codebook streams through shared memory in 32-column chunks converted to float64 once
+// per chunk (all warps of a block in lockstep); each warp decides two rows at a time, each
+// lane keeping the running sequential sums of its 8 codewords for both, so the summation
+// order is scipy cdist's and the argmin np.argmin's (first NaN, else lowest index).
+constexpr int kExactRows = 4;
+
 __global__ void __launch_bounds__(256) encode_exact_k_kernel(const float* __restrict__ x, int64_t n, int d,
                                                             const float* __restrict__ cw, int m, int l, int ks,
                                                             const uint32_t* __restrict__ flags,
                                                             const unsigned int* __restrict__ counters,
                                                             uint32_t flag_cap, uint8_t* __restrict__ codes, int stride) {
-  __shared__ float s_cb[256 * 33];
+  extern __shared__ double s_cbd[];  // 256 x 33 float64
   const int mm = blockIdx.y;
   const bool all = counters[1] != 0;
   const int64_t total = all ? n : (int64_t)min(counters[2 + mm], flag_cap);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const float* cb = cw + (size_t)mm * l * ks;
-  for (int64_t i0 = (int64_t)blockIdx.x * 8; i0 < total; i0 += (int64_t)gridDim.x * 8) {
-    const int64_t i = i0 + warp;
-    const bool active = i < total;
-    const int64_t row = active ? (all ? i : (int64_t)flags[(size_t)mm * flag_cap + i]) : 0;
-    const float* xv = x + row * d + (size_t)mm * ks;
-    double acc[8];
+  int cbase[8];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) acc[u] = 0.0;
-    int cbase[8];
+  for (int u = 0; u < 8; ++u) cbase[u] = min(lane + 32 * u, l - 1) * 33;  // c >= l aliases l - 1
+  constexpr int kRowsPerBlock = 8 * kExactRows;
+  for (int64_t i0 = (int64_t)blockIdx.x * kRowsPerBlock; i0 < total; i0 += (int64_t)gridDim.x * kRowsPerBlock) {
+    bool active[kExactRows];
+    int64_t row[kExactRows];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) cbase[u] = min(lane + 32 * u, l - 1) * 33;
+    for (int r = 0; r < kExactRows; ++r) {
+      const int64_t i = i0 + warp * kExactRows + r;
+      active[r] = i < total;
+      row[r] = active[r] ? (all ? i : (int64_t)flags[(size_t)mm * flag_cap + i]) : 0;
+    }
+    double acc[kExactRows][8];
+#pragma unroll
+    for (int r = 0; r < kExactRows; ++r)
+#pragma unroll
+      for (int u = 0; u < 8; ++u) acc[r][u] = 0.0;
     for (int k0 = 0; k0 < ks; k0 += 32) {
       __syncthreads();
       for (int e = threadIdx.x; e < l * 32; e += blockDim.x) {
         const int c = e >> 5, k = e & 31;
-        s_cb[c * 33 + k] = cb[(size_t)c * ks + k0 + k];
+        s_cbd[c * 33 + k] = (double)cb[(size_t)c * ks + k0 + k];
       }
       __syncthreads();
-      const float xk_lane = active ? xv[k0 + lane] : 0.f;
+      float xl[kExactRows];
+#pragma unroll
+      for (int r = 0; r < kExactRows; ++r) xl[r] = active[r] ? x[row[r] * d + (size_t)mm * ks + k0 + lane] : 0.f;
+#pragma unroll 2
       for (int k = 0; k < 32; ++k) {
-        const double xk = (double)__shfl_sync(0xffffffffu, xk_lane, k);
-        double df[8];
+        double c[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) df[u] = __dsub_rn(xk, (double)s_cb[cbase[u] + k]);
+        for (int u = 0; u < 8; ++u) c[u] = s_cbd[cbase[u] + k];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) df[u] = __dmul_rn(df[u], df[u]);
+        for (int r = 0; r < kExactRows; ++r) {
+          const double xk = (double)__shfl_sync(0xffffffffu, xl[r], k);
+          double df[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) acc[u] = __dadd_rn(acc[u], df[u]);
+          for (int u = 0; u < 8; ++u) df[u] = __dsub_rn(xk, c[u]);
+#pragma unroll
+          for (int u = 0; u < 8; ++u) df[u] = __dmul_rn(df[u], df[u]);
+#pragma unroll
+          for (int u = 0; u < 8; ++u) acc[r][u] = __dadd_rn(acc[r][u], df[u]);
+        }
       }
     }
-    double best = __longlong_as_double(0x7ff0000000000000LL);
-    int bl = 0x7fffffff;
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int c = lane + 32 * u;
-      if (argmin_less(acc[u], c, best, bl)) {
-        best = acc[u];
-        bl = c;
+    for (int r = 0; r < kExactRows; ++r) {
+      double best = __longlong_as_double(0x7ff0000000000000LL);
+      int bl = 0x7fffffff;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int c = lane + 32 * u;
+        if (argmin_less(acc[r][u], c, best, bl)) {
+          best = acc[r][u];
+          bl = c;
+        }
       }
-    }
-    for (int o = 16; o > 0; o >>= 1) {
-      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-      const int oi = __shfl_xor_sync(0xffffffffu, bl, o);
-      if (argmin_less(ob, oi, best, bl)) {
-        best = ob;
-        bl = oi;
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bl, o);
+        if (argmin_less(ob, oi, best, bl)) {
+          best = ob;
+          bl = oi;
+        }
       }
+      if (active[r] && lane == 0) codes[row[r] * stride + mm] = (uint8_t)bl;
     }
-    if (active && lane == 0) codes[row * stride + mm] = (uint8_t)bl;
   }
 }
 
@@ -1319,7 +1342,7 @@ int launch_encode_tc(const float* d_x, int64_t n, int d, const float* d_cw, int 
   EncWS& ws = g_encws[dev & 63];
   std::lock_guard<std::mutex> lock(ws.mu);
   const size_t b_bytes = (size_t)m * G::B_BYTES;
-  const uint32_t cap = (uint32_t)std::min<int64_t>(n, n / 128 + 4096);  // flagged rows per subspace
+  const uint32_t cap = (uint32_t)std::min<int64_t>(n, n / 4 + 4096);  // flagged rows per subspace
   const size_t need = align_up(b_bytes, 256) + align_up((size_t)m * CST_LEN * 4, 256) +
                       align_up((size_t)m * cap * 4, 256) + align_up((size_t)(m + 2) * 4, 256);
   if (ws.bytes < need) {
@@ -1392,7 +1415,7 @@ int launch_encode_tck(const float* d_x, int64_t n, int d, const float* d_cw, int
   EncWS& ws = g_encws[dev & 63];
   std::lock_guard<std::mutex> lock(ws.mu);
   const size_t b_bytes = (size_t)m * G::bprep_bytes(ks);
-  const uint32_t cap = (uint32_t)std::min<int64_t>(n, n / 128 + 4096);
+  const uint32_t cap = (uint32_t)std::min<int64_t>(n, n / 4 + 4096);  // flagged rows per subspace
   const size_t need = align_up(b_bytes, 256) + align_up((size_t)m * CST_LEN * 4, 256) +
                       align_up((size_t)m * cap * 4, 256) + align_up((size_t)(m + 2) * 4, 256);
   if (ws.bytes < need) {
@@ -1443,7 +1466,10 @@ int launch_encode_tck(const float* d_x, int64_t n, int d, const float* d_cw, int
   encode_tck_kernel<<<ep.tstride * m, kThreads, G::SMEM, stream>>>(map, ep);
   PQK_LAUNCH_CHECK("encode_tck_kernel");
   const dim3 egrid((unsigned)std::max(1, 2 * di.sms / m), (unsigned)m);
-  encode_exact_k_kernel<<<egrid, 256, 0, stream>>>(d_x, n, d, d_cw, m, l, ks, flags, counters, cap, d_codes, stride);
+  const int esmem = 256 * 33 * 8;
+  PQK_CUDA_TRY(cudaFuncSetAttribute(encode_exact_k_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, esmem));
+  encode_exact_k_kernel<<<egrid, 256, esmem, stream>>>(d_x, n, d, d_cw, m, l, ks, flags, counters, cap, d_codes,
+                                                       stride);
   PQK_LAUNCH_CHECK("encode_exact_k_kernel");
   encode_stats_kernel<<<1, 1, 0, stream>>>(counters, flagged_out);
   PQK_LAUNCH_CHECK("encode_stats_kernel");

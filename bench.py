@@ -315,6 +315,7 @@ def main() -> None:
         if cfg.get("gpu_data"):
             # billion-scale shard: vectors generated on device per seeded chunk, encoded in place
             codes_dev = torch.empty((n_loc, mp), dtype=torch.uint8, device=dev)
+            enc_flagged_sum = 0
             chunk = (1 << 32) // (4 * cfg["dim"])  # 4 GiB of fp32 vectors per encode call
             gen = {"mixture": mixture_gpu, "sift": sift_like_gpu, "deep": deep_like_gpu}[cfg["gpu_data"]]
             for s in range(0, n_loc, chunk):
@@ -326,6 +327,7 @@ def main() -> None:
                 e1.record()
                 torch.cuda.synchronize(dev)
                 enc_ms += e0.elapsed_time(e1)
+                enc_flagged_sum += int(stats_enc[_lib.STAT_ENCODE_FLAGGED].item())  # per call
                 del vec
         else:
             vectors = make_vectors(cfgn, n_loc, rank)
@@ -342,7 +344,7 @@ def main() -> None:
             enc_ms = min(times)
             del vec_dev
         codes_host = engine.download_codes(codes_dev, m)
-        enc_flagged = int(stats_enc[_lib.STAT_ENCODE_FLAGGED].item())
+        enc_flagged = enc_flagged_sum if cfg.get("gpu_data") else int(stats_enc[_lib.STAT_ENCODE_FLAGGED].item())
         del codes_dev
     log(f"[bench] rank {rank}: workload ready in {time.perf_counter() - t0:.1f}s")
 

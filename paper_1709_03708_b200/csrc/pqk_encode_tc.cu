@@ -113,6 +113,7 @@ constexpr int kEpiWarps = 8;   // 2 per TMEM lane quadrant: one per accumulator
 constexpr int kTrWarps = 8;    // transform warps (16 rows each)
 constexpr int kThreads = (2 + kEpiWarps + kTrWarps) * 32;
 constexpr int kChunk = 32;     // epilogue columns per tcgen05.ld pair
+constexpr bool kMmaHalves = false;  // N=128 MMA halves (separately released) vs N=256
 constexpr float kX2Limit = 1073741824.0f;  // 2^30: |s x|^2 bound for the fp16 extension parts
 
 // per-subspace constants written by encode_prep_kernel (floats)
@@ -394,9 +395,11 @@ __global__ void __launch_bounds__(kThreads, 1) encode_tc_kernel(const __grid_con
   } else if (warp == 1) {
     // ---------------- MMA issuer ----------------
     if (lane == 0) {
-      // two N = 128 halves per accumulator, each released separately by the epilogue, so
-      // that the next item's first half runs while the epilogue still reads the second
-      const uint32_t idesc = tc::idesc_f16_f32(kRows, kN / 2);
+      // kMmaHalves: two N = 128 halves per accumulator, each released separately by the
+      // epilogue (the next item's first half can run while the epilogue reads the second);
+      // otherwise one N = 256 instruction per K step, both halves committed together
+      constexpr int NH = kMmaHalves ? 2 : 1;
+      const uint32_t idesc = tc::idesc_f16_f32(kRows, kN / NH);
       constexpr uint32_t sboE = (uint32_t)(KE / 8) * 128, sboP = (uint32_t)(KP / 8) * 128;
       const uint32_t b_hi0 = smem_u32(sB), b_lo0 = smem_u32(sB + G::B_HI);
       for (int w = 0; w < items; ++w) {
@@ -409,8 +412,9 @@ __global__ void __launch_bounds__(kThreads, 1) encode_tc_kernel(const __grid_con
         for (int j = 0; j < kTrWarps; ++j) lo_any |= s_lo[ab * kTrWarps + j];
         const uint32_t a_hi = smem_u32(sA + ab * G::A_BYTES), a_lo = a_hi + G::A_HI;
 #pragma unroll
-        for (int hf = 0; hf < 2; ++hf) {
+        for (int hf = 0; hf < NH; ++hf) {
           mbar_wait_spin(&tempty[2 * ab + hf], ph ^ 1u);
+          if (NH == 1) mbar_wait_spin(&tempty[2 * ab + 1], ph ^ 1u);
           tc::fence_after();
           const uint32_t tacc = tbase + (uint32_t)ab * kN + (uint32_t)hf * (kN / 2);
           const uint32_t b_hi = b_hi0 + (uint32_t)hf * 16u * sboE, b_lo = b_lo0 + (uint32_t)hf * 16u * sboP;
@@ -433,6 +437,7 @@ __global__ void __launch_bounds__(kThreads, 1) encode_tc_kernel(const __grid_con
           tc::mma_f16(tacc, tc::smem_desc(a_hi + (KP / 16) * 256, 128, sboE),
                       tc::smem_desc(b_hi + (KP / 16) * 256, 128, sboE), idesc, 1u);
           tc::commit(&tfull[2 * ab + hf]);
+          if (NH == 1) tc::commit(&tfull[2 * ab + 1]);
         }
         tc::commit(&aempty[ab]);
       }

@@ -486,6 +486,33 @@ def main() -> None:
         hbm_peak = float(json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"])
     except Exception:
         pass
+    # code streaming (north_star: HBM roofline fraction): the histogram pass reads every code
+    # row (MP bytes) and label (4 B) and the objective pass every sd (8 B); timed with events
+    # on the resident engine after the bench steps (its labels/sd are the last iteration's)
+    with torch.cuda.device(dev):
+        cs_h, cs_o = [], []
+        for _ in range(5):
+            flush.fill_(1)
+            torch.cuda.synchronize(dev)
+            e0.record()
+            eng.histogram()
+            e1.record()
+            eng.objective()
+            e2 = torch.cuda.Event(enable_timing=True)
+            e2.record()
+            torch.cuda.synchronize(dev)
+            cs_h.append(e0.elapsed_time(e1))
+            cs_o.append(e1.elapsed_time(e2))
+    h_ms, o_ms = float(np.median(cs_h)), float(np.median(cs_o))
+    h_bytes, o_bytes = n_loc * (mp + 4), n_loc * 8
+    out["code_streaming"] = {
+        "histogram_ms": h_ms, "histogram_gbs": h_bytes / (h_ms / 1e3) / 1e9,
+        "histogram_hbm_frac": h_bytes / (h_ms / 1e3) / 1e9 / hbm_peak,
+        "objective_ms": o_ms, "objective_gbs": o_bytes / (o_ms / 1e3) / 1e9,
+        "objective_hbm_frac": o_bytes / (o_ms / 1e3) / 1e9 / hbm_peak,
+        "note": "histogram: codes (MP B) + labels (4 B) per code, atomics into K x M x 256 int32 (L2); objective: "
+                "8 B sd per code through numpy's pairwise tree; L2 flushed before each; small at config 2 "
+                "(launch- and atomic-latency bound), scales with N (configs 4/5)"}
     out["encode"] = {"vectors": n_loc, "ms": enc_ms, "vectors_per_s": n_loc / (enc_ms / 1e3),
                      "hbm_gbs": enc_bytes / (enc_ms / 1e3) / 1e9,
                      "hbm_frac": enc_bytes / (enc_ms / 1e3) / 1e9 / hbm_peak,

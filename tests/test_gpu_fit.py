@@ -116,3 +116,14 @@ def test_validation(pqk):
         pqk.fit(codes, tables, 2, update="fancy")
     with pytest.raises(ValueError, match="initial_centers has"):
         pqk.fit(codes, tables, 2, initial_centers=np.zeros((3, 1), dtype=np.uint8))
+
+
+@pytest.mark.parametrize("m,n,k,iters", [(16, 120_000, 3000, 4), (32, 30_000, 700, 3), (12, 20_000, 1500, 3)])
+def test_fit_long_codes_matches_oracle(pqk, oracle, m, n, k, iters):
+    """Long codes (BASELINE config 5's M=16, and M=32 / a padded M=12) on clustered data:
+    the M=16/32 scan variants, their vote and repair paths, several K chunks."""
+    tables = random_tables(m, 256, seed=50 + m, sub_dim=4)
+    codes = mixture_codes(n, m, 256, 400, seed=m)
+    res = pqk.fit(codes, tables, k, max_iterations=iters, seed=m)
+    ref = oracle.fit(codes, tables, k, max_iterations=iters, seed=m, scan=oracle.assign_c)
+    _compare(res, ref)

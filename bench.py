@@ -279,6 +279,11 @@ def main() -> None:
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # PQK_BENCH_BACKEND=gloo: functional check of the N>1 code path on a box with fewer GPUs
+    # than ranks (ranks share devices; the timing of such a run means nothing)
+    backend_name = os.environ.get("PQK_BENCH_BACKEND", "nccl")
+    if backend_name != "nccl":
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     use_dist = world > 1 or args.dist
@@ -289,7 +294,10 @@ def main() -> None:
         os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         os.environ.setdefault("MASTER_PORT", "29517")
-        dist.init_process_group("nccl", device_id=dev, rank=rank, world_size=world)
+        if backend_name == "nccl":
+            dist.init_process_group("nccl", device_id=dev, rank=rank, world_size=world)
+        else:
+            dist.init_process_group(backend_name, rank=rank, world_size=world)
     lib = _lib.load()
 
     cfgn = args.config

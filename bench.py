@@ -441,7 +441,7 @@ def main() -> None:
     prof = ROOT / "profiles" / "scan_traffic.json"
     if prof.exists():
         try:
-            traffic = json.loads(prof.read_text()).get(cfgn)
+            traffic = json.loads(prof.read_text()).get(cfgn)  # DRAM bytes per scan launch (ncu)
         except Exception:
             traffic = None
 

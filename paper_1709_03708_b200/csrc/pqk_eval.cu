@@ -170,31 +170,31 @@ __global__ void __launch_bounds__(256) cluster_means_kernel(const T* __restrict_
   }
 }
 
-// numpy pairwise_sum (loops_utils.h.src) of f(0..n-1), f computed on the fly
+// numpy pairwise_sum of one row by a group of 8 lanes: lane j of the group owns numpy's
+// accumulator r[j] (elements j, j + 8, j + 16, ... added in order), the 8 accumulators are
+// combined as ((r0 + r1) + (r2 + r3)) + ((r4 + r5) + (r6 + r7)) by xor-shuffles (IEEE
+// addition is commutative, so every lane ends with the same value), the tail (n % 8) and
+// rows shorter than 8 are added in order; rows longer than 128 split as numpy does.
 template <typename F>
-__device__ double np_pairwise_fn(const F& f, int off, int n) {
+__device__ double np_pairwise8(const F& f, int off, int n, int j) {
   if (n < 8) {
     double r = 0.0;
     for (int i = 0; i < n; ++i) r = __dadd_rn(r, f(off + i));
     return r;
   }
   if (n <= 128) {
-    double r[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) r[j] = f(off + j);
-    int i = 8;
-    for (; i < n - (n % 8); i += 8) {
-#pragma unroll
-      for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], f(off + i + j));
-    }
-    double s = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
-                         __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
-    for (; i < n; ++i) s = __dadd_rn(s, f(off + i));
-    return s;
+    double r = f(off + j);
+    const int full = n - (n % 8);
+    for (int i = 8; i < full; i += 8) r = __dadd_rn(r, f(off + i + j));
+    r = __dadd_rn(r, __shfl_xor_sync(0xffffffffu, r, 1));
+    r = __dadd_rn(r, __shfl_xor_sync(0xffffffffu, r, 2));
+    r = __dadd_rn(r, __shfl_xor_sync(0xffffffffu, r, 4));
+    for (int i = full; i < n; ++i) r = __dadd_rn(r, f(off + i));
+    return r;
   }
   int n2 = n / 2;
   n2 -= n2 % 8;
-  return __dadd_rn(np_pairwise_fn(f, off, n2), np_pairwise_fn(f, off + n2, n - n2));
+  return __dadd_rn(np_pairwise8(f, off, n2, j), np_pairwise8(f, off + n2, n - n2, j));
 }
 
 template <typename T>
@@ -207,14 +207,18 @@ struct SqDiff {
   }
 };
 
+// sq[i] for 4 rows per warp (8 lanes per row; loads of 8 consecutive elements per row)
 template <typename T>
-__global__ void __launch_bounds__(128) assigned_sq_kernel(const T* __restrict__ x, int64_t n, int d,
+__global__ void __launch_bounds__(256) assigned_sq_kernel(const T* __restrict__ x, int64_t n, int d,
                                                          const double* __restrict__ centers,
                                                          const int32_t* __restrict__ labels, double* __restrict__ sq) {
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const SqDiff<T> f{x + i * d, centers + (size_t)labels[i] * d};
-  sq[i] = np_pairwise_fn(f, 0, d);
+  const int lane = threadIdx.x & 31;
+  const int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 3;
+  const bool valid = row < n;
+  const int64_t rr = valid ? row : n - 1;  // whole warps stay convergent for the shuffles
+  const SqDiff<T> f{x + rr * d, centers + (size_t)labels[rr] * d};
+  const double v = np_pairwise8(f, 0, d, lane & 7);
+  if (valid && (lane & 7) == 0) sq[row] = v;
 }
 
 }  // namespace ev
@@ -336,11 +340,11 @@ extern "C" int pqk_assigned_sq_device(const void* d_x, int32_t dtype, int64_t n,
   cudaStream_t stream = (cudaStream_t)stream_;
   if (!d_x || n < 1 || d < 1 || !d_centers || !d_labels || !d_sq || (dtype != 0 && dtype != 1))
     return fail(PQK_EINVAL, "pqk_assigned_sq_device: bad arguments");
-  const unsigned g = (unsigned)((n + 127) / 128);
+  const unsigned g = (unsigned)((n * 8 + 255) / 256);  // 8 lanes per row
   if (dtype == 0)
-    ev::assigned_sq_kernel<float><<<g, 128, 0, stream>>>(static_cast<const float*>(d_x), n, d, d_centers, d_labels, d_sq);
+    ev::assigned_sq_kernel<float><<<g, 256, 0, stream>>>(static_cast<const float*>(d_x), n, d, d_centers, d_labels, d_sq);
   else
-    ev::assigned_sq_kernel<double><<<g, 128, 0, stream>>>(static_cast<const double*>(d_x), n, d, d_centers, d_labels, d_sq);
+    ev::assigned_sq_kernel<double><<<g, 256, 0, stream>>>(static_cast<const double*>(d_x), n, d, d_centers, d_labels, d_sq);
   PQK_LAUNCH_CHECK("assigned_sq_kernel");
   return PQK_OK;
 }

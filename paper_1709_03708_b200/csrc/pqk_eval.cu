@@ -21,6 +21,7 @@ constexpr int kTile = 1024;
 constexpr int kSortThreads = 256;
 constexpr int kRounds = kTile / kSortThreads;
 constexpr int kScanBlock = 1024;  // elements per block in the exclusive scan (256 threads x 4)
+constexpr int kMeansBatch = 4;    // member rows loaded ahead of their (ordered) additions
 
 __global__ void __launch_bounds__(kSortThreads) rs_hist_kernel(const uint32_t* __restrict__ keys, int64_t n, int shift,
                                                               uint32_t* __restrict__ hist, int nb) {
@@ -142,11 +143,12 @@ __global__ void __launch_bounds__(256) cluster_means_kernel(const T* __restrict_
     for (uint32_t j0 = 0; j0 < cnt; j0 += 32) {
       const uint32_t nj = min(32u, cnt - j0);
       const uint32_t my_row = lane < (int)nj ? order[start + j0 + lane] : 0u;
-      for (uint32_t j = 0; j < nj; j += 4) {
-        // rows j..j+3: loads first, then the adds in member order
-        T v[4][4];
+      for (uint32_t j = 0; j < nj; j += kMeansBatch) {
+        // rows j..j+kMeansBatch-1: loads first (memory-level parallelism), then the adds in
+        // member order
+        T v[kMeansBatch][4];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
+        for (int q = 0; q < kMeansBatch; ++q) {
           const uint32_t row = __shfl_sync(0xffffffffu, my_row, (int)min(j + q, nj - 1));
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
@@ -155,7 +157,7 @@ __global__ void __launch_bounds__(256) cluster_means_kernel(const T* __restrict_
           }
         }
 #pragma unroll
-        for (int q = 0; q < 4; ++q)
+        for (int q = 0; q < kMeansBatch; ++q)
           if (j + q < nj) {
 #pragma unroll
             for (int u = 0; u < 4; ++u) acc[u] = __dadd_rn(acc[u], (double)v[q][u]);

@@ -164,6 +164,12 @@ int pqk_train_step_device(const float* d_x, int64_t n, int32_t d, int32_t col0, 
                           int32_t l, int32_t* d_labels, double* d_sums, int32_t* d_counts, double* d_own,
                           void* d_ws, size_t ws_bytes, int64_t* d_stats, void* stream);
 
+/* DistanceTables (pq.py:254-268): tables[m][i][j] = sum_d (c_i - c_j)^2, float64 with the
+ * difference and square rounded separately, summed in increasing d; codewords (m, l,
+ * dsub) float32, tables (m, l, l) float64. */
+int pqk_build_tables_device(const float* d_codewords, int32_t m, int32_t l, int32_t dsub, double* d_tables,
+                            void* stream);
+
 /* Original-space evaluation (baselines.py:26-37 cluster_means, :385-413
  * original_space_error).  means[k][:] = float64 mean of the rows labelled k, summed in
  * increasing row index from 0.0 (np.bincount with weights), 0 for empty clusters;

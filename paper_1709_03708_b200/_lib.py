@@ -68,6 +68,7 @@ SIGNATURES: dict[str, tuple] = {
     "pqk_tc_selftest": (C.c_int, [_p, _p, _p, _i32, _p]),
     "pqk_train_workspace_bytes": (_sz, [_i64, _i32]),
     "pqk_train_step_device": (C.c_int, [_p, _i64, _i32, _i32, _i32, _p, _i32, _p, _p, _p, _p, _p, _sz, _p, _p]),
+    "pqk_build_tables_device": (C.c_int, [_p, _i32, _i32, _i32, _p, _p]),
     "pqk_cluster_means_workspace_bytes": (_sz, [_i64, _i32]),
     "pqk_cluster_means_device": (C.c_int, [_p, _i32, _i64, _i32, _p, _i32, _p, _p, _p, _sz, _p]),
     "pqk_assigned_sq_device": (C.c_int, [_p, _i32, _i64, _i32, _p, _p, _p, _p]),

@@ -152,6 +152,24 @@ __global__ void __launch_bounds__(128) train_own_kernel(const float* __restrict_
   own[i] = np_pairwise(row, dsub);
 }
 
+// DistanceTables (pq.py:254-268): t[m][i][j] = sum_d (c_i - c_j)^2 in float64, the
+// difference and square rounded separately and summed in increasing d (scipy cdist /
+// the numpy loop of build_distance_tables).  One thread per (i, j).
+__global__ void build_tables_kernel(const float* __restrict__ cw, int l, int dsub, double* __restrict__ t) {
+  const int mm = blockIdx.y;
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= l * l) return;
+  const int i = e / l, j = e - i * l;
+  const float* ci = cw + ((size_t)mm * l + i) * dsub;
+  const float* cj = cw + ((size_t)mm * l + j) * dsub;
+  double acc = 0.0;
+  for (int k = 0; k < dsub; ++k) {
+    const double df = __dsub_rn((double)ci[k], (double)cj[k]);
+    acc = __dadd_rn(acc, __dmul_rn(df, df));
+  }
+  t[((size_t)mm * l + i) * l + j] = acc;
+}
+
 __global__ void train_stats_kernel(const unsigned long long* __restrict__ empty, int64_t* __restrict__ stats) {
   stats[PQK_STAT_EMPTY] = (int64_t)*empty;
 }
@@ -208,5 +226,15 @@ extern "C" int pqk_train_step_device(const float* d_x, int64_t n, int32_t d, int
   PQK_LAUNCH_CHECK("train_own_kernel");
   train_stats_kernel<<<1, 1, 0, stream>>>(empty, d_stats);
   PQK_LAUNCH_CHECK("train_stats_kernel");
+  return PQK_OK;
+}
+
+extern "C" int pqk_build_tables_device(const float* d_codewords, int32_t m, int32_t l, int32_t dsub, double* d_tables,
+                                       void* stream) {
+  if (!d_codewords || m < 1 || l < 1 || l > kMaxL || dsub < 1 || !d_tables)
+    return fail(PQK_EINVAL, "pqk_build_tables_device: bad arguments");
+  const dim3 grid((unsigned)((l * l + 255) / 256), (unsigned)m);
+  build_tables_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(d_codewords, l, dsub, d_tables);
+  PQK_LAUNCH_CHECK("build_tables_kernel");
   return PQK_OK;
 }

@@ -521,3 +521,15 @@ def original_space_error_device(x_dev: "torch.Tensor", labels_dev: "torch.Tensor
     means = cluster_means_device(x_dev, labels_dev, k, dev)
     sq = assigned_sq_device(x_dev, means, labels_dev, dev)
     return mean_objectives(sq, int(x_dev.shape[0]), dev)[0]
+
+
+def build_tables_host(codewords: np.ndarray, *, device=None) -> np.ndarray:
+    """(M, L, L) float64 DistanceTables of (M, L, dsub) float32 codewords, computed on the GPU."""
+    cw = np.ascontiguousarray(codewords, dtype=np.float32)
+    m, l, dsub = cw.shape
+    dev = device_of(device)
+    with torch.cuda.device(dev):
+        cw_dev = torch.from_numpy(np.array(cw)).to(dev)
+        t = torch.empty((m, l, l), dtype=torch.float64, device=dev)
+        call("pqk_build_tables_device", _ptr(cw_dev), m, l, dsub, _ptr(t), _stream(dev))
+        return t.cpu().numpy()

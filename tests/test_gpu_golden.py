@@ -111,3 +111,14 @@ def test_reference_plugin_boundary(pqk):
         t = tables(g, f"c{i}_")
         got = pqk.b200_assign_strategy(g[f"c{i}_codes"].astype(np.int32), g[f"c{i}_centers"], t, 8)
         np.testing.assert_array_equal(got, g[f"c{i}_labels"])
+
+
+def test_build_distance_tables_golden(pqk):
+    """pq.build_distance_tables on the GPU vs the reference's tables (SHA-256 of all bytes)."""
+    import hashlib
+
+    g = load("tables_mean")
+    for i in range(4):
+        cw = g[f"b{i}_codebook"] if f"b{i}_codebook" in g else g[f"b{i}_codewords"]
+        t = pqk.build_distance_tables(pqk.PQCodebook(cw)).tables
+        assert hashlib.sha256(t.tobytes()).hexdigest() == str(g[f"b{i}_tables_sha256"]), i

@@ -66,13 +66,15 @@ static void plan_levels(int64_t n, std::vector<std::vector<PlanNode>>& levels, i
 struct HostCtx {
   bool init = false;
   cudaStream_t stream = nullptr;
+  cudaStream_t copy_stream = nullptr;  // D2H of results that are final early (labels)
+  cudaEvent_t assigned = nullptr;
   std::mutex mu;
   struct Buf {
     void* p = nullptr;
     size_t bytes = 0;
   };
   Buf raw, codes, centers_raw, centers, t64, t32, labels, sd, ws, stats, hist, counts, newc, rws, vec, cw, obj, objws,
-      plan;
+      plan, scale;
   // cached numpy-summation plan for the last n (uploaded into `plan`)
   int64_t plan_n = -1, plan_nleaves = 0, plan_nnodes = 0;
   size_t plan_o_len = 0, plan_o_na = 0, plan_o_nb = 0;
@@ -98,6 +100,8 @@ static int ctx_begin(int device, HostCtx*& ctx) {
   ctx = &g_ctx[device];
   if (!ctx->init) {
     PQK_CUDA_TRY(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+    PQK_CUDA_TRY(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+    PQK_CUDA_TRY(cudaEventCreateWithFlags(&ctx->assigned, cudaEventDisableTiming));
     ctx->init = true;
   }
   return PQK_OK;
@@ -109,15 +113,78 @@ static int ctx_begin(int device, HostCtx*& ctx) {
     if (_rc != PQK_OK) return _rc; \
   } while (0)
 
-// Upload tables, build the scaled fp32 copy.
+// Table statistics on the device (the host-buffer entry points upload the tables anyway):
+// out[0] = bits of the largest entry, out[1] = bits of the smallest nonzero entry (both
+// nonnegative doubles, so their bit patterns order as uint64), out[2] = entries that are
+// NaN, negative or infinite.
+__global__ void table_stats_kernel(const double* __restrict__ t, int64_t count, unsigned long long* __restrict__ out) {
+  unsigned long long mx = 0ull, mn = 0x7ff0000000000000ull, bad = 0ull;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x) {
+    const double v = t[i];
+    const bool ok = v >= 0.0 && v <= 1.7976931348623157e308;
+    bad += !ok;
+    const unsigned long long b = (unsigned long long)__double_as_longlong(v);
+    if (ok) {
+      mx = b > mx ? b : mx;
+      if (v > 0.0) mn = b < mn ? b : mn;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long omx = __shfl_xor_sync(0xffffffffu, mx, o), omn = __shfl_xor_sync(0xffffffffu, mn, o);
+    mx = omx > mx ? omx : mx;
+    mn = omn < mn ? omn : mn;
+    bad += __shfl_xor_sync(0xffffffffu, bad, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMax(&out[0], mx);
+    atomicMin(&out[1], mn);
+    if (bad) atomicAdd(&out[2], bad);
+  }
+}
+
+// The exponent / fp64-only decision of pqk_table_scale from the table's extremes.
+static void table_scale_decide(double mx, double mn, int32_t* e_out, int32_t* f64_out) {
+  *e_out = 0;
+  *f64_out = 0;
+  if (mx == 0.0) return;
+  // keep nonzero entries inside [2^-100, 2^100] after scaling: far from fp32
+  // subnormals (relative error bound) and from overflow of sums of up to 2^20 terms.
+  int e = 0;
+  if (mx > ldexp(1.0, 100) || mn < ldexp(1.0, -100)) {
+    int ex = 0;
+    std::frexp(mx, &ex);  // mx in [2^(ex-1), 2^ex)
+    e = 100 - ex;
+  }
+  if (ldexp(mx, e) > ldexp(1.0, 100) || ldexp(mn, e) < ldexp(1.0, -100)) {
+    *f64_out = 1;
+    return;
+  }
+  *e_out = e;
+}
+
+// Upload tables, build the scaled fp32 copy (scale decided on the device).
 static int upload_tables(HostCtx* c, const double* tables, int m, int l, int& fp64_only) {
   const int mp = padded_m(m);
   const size_t cnt = (size_t)m * l * l;
   PQK_TRY(ensure(c->t64, cnt * sizeof(double)));
   PQK_TRY(ensure(c->t32, (size_t)mp * l * l * sizeof(float)));
+  PQK_TRY(ensure(c->scale, 4 * sizeof(unsigned long long)));
   PQK_CUDA_TRY(cudaMemcpyAsync(c->t64.p, tables, cnt * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  const unsigned long long init[3] = {0ull, 0x7ff0000000000000ull, 0ull};
+  PQK_CUDA_TRY(cudaMemcpyAsync(c->scale.p, init, sizeof(init), cudaMemcpyHostToDevice, c->stream));
+  const DevInfo& di = dev_info();
+  table_stats_kernel<<<std::max(1, std::min((int)((cnt + 255) / 256), 4 * di.sms)), 256, 0, c->stream>>>(
+      (const double*)c->t64.p, (int64_t)cnt, (unsigned long long*)c->scale.p);
+  PQK_LAUNCH_CHECK("table_stats_kernel");
+  unsigned long long st[3];
+  PQK_CUDA_TRY(cudaMemcpyAsync(st, c->scale.p, sizeof(st), cudaMemcpyDeviceToHost, c->stream));
+  PQK_CUDA_TRY(cudaStreamSynchronize(c->stream));
+  if (st[2]) return fail(PQK_EINVAL, "table entries must be finite and non-negative");
+  double mx, mn;
+  std::memcpy(&mx, &st[0], sizeof(double));
+  std::memcpy(&mn, &st[1], sizeof(double));  // +inf when there is no nonzero entry
   int32_t e = 0, f64 = 0;
-  PQK_TRY(pqk_table_scale(tables, (int64_t)cnt, &e, &f64));
+  table_scale_decide(mx, mn, &e, &f64);
   fp64_only = f64;
   return pqk_tables_to_f32((const double*)c->t64.p, m, l, e, (float*)c->t32.p, c->stream);
 }
@@ -183,22 +250,7 @@ extern "C" int pqk_table_scale(const double* t, int64_t count, int32_t* exp2_out
     mn = (v > 0.0 && v < mn) ? v : mn;
   }
   if (bad) return fail(PQK_EINVAL, "table entries must be finite and non-negative");
-  *exp2_out = 0;
-  *fp64_only_out = 0;
-  if (mx == 0.0) return PQK_OK;
-  // keep nonzero entries inside [2^-100, 2^100] after scaling: far from fp32
-  // subnormals (relative error bound) and from overflow of sums of up to 2^20 terms.
-  int e = 0;
-  if (mx > ldexp(1.0, 100) || mn < ldexp(1.0, -100)) {
-    int ex = 0;
-    std::frexp(mx, &ex);  // mx in [2^(ex-1), 2^ex)
-    e = 100 - ex;
-  }
-  if (ldexp(mx, e) > ldexp(1.0, 100) || ldexp(mn, e) < ldexp(1.0, -100)) {
-    *fp64_only_out = 1;
-    return PQK_OK;
-  }
-  *exp2_out = e;
+  table_scale_decide(mx, mn, exp2_out, fp64_only_out);
   return PQK_OK;
 }
 
@@ -359,6 +411,11 @@ extern "C" int pqk_lloyd_step_host(const uint8_t* codes, int64_t n, int32_t m, c
   PQK_TRY(pqk_assign_device((const uint8_t*)c->codes.p, n, m, l, (const uint8_t*)c->centers.p, k,
                             (const double*)c->t64.p, (const float*)c->t32.p, fp64_only, c->ws.p, wsb,
                             (uint32_t*)c->labels.p, (double*)c->sd.p, dstats, c->stream));
+  // labels are final once assigned: copy them out on the side while the update runs
+  PQK_CUDA_TRY(cudaEventRecord(c->assigned, c->stream));
+  PQK_CUDA_TRY(cudaStreamWaitEvent(c->copy_stream, c->assigned, 0));
+  PQK_CUDA_TRY(cudaMemcpyAsync(labels, c->labels.p, (size_t)n * sizeof(uint32_t), cudaMemcpyDeviceToHost,
+                               c->copy_stream));
   PQK_TRY(pqk_objective_device((const double*)c->sd.p, n, nleaves, ndepth, (const int64_t*)pb,
                                (const int32_t*)(pb + o_len), depth_start_h, (const int32_t*)(pb + o_na),
                                (const int32_t*)(pb + o_nb), c->objws.p, owsb, (double*)c->obj.p, c->stream));
@@ -374,7 +431,6 @@ extern "C" int pqk_lloyd_step_host(const uint8_t* codes, int64_t n, int32_t m, c
     PQK_TRY(pqk_repair_device((const double*)c->sd.p, (const uint8_t*)c->codes.p, n, m, (const int32_t*)c->counts.p,
                               k, (uint8_t*)c->newc.p, c->rws.p, rwsb, dstats, c->stream));
   }
-  PQK_CUDA_TRY(cudaMemcpyAsync(labels, c->labels.p, (size_t)n * sizeof(uint32_t), cudaMemcpyDeviceToHost, c->stream));
   PQK_CUDA_TRY(cudaMemcpyAsync(obj2, c->obj.p, 2 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
   PQK_CUDA_TRY(cudaMemcpyAsync(stats, dstats, PQK_STATS_LEN * sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
   if (mp == m) {
@@ -386,6 +442,7 @@ extern "C" int pqk_lloyd_step_host(const uint8_t* codes, int64_t n, int32_t m, c
     PQK_CUDA_TRY(cudaStreamSynchronize(c->stream));
     for (int64_t i = 0; i < k; ++i) std::memcpy(new_centers + i * m, tmp.data() + i * mp, m);
   }
+  PQK_CUDA_TRY(cudaStreamSynchronize(c->copy_stream));
   return PQK_OK;
 }
 
@@ -397,7 +454,7 @@ extern "C" int pqk_host_release(int32_t device) {
   PQK_CUDA_TRY(cudaSetDevice(device));
   HostCtx::Buf* bufs[] = {&c.raw, &c.codes, &c.centers_raw, &c.centers, &c.t64, &c.t32, &c.labels,
                           &c.sd,  &c.ws,    &c.stats,       &c.hist,    &c.counts, &c.newc, &c.rws,
-                          &c.vec, &c.cw,    &c.obj,         &c.objws,   &c.plan};
+                          &c.vec, &c.cw,    &c.obj,         &c.objws,   &c.plan, &c.scale};
   for (auto* b : bufs) {
     if (b->p) cudaFree(b->p);
     b->p = nullptr;

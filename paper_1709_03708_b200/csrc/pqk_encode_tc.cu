@@ -101,6 +101,7 @@ extern "C" int pqk_tc_selftest(const void* d_a, const void* d_b, float* d_c, int
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <map>
 #include <mutex>
 
 namespace pqk {
@@ -1317,12 +1318,21 @@ __global__ void encode_stats_kernel(const unsigned int* __restrict__ counters, u
 // ---------------------------------------------------------------------------
 // host side
 namespace {
+// Encoder workspace (prepared codebook operands, flag buckets, counters), one per
+// (device, stream): launches on one stream are ordered, so a buffer is reused only after
+// the previous encode on that stream has finished with it.
 struct EncWS {
-  std::mutex mu;
   void* p = nullptr;
   size_t bytes = 0;
 };
-EncWS g_encws[64];
+std::mutex g_encws_mu;
+std::map<std::pair<int, cudaStream_t>, EncWS> g_encws;
+
+EncWS& enc_workspace(cudaStream_t stream) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return g_encws[{dev, stream}];
+}
 
 PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -1342,10 +1352,8 @@ int launch_encode_tc(const float* d_x, int64_t n, int d, const float* d_cw, int 
   using namespace enc;
   using G = Geo<KP>;
   const DevInfo& di = dev_info();
-  int dev = 0;
-  cudaGetDevice(&dev);
-  EncWS& ws = g_encws[dev & 63];
-  std::lock_guard<std::mutex> lock(ws.mu);
+  std::lock_guard<std::mutex> lock(g_encws_mu);
+  EncWS& ws = enc_workspace(stream);
   const size_t b_bytes = (size_t)m * G::B_BYTES;
   const uint32_t cap = (uint32_t)std::min<int64_t>(n, n / 4 + 4096);  // flagged rows per subspace
   const size_t need = align_up(b_bytes, 256) + align_up((size_t)m * CST_LEN * 4, 256) +
@@ -1415,10 +1423,8 @@ int launch_encode_tck(const float* d_x, int64_t n, int d, const float* d_cw, int
   using namespace enc;
   using G = GeoK;
   const DevInfo& di = dev_info();
-  int dev = 0;
-  cudaGetDevice(&dev);
-  EncWS& ws = g_encws[dev & 63];
-  std::lock_guard<std::mutex> lock(ws.mu);
+  std::lock_guard<std::mutex> lock(g_encws_mu);
+  EncWS& ws = enc_workspace(stream);
   const size_t b_bytes = (size_t)m * G::bprep_bytes(ks);
   const uint32_t cap = (uint32_t)std::min<int64_t>(n, n / 4 + 4096);  // flagged rows per subspace
   const size_t need = align_up(b_bytes, 256) + align_up((size_t)m * CST_LEN * 4, 256) +

@@ -113,9 +113,11 @@ int pqk_paired_distance_device(const uint8_t* d_a, const uint8_t* d_b, const uin
                                int32_t m, int32_t l, const double* d_t64, double* d_out, void* stream);
 
 /* Histogram of member subindices (clustering.py:344-347) and counts (clustering.py:458):
- * hist[k][m][s] (int32, zeroed here), counts[k] (int32, zeroed here). */
+ * hist[k][m][s] (uint32, zeroed here), counts[k] (uint32, zeroed here).  Shards of
+ * up to 2^32 - 1 codes (the scan runs in 2^30-code windows); over all shards the
+ * total stays below 2^32 so the reduced counts fit uint32. */
 int pqk_histogram_device(const uint8_t* d_codes, int64_t n, int32_t m, int32_t l,
-                         const uint32_t* d_labels, int64_t k, int32_t* d_hist, int32_t* d_counts, void* stream);
+                         const uint32_t* d_labels, int64_t k, uint32_t* d_hist, uint32_t* d_counts, void* stream);
 
 /* Sparse-voting update (clustering.py:349-356): for filled k,
  * new_centers[k][m] = argmin_j sum_s hist[k][m][s] * T[m][s][j] (lowest j on ties,
@@ -123,15 +125,16 @@ int pqk_histogram_device(const uint8_t* d_codes, int64_t n, int32_t m, int32_t l
  * fp64, double-double on near ties).  Empty clusters get code 0 (repaired by
  * pqk_repair_device).  Writes NNZ_TOTAL, FILLED, EMPTY, VOTE_EXACT stats.  Requires
  * hist/counts already reduced over all shards. */
-int pqk_vote_device(const int32_t* d_hist, const int32_t* d_counts, int64_t k, int32_t m, int32_t l,
+int pqk_vote_device(const uint32_t* d_hist, const uint32_t* d_counts, int64_t k, int32_t m, int32_t l,
                     const double* d_t64, const float* d_t32, uint8_t* d_new_centers, int64_t* d_stats,
                     void* stream);
 
 /* Empty-cluster repair (clustering.py:460-466): the E empty clusters (ascending k)
- * take the codes of the E codes with largest sd_sq (lowest index among ties). */
+ * take the codes of the E codes with largest sd_sq (lowest index among ties).  Code
+ * indices are 32-bit in the selection keys: n (and base_index + n) <= 2^32. */
 size_t pqk_repair_workspace_bytes(int64_t n, int64_t k);
 int pqk_repair_device(const double* d_sd_sq, const uint8_t* d_codes, int64_t n, int32_t m,
-                      const int32_t* d_counts, int64_t k, uint8_t* d_new_centers,
+                      const uint32_t* d_counts, int64_t k, uint8_t* d_new_centers,
                       void* d_ws, size_t ws_bytes, int64_t* d_stats, void* stream);
 /* Local top-E candidates for the multi-GPU repair: writes E (key,index) pairs
  * sorted by (sd_sq desc, index asc); index offset by base_index. */

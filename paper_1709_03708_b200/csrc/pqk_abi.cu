@@ -420,15 +420,15 @@ extern "C" int pqk_lloyd_step_host(const uint8_t* codes, int64_t n, int32_t m, c
                                (const int32_t*)(pb + o_len), depth_start_h, (const int32_t*)(pb + o_na),
                                (const int32_t*)(pb + o_nb), c->objws.p, owsb, (double*)c->obj.p, c->stream));
   PQK_TRY(pqk_histogram_device((const uint8_t*)c->codes.p, n, m, l, (const uint32_t*)c->labels.p, k,
-                               (int32_t*)c->hist.p, (int32_t*)c->counts.p, c->stream));
-  PQK_TRY(pqk_vote_device((const int32_t*)c->hist.p, (const int32_t*)c->counts.p, k, m, l, (const double*)c->t64.p,
+                               (uint32_t*)c->hist.p, (uint32_t*)c->counts.p, c->stream));
+  PQK_TRY(pqk_vote_device((const uint32_t*)c->hist.p, (const uint32_t*)c->counts.p, k, m, l, (const double*)c->t64.p,
                           fp64_only ? nullptr : (const float*)c->t32.p,
                           (uint8_t*)c->newc.p, dstats, c->stream));
   int64_t hstats[PQK_STATS_LEN];
   PQK_CUDA_TRY(cudaMemcpyAsync(hstats, dstats, sizeof(hstats), cudaMemcpyDeviceToHost, c->stream));
   PQK_CUDA_TRY(cudaStreamSynchronize(c->stream));
   if (hstats[PQK_STAT_EMPTY] > 0) {
-    PQK_TRY(pqk_repair_device((const double*)c->sd.p, (const uint8_t*)c->codes.p, n, m, (const int32_t*)c->counts.p,
+    PQK_TRY(pqk_repair_device((const double*)c->sd.p, (const uint8_t*)c->codes.p, n, m, (const uint32_t*)c->counts.p,
                               k, (uint8_t*)c->newc.p, c->rws.p, rwsb, dstats, c->stream));
   }
   PQK_CUDA_TRY(cudaMemcpyAsync(obj2, c->obj.p, 2 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));

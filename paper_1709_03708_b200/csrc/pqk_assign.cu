@@ -512,9 +512,10 @@ __global__ void __launch_bounds__(256) rescan_cta_kernel(
   }
 }
 
-__global__ void assign_stats_kernel(const int32_t* __restrict__ counters, int64_t* __restrict__ stats) {
+// first window sets the statistics, later windows add their flagged codes
+__global__ void assign_stats_kernel(const int32_t* __restrict__ counters, int64_t* __restrict__ stats, int first) {
   stats[PQK_STAT_UNIQUE_CENTERS] = counters[0];
-  stats[PQK_STAT_FLAGGED] = counters[1];
+  stats[PQK_STAT_FLAGGED] = (first ? 0 : stats[PQK_STAT_FLAGGED]) + counters[1];
   stats[PQK_STAT_NCHUNKS] = counters[2];
 }
 
@@ -559,6 +560,10 @@ struct AssignWS {
   size_t total;
 };
 
+// Rows per scan window: the scan and the flag list index rows of a window in 32 bits;
+// larger shards are scanned window by window (the table chunks are built once).
+constexpr int64_t kScanWindow = (int64_t)1 << 30;
+
 static AssignWS assign_ws_layout(void* base, int64_t n, int64_t k, int mp, int l) {
   AssignWS w{};
   uint32_t hs = 64;
@@ -581,7 +586,7 @@ static AssignWS assign_ws_layout(void* base, int64_t n, int64_t k, int mp, int l
   const size_t o_p2i = take(k * sizeof(int32_t), 256);
   const size_t o_uc = take((size_t)k * mp, 256);
   const size_t o_q = take((size_t)nchunks_max * l * mp * kc * sizeof(float), 1024);
-  const size_t o_fl = take((size_t)std::max<int64_t>(n, 1) * sizeof(int32_t), 256);
+  const size_t o_fl = take((size_t)std::max<int64_t>(std::min(n, kScanWindow), 1) * sizeof(int32_t), 256);
   w.total = align_up(off, 256);
   char* b = static_cast<char*>(base);
   if (b) {
@@ -686,8 +691,7 @@ extern "C" int pqk_assign_device(const uint8_t* d_codes, int64_t n, int32_t m, i
   const int mp = padded_m(m);
   if (mp == 0 || l < 2 || l > kMaxL) return fail(PQK_EINVAL, "pqk_assign_device: M must be >= 1 and L in [2, 256]");
   if (k < 1) return fail(PQK_EINVAL, "centers must be non-empty");
-  if (n < 0 || n >= (int64_t)1 << 31 || k >= (int64_t)1 << 30)
-    return fail(PQK_EUNSUPPORTED, "pqk_assign_device: n must be < 2^31 and k < 2^30 per device");
+  if (n < 0 || k >= (int64_t)1 << 30) return fail(PQK_EUNSUPPORTED, "pqk_assign_device: k must be < 2^30");
   if (n == 0) return PQK_OK;
   if (!d_codes || !d_centers || !d_t64 || !d_labels || !d_sd_sq || !d_ws)
     return fail(PQK_EINVAL, "pqk_assign_device: null pointer");
@@ -713,7 +717,6 @@ extern "C" int pqk_assign_device(const uint8_t* d_codes, int64_t n, int32_t m, i
     const int kc = kc_for(mp);
     const int64_t units = ((k + kc - 1) / kc) * l * mp * (kc / 4);
     const int qgrid = (int)std::min<int64_t>((units + 255) / 256, (int64_t)di.sms * 16);
-    int rc = PQK_OK;
     switch (mp) {
       case 4: qbuild_kernel<4, 8><<<qgrid, 256, 0, stream>>>(d_t32, l, w.ucodes, w.counters, (float4*)w.q); break;
       case 8: qbuild_kernel<8, 4><<<qgrid, 256, 0, stream>>>(d_t32, l, w.ucodes, w.counters, (float4*)w.q); break;
@@ -721,57 +724,68 @@ extern "C" int pqk_assign_device(const uint8_t* d_codes, int64_t n, int32_t m, i
       case 32: qbuild_kernel<32, 4><<<qgrid, 256, 0, stream>>>(d_t32, l, w.ucodes, w.counters, (float4*)w.q); break;
     }
     PQK_LAUNCH_CHECK("qbuild_kernel");
-    // 3. scan
-    ScanParams sp{};
-    sp.codes = d_codes;
-    sp.n = n;
-    sp.q = w.q;
-    sp.l = l;
-    sp.m = m;
-    sp.counters = w.counters;
-    sp.pos2idx = w.pos2idx;
-    sp.ucodes = w.ucodes;
-    sp.t64 = d_t64;
-    sp.cert_factor = 1.0 + 4.0 * (2.0 * m) * ldexp(1.0, -24);
-    sp.labels = d_labels;
-    sp.sd_sq = d_sd_sq;
-    sp.flags = w.flags;
-    sp.flag_count = w.counters + 1;
-    switch (mp) {
-      case 4: rc = launch_scan<4, 8, 11, 4, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14>(sp, l, stream); break;
-      case 8: rc = launch_scan<8, 4, 11, 4, 1, 2, 3, 4, 5, 6, 7, 8>(sp, l, stream); break;
-      case 16: rc = launch_scan<16, 4, 11, 3, 1, 2, 3, 4>(sp, l, stream); break;
-      case 32: rc = launch_scan<32, 4, 11, 1, 1, 2>(sp, l, stream); break;
-    }
-    if (rc != PQK_OK) return rc;
   }
-  // 4. exact rescan of uncertified codes (or every code in fp64-only mode)
-  {
-    const size_t rows_bytes = (size_t)m * l * sizeof(double);
-    if (rows_bytes <= 96 * 1024) {
-      static bool attr_set[64] = {};
-      int dev = 0;
-      cudaGetDevice(&dev);
-      if (!attr_set[dev & 63]) {
-        PQK_CUDA_TRY(cudaFuncSetAttribute(rescan_cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
-        attr_set[dev & 63] = true;
+  const size_t rows_bytes = (size_t)m * l * sizeof(double);
+  const bool cta_rescan = rows_bytes <= 96 * 1024;
+  if (cta_rescan) {
+    static bool attr_set[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!attr_set[dev & 63]) {
+      PQK_CUDA_TRY(cudaFuncSetAttribute(rescan_cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
+      attr_set[dev & 63] = true;
+    }
+  }
+  for (int64_t w0 = 0; w0 < n; w0 += kScanWindow) {
+    const int64_t wn = std::min(kScanWindow, n - w0);
+    const uint8_t* codes = d_codes + w0 * mp;
+    uint32_t* labels = d_labels + w0;
+    double* sd_sq = d_sd_sq + w0;
+    if (w0 > 0) PQK_CUDA_TRY(cudaMemsetAsync(w.counters + 1, 0, sizeof(int32_t), stream));
+    if (fast) {
+      // 3. scan
+      ScanParams sp{};
+      sp.codes = codes;
+      sp.n = wn;
+      sp.q = w.q;
+      sp.l = l;
+      sp.m = m;
+      sp.counters = w.counters;
+      sp.pos2idx = w.pos2idx;
+      sp.ucodes = w.ucodes;
+      sp.t64 = d_t64;
+      sp.cert_factor = 1.0 + 4.0 * (2.0 * m) * ldexp(1.0, -24);
+      sp.labels = labels;
+      sp.sd_sq = sd_sq;
+      sp.flags = w.flags;
+      sp.flag_count = w.counters + 1;
+      int rc = PQK_OK;
+      switch (mp) {
+        case 4: rc = launch_scan<4, 8, 11, 4, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14>(sp, l, stream); break;
+        case 8: rc = launch_scan<8, 4, 11, 4, 1, 2, 3, 4, 5, 6, 7, 8>(sp, l, stream); break;
+        case 16: rc = launch_scan<16, 4, 11, 3, 1, 2, 3, 4>(sp, l, stream); break;
+        case 32: rc = launch_scan<32, 4, 11, 1, 1, 2>(sp, l, stream); break;
       }
-      const int grid = (int)std::min<int64_t>(fast ? (int64_t)di.sms * 2 : n, (int64_t)di.sms * 8);
+      if (rc != PQK_OK) return rc;
+    }
+    // 4. exact rescan of uncertified codes (or every code in fp64-only mode)
+    if (cta_rescan) {
+      const int grid = (int)std::min<int64_t>(fast ? (int64_t)di.sms * 2 : wn, (int64_t)di.sms * 8);
       rescan_cta_kernel<<<std::max(grid, 1), 256, rows_bytes, stream>>>(
-          d_codes, n, mp, m, l, w.ucodes, w.counters, w.flags, w.counters + 1, w.pos2idx, d_t64, d_labels, d_sd_sq,
+          codes, wn, mp, m, l, w.ucodes, w.counters, w.flags, w.counters + 1, w.pos2idx, d_t64, labels, sd_sq,
           fast ? 0 : 1);
       PQK_LAUNCH_CHECK("rescan_cta_kernel");
     } else {
-      const int64_t warps = fast ? (int64_t)di.sms * 32 : std::min<int64_t>(n, (int64_t)di.sms * 64);
+      const int64_t warps = fast ? (int64_t)di.sms * 32 : std::min<int64_t>(wn, (int64_t)di.sms * 64);
       const int grid = (int)std::max<int64_t>(1, (warps * 32 + 255) / 256);
-      rescan_kernel<<<grid, 256, 0, stream>>>(d_codes, n, mp, m, l, w.ucodes, w.counters, w.flags, w.counters + 1,
-                                              w.pos2idx, d_t64, d_labels, d_sd_sq, fast ? 0 : 1);
+      rescan_kernel<<<grid, 256, 0, stream>>>(codes, wn, mp, m, l, w.ucodes, w.counters, w.flags, w.counters + 1,
+                                              w.pos2idx, d_t64, labels, sd_sq, fast ? 0 : 1);
       PQK_LAUNCH_CHECK("rescan_kernel");
     }
-  }
-  if (d_stats) {
-    assign_stats_kernel<<<1, 1, 0, stream>>>(w.counters, d_stats);
-    PQK_LAUNCH_CHECK("assign_stats_kernel");
+    if (d_stats) {
+      assign_stats_kernel<<<1, 1, 0, stream>>>(w.counters, d_stats, w0 == 0);
+      PQK_LAUNCH_CHECK("assign_stats_kernel");
+    }
   }
   return PQK_OK;
 }

@@ -27,14 +27,14 @@ namespace pqk {
 // ---------------------------------------------------------------------------
 // histogram
 __global__ void histogram_kernel(const uint8_t* __restrict__ codes, int64_t n, int mp, int m, int l,
-                                 const uint32_t* __restrict__ labels, int32_t* __restrict__ hist,
-                                 int32_t* __restrict__ counts) {
+                                 const uint32_t* __restrict__ labels, uint32_t* __restrict__ hist,
+                                 uint32_t* __restrict__ counts) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t k = labels[i];
     const uint8_t* x = codes + i * mp;
-    atomicAdd(&counts[k], 1);
-    int32_t* hk = hist + k * m * l;
-    for (int mm = 0; mm < m; ++mm) atomicAdd(&hk[mm * l + x[mm]], 1);
+    atomicAdd(&counts[k], 1u);
+    uint32_t* hk = hist + k * m * l;
+    for (int mm = 0; mm < m; ++mm) atomicAdd(&hk[mm * l + x[mm]], 1u);
   }
 }
 
@@ -102,14 +102,14 @@ __device__ __forceinline__ void warp_best(Best& b) {
   for (int o = 16; o > 0; o >>= 1) b = merge_best(b, shfl_best(b, o));
 }
 
-__global__ void __launch_bounds__(32 * kVoteWarps) vote_kernel(const int32_t* __restrict__ hist,
-                                                               const int32_t* __restrict__ counts, int64_t k, int m,
+__global__ void __launch_bounds__(32 * kVoteWarps) vote_kernel(const uint32_t* __restrict__ hist,
+                                                               const uint32_t* __restrict__ counts, int64_t k, int m,
                                                                int l, int mp, const double* __restrict__ t64,
                                                                const float* __restrict__ t32,
                                                                uint8_t* __restrict__ newc,
                                                                unsigned long long* __restrict__ acc) {
   __shared__ int s_s[kVoteWarps][kMaxL];
-  __shared__ int s_h[kVoteWarps][kMaxL];
+  __shared__ uint32_t s_h[kVoteWarps][kMaxL];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t gw = (int64_t)blockIdx.x * kVoteWarps + warp;
   if (gw >= k * m) return;
@@ -117,12 +117,12 @@ __global__ void __launch_bounds__(32 * kVoteWarps) vote_kernel(const int32_t* __
   const int64_t kk = gw - (int64_t)mm * k;
   if (counts[kk] == 0) return;  // empty: left 0, repaired later
   int* ss = s_s[warp];
-  int* sh = s_h[warp];
-  const int32_t* hrow = hist + (kk * m + mm) * l;
+  uint32_t* sh = s_h[warp];
+  const uint32_t* hrow = hist + (kk * m + mm) * l;
   int nnz = 0;
   for (int base = 0; base < l; base += 32) {
     const int s = base + lane;
-    const int h = (s < l) ? hrow[s] : 0;
+    const uint32_t h = (s < l) ? hrow[s] : 0u;
     const unsigned bal = __ballot_sync(0xffffffffu, h != 0);
     if (h) {
       const int pos = nnz + __popc(bal & ((1u << lane) - 1u));
@@ -140,7 +140,7 @@ __global__ void __launch_bounds__(32 * kVoteWarps) vote_kernel(const int32_t* __
 #pragma unroll
     for (int i = 0; i < 8; ++i) v[i] = 0.0f;
     for (int j = 0; j < nnz; ++j) {
-      const float h = (float)sh[j];
+      const float h = __uint2float_rn(sh[j]);
       const float* row = tf + (size_t)ss[j] * l;
 #pragma unroll
       for (int i = 0; i < 8; ++i)
@@ -217,14 +217,14 @@ __global__ void __launch_bounds__(32 * kVoteWarps) vote_kernel(const int32_t* __
 
 // ---------------------------------------------------------------------------
 // order-preserving compaction of a flag array (two kernels; blockDim == 1024)
-__global__ void empty_count_kernel(const int32_t* __restrict__ counts, int64_t k, int32_t* __restrict__ blockcnt) {
+__global__ void empty_count_kernel(const uint32_t* __restrict__ counts, int64_t k, int32_t* __restrict__ blockcnt) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int f = (i < k) && counts[i] == 0;
   const int c = __syncthreads_count(f);
   if (threadIdx.x == 0) blockcnt[blockIdx.x] = c;
 }
 
-__global__ void empty_compact_kernel(const int32_t* __restrict__ counts, int64_t k,
+__global__ void empty_compact_kernel(const uint32_t* __restrict__ counts, int64_t k,
                                      const int32_t* __restrict__ blockcnt, int32_t* __restrict__ empty_list) {
   __shared__ int s_off;
   __shared__ int s_warp[32];
@@ -254,7 +254,7 @@ __global__ void empty_compact_kernel(const int32_t* __restrict__ counts, int64_t
 }
 
 // number of empty clusters (acc[2]) and the public vote stats
-__global__ void empties_kernel(const int32_t* __restrict__ counts, int64_t k, unsigned long long* __restrict__ acc) {
+__global__ void empties_kernel(const uint32_t* __restrict__ counts, int64_t k, unsigned long long* __restrict__ acc) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int c = __syncthreads_count((i < k) && counts[i] == 0);
   if (threadIdx.x == 0 && c) atomicAdd(&acc[2], (unsigned long long)c);
@@ -612,11 +612,12 @@ static int run_select(const double* d_sd, int64_t n, int64_t base, const int64_t
 using namespace pqk;
 
 extern "C" int pqk_histogram_device(const uint8_t* d_codes, int64_t n, int32_t m, int32_t l,
-                                    const uint32_t* d_labels, int64_t k, int32_t* d_hist, int32_t* d_counts,
+                                    const uint32_t* d_labels, int64_t k, uint32_t* d_hist, uint32_t* d_counts,
                                     void* stream_) {
   cudaStream_t stream = (cudaStream_t)stream_;
   const int mp = padded_m(m);
   if (mp == 0 || l < 1 || l > kMaxL || k < 1 || n < 0) return fail(PQK_EINVAL, "pqk_histogram_device: bad arguments");
+  if (n > (int64_t)UINT32_MAX) return fail(PQK_EUNSUPPORTED, "pqk_histogram_device: n must be < 2^32 (uint32 counts)");
   PQK_CUDA_TRY(cudaMemsetAsync(d_hist, 0, (size_t)k * m * l * sizeof(int32_t), stream));
   PQK_CUDA_TRY(cudaMemsetAsync(d_counts, 0, (size_t)k * sizeof(int32_t), stream));
   if (n == 0) return PQK_OK;
@@ -628,7 +629,7 @@ extern "C" int pqk_histogram_device(const uint8_t* d_codes, int64_t n, int32_t m
 }
 
 // d_stats has PQK_STATS_LEN slots: 0..15 public, 16..19 scratch accumulators of the vote.
-extern "C" int pqk_vote_device(const int32_t* d_hist, const int32_t* d_counts, int64_t k, int32_t m, int32_t l,
+extern "C" int pqk_vote_device(const uint32_t* d_hist, const uint32_t* d_counts, int64_t k, int32_t m, int32_t l,
                                const double* d_t64, const float* d_t32, uint8_t* d_new_centers, int64_t* d_stats,
                                void* stream_) {
   cudaStream_t stream = (cudaStream_t)stream_;
@@ -654,11 +655,12 @@ extern "C" size_t pqk_repair_workspace_bytes(int64_t n, int64_t k) {
 }
 
 extern "C" int pqk_repair_device(const double* d_sd_sq, const uint8_t* d_codes, int64_t n, int32_t m,
-                                 const int32_t* d_counts, int64_t k, uint8_t* d_new_centers, void* d_ws,
+                                 const uint32_t* d_counts, int64_t k, uint8_t* d_new_centers, void* d_ws,
                                  size_t ws_bytes, int64_t* d_stats, void* stream_) {
   cudaStream_t stream = (cudaStream_t)stream_;
   const int mp = padded_m(m);
   if (mp == 0 || k < 1 || n < 1 || !d_ws || !d_stats) return fail(PQK_EINVAL, "pqk_repair_device: bad arguments");
+  if (n > ((int64_t)1 << 32)) return fail(PQK_EUNSUPPORTED, "pqk_repair_device: n must be <= 2^32 (32-bit key index)");
   RepairWS w = repair_layout(d_ws, n, k);
   if (ws_bytes < w.total) return fail(PQK_EINVAL, "pqk_repair_device: workspace too small");
   const int kb = (int)((k + 1023) / 1024);
@@ -679,7 +681,9 @@ extern "C" int pqk_repair_candidates_device(const double* d_sd_sq, int64_t n, in
                                             void* d_ws, size_t ws_bytes, uint64_t* d_out_keys, int64_t* d_out_index,
                                             void* stream_) {
   cudaStream_t stream = (cudaStream_t)stream_;
-  if (n < 1 || e < 0 || !d_ws) return fail(PQK_EINVAL, "pqk_repair_candidates_device: bad arguments");
+  if (n < 1 || e < 0 || base_index < 0 || !d_ws) return fail(PQK_EINVAL, "pqk_repair_candidates_device: bad arguments");
+  if (base_index + n > ((int64_t)1 << 32))
+    return fail(PQK_EUNSUPPORTED, "pqk_repair_candidates_device: base_index + n must be <= 2^32 (32-bit key index)");
   if (e == 0) return PQK_OK;
   RepairWS w = repair_layout(d_ws, n, std::max<int64_t>(e, 1));
   if (ws_bytes < w.total) return fail(PQK_EINVAL, "pqk_repair_candidates_device: workspace too small");

@@ -145,6 +145,8 @@ class DistributedLloyd:
     def __init__(self, backend, n_total: int, k: int, m: int, group=None):
         self.b = backend
         self.n_total = int(n_total)
+        if self.n_total >= 2**32:
+            raise ValueError("n_total must be < 2^32 (uint32 counts, 32-bit repair key index)")
         self.k = int(k)
         self.m = int(m)
         self.group = group

@@ -10,8 +10,8 @@ Data layout in HBM (one device, one shard of N codes):
   t32      (MP, L, L) f32  ldexp-scaled copy, the assignment filter's source
   labels   (N,) int32 (bit pattern of the reference's uint32 labels)
   sd       (N,) f64        distance of each code to its center (clustering.py:447)
-  hist     (K, M, L) int32 member histograms (clustering.py:344-347)
-  counts   (K,) int32
+  hist     (K, M, L) uint32 member histograms (clustering.py:344-347), in int32 tensors
+  counts   (K,) uint32, in an int32 tensor
   centers  (K, MP) uint8 ×2 (current / next)
 """
 
@@ -399,11 +399,13 @@ def vote_host(hist: np.ndarray, tables: np.ndarray, *, device=None) -> np.ndarra
     dev = device_of(device)
     dt = device_tables(tables, dev)
     k = hist.shape[0]
-    if hist.max(initial=0) >= 2**31:
-        raise ValueError("histogram counts must fit in int32")
+    counts_h = hist[:, 0, :].sum(axis=1) if k else np.zeros(0, np.int64)
+    if hist.min(initial=0) < 0 or counts_h.max(initial=0) >= 2**32:
+        raise ValueError("histogram counts must be non-negative and fit in uint32")
     with torch.cuda.device(dev):
-        h = torch.from_numpy(np.ascontiguousarray(hist, dtype=np.int32)).to(dev)
-        counts = torch.from_numpy(hist[:, 0, :].sum(axis=1).astype(np.int32)).to(dev)
+        # uint32 counts carried in int32 tensors (the kernels read them unsigned)
+        h = torch.from_numpy(np.ascontiguousarray(hist, dtype=np.uint32).view(np.int32)).to(dev)
+        counts = torch.from_numpy(counts_h.astype(np.uint32).view(np.int32)).to(dev)
         out = torch.zeros((k, dt.mp), dtype=torch.uint8, device=dev)
         stats = torch.zeros(STATS_LEN, dtype=torch.int64, device=dev)
         call("pqk_vote_device", _ptr(h), _ptr(counts), k, dt.m, dt.l, _ptr(dt.t64),

@@ -262,6 +262,7 @@ def main() -> None:
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-graphs", action="store_true", help="launch the iteration eagerly (no CUDA graphs)")
     ap.add_argument("--dist", action="store_true", help="sharded NCCL driver even with one rank")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "b200" else args.warmup
@@ -367,8 +368,22 @@ def main() -> None:
         centers0 = codes_host[rng.choice(n_loc, size=k, replace=False)].copy()
     eng = backend.eng
 
+    graphs = None
+    graph_launches = [0]  # kernels launched by graph replays (pqk_launch_count sees captures only)
+
     def step_single(cur):
-        # the iteration body of fit(): one host read (objective + stats) per iteration
+        # the iteration body of fit(): one host read (objective + stats) per iteration; the
+        # device part replays from CUDA graphs after the first (eager) iteration, as fit() does
+        nonlocal graphs
+        if graphs is not None:
+            graphs.main.replay()
+            graph_launches[0] += graphs.main_launches
+            _, st = eng.read_obj_stats()
+            if st[_lib.STAT_EMPTY]:
+                graphs.repair.replay()
+                graph_launches[0] += graphs.repair_launches
+            cur.copy_(eng.new_centers)
+            return cur, st
         eng.assign(cur)
         eng.objective()
         eng.histogram()
@@ -376,7 +391,10 @@ def main() -> None:
         _, st = eng.read_obj_stats()
         if st[_lib.STAT_EMPTY]:
             eng.repair()
-        return eng.new_centers.clone(), st
+        nxt = eng.new_centers.clone()
+        if not args.no_graphs:
+            graphs = engine.IterationGraphs(eng, nxt)
+        return nxt, st
 
     def step(cur):
         if not use_dist:
@@ -399,6 +417,7 @@ def main() -> None:
         torch.cuda.synchronize(dev)
         step_ms, scan_ms, uniq, flagged, vote_fp64, vote_dd = [], [], [], [], [], []
         launches0 = lib.pqk_launch_count()
+        graph_launches[0] = 0
         with ClockSampler(local) as clocks:
             for _ in range(args.steps):
                 flush.fill_(1)
@@ -417,7 +436,7 @@ def main() -> None:
                 flagged.append(int(st[_lib.STAT_FLAGGED]))
                 vote_fp64.append(int(st[_lib.STAT_VOTE_FP64]))
                 vote_dd.append(int(st[_lib.STAT_VOTE_EXACT]))
-        launches = lib.pqk_launch_count() - launches0
+        launches = lib.pqk_launch_count() - launches0 + graph_launches[0]
     lib.pqk_set_profile_events(None, None)
 
     total_ms = float(np.sum(step_ms))
@@ -464,6 +483,7 @@ def main() -> None:
                    "votes_fp64_per_iter": int(np.median(vote_fp64)), "votes_dd_per_iter": int(np.median(vote_dd)),
                    "l2": "flushed (512 MB write) between timed iterations",
                    "step": "assign+certify+objective+histogram+allreduce+vote+repair",
+                   "launch": "eager" if (use_dist or args.no_graphs) else "cuda graphs (after first warm-up step)",
                    "parallelism": f"codes sharded dp{world}"},
         "roofline": {"bound": "smem", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic,

@@ -338,6 +338,11 @@ def fit_device(
         return _fit_on_device(codes_dev, n, t, k, centers, max_iterations, update, None, None, 1, dev)
 
 
+# Replay the device part of each Lloyd iteration from CUDA graphs (engine.IterationGraphs)
+# after the first, eager iteration: ~45 kernel launches become two graph launches.
+USE_CUDA_GRAPHS = True
+
+
 def _fit_on_device(codes_dev, n, t, k, centers, max_iterations, update, external, codes, threads, dev):
     """The Lloyd loop of fit (clustering.py:437-482) on a device code buffer."""
     import torch
@@ -352,26 +357,33 @@ def _fit_on_device(codes_dev, n, t, k, centers, max_iterations, update, external
         previous = None
         converged = False
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        graphs = None  # CUDA graphs of the iteration body, captured after iteration 1
+        use_graphs = USE_CUDA_GRAPHS
         for iteration in range(1, max_iterations + 1):
             # One stream-ordered iteration: assign, objective sums, histogram and the
             # (speculative) vote into the next-centers buffer, then a single host read of
             # objective + stats.  If the stop rule fires the vote result is discarded, so
             # the observable semantics are the reference's (clustering.py:442-481).
             ev[0].record()
-            if device_scan:
-                eng.assign(cur)
+            if graphs is not None:
+                graphs.main.replay()
+                ev_assigned = graphs.ev_assigned
             else:
-                host_centers = engine.download_codes(cur, m_count)
-                lab = np.asarray(external(codes, host_centers, t, threads), dtype=np.uint32)
-                eng.labels[:n].copy_(torch.from_numpy(lab.view(np.int32)).to(dev))
-                eng.distances_for_labels(cur)
-            ev[1].record()
-            eng.objective()
-            eng.histogram()
-            eng.vote()
+                if device_scan:
+                    eng.assign(cur)
+                else:
+                    host_centers = engine.download_codes(cur, m_count)
+                    lab = np.asarray(external(codes, host_centers, t, threads), dtype=np.uint32)
+                    eng.labels[:n].copy_(torch.from_numpy(lab.view(np.int32)).to(dev))
+                    eng.distances_for_labels(cur)
+                ev[1].record()
+                ev_assigned = ev[1]
+                eng.objective()
+                eng.histogram()
+                eng.vote()
             ev[2].record()
             sums, stats = eng.read_obj_stats()
-            assign_seconds = ev[0].elapsed_time(ev[1]) / 1e3
+            assign_seconds = ev[0].elapsed_time(ev_assigned) / 1e3
             objective = engine.mean_from_sum(sums[0], n)
             objective_sq = engine.mean_from_sum(sums[1], n)
             if previous is not None and objective == previous:
@@ -382,10 +394,13 @@ def _fit_on_device(codes_dev, n, t, k, centers, max_iterations, update, external
             start = time.perf_counter()
             empty = int(stats[engine._lib.STAT_EMPTY])
             if empty:
-                eng.repair()
-            nxt = eng.new_centers.clone()
+                if graphs is not None:
+                    graphs.repair.replay()
+                else:
+                    eng.repair()
+            cur.copy_(eng.new_centers)
             torch.cuda.current_stream(dev).synchronize()
-            update_seconds = ev[1].elapsed_time(ev[2]) / 1e3 + (time.perf_counter() - start)
+            update_seconds = ev_assigned.elapsed_time(ev[2]) / 1e3 + (time.perf_counter() - start)
             filled = int(stats[engine._lib.STAT_FILLED])
             nnz_total = int(stats[engine._lib.STAT_NNZ_TOTAL])
             mean_nnz = nnz_total / (filled * m_count) if filled else 0.0
@@ -400,8 +415,9 @@ def _fit_on_device(codes_dev, n, t, k, centers, max_iterations, update, external
                     mean_histogram_nnz=None if update == "naive" else mean_nnz,
                 )
             )
-            cur = nxt
             previous = objective
+            if graphs is None and device_scan and use_graphs and iteration < max_iterations:
+                graphs = engine.IterationGraphs(eng, cur)
         labels = eng.labels_host().copy()
         final_centers = engine.download_codes(cur, m_count).astype(np.uint8)
     return ClusteringResult(final_centers, labels, trace, len(trace), converged)

@@ -613,10 +613,10 @@ static int launch_scan_c(int c_need, const ScanParams& p, int grid, int l, cudaS
   auto kern = scan_kernel<MP, KC, C, NW, S>;
   PQK_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   ProfileEvents& pe = profile_events();
-  if (pe.before) PQK_CUDA_TRY(cudaEventRecord(pe.before, stream));
+  if (pe.before) PQK_CUDA_TRY(record_profile_event(pe.before, stream));
   kern<<<grid, (NW + 1) * 32, smem, stream>>>(p);
   PQK_LAUNCH_CHECK("scan_kernel");
-  if (pe.after) PQK_CUDA_TRY(cudaEventRecord(pe.after, stream));
+  if (pe.after) PQK_CUDA_TRY(record_profile_event(pe.after, stream));
   return PQK_OK;
 }
 

@@ -38,6 +38,16 @@ struct ProfileEvents {
 };
 ProfileEvents& profile_events();
 
+// Record a profile event; inside a CUDA-graph capture it becomes an external event-record
+// node so the event fires on every replay.
+inline cudaError_t record_profile_event(cudaEvent_t ev, cudaStream_t stream) {
+  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+  cudaError_t e = cudaStreamIsCapturing(stream, &st);
+  if (e != cudaSuccess) return e;
+  return st == cudaStreamCaptureStatusActive ? cudaEventRecordWithFlags(ev, stream, cudaEventRecordExternal)
+                                             : cudaEventRecord(ev, stream);
+}
+
 constexpr int kMaxL = 256;
 
 // Padded subspace count of the device code layout: the assignment scan rotates the

@@ -354,6 +354,37 @@ class ShardEngine:
         return self.sd[: self.n].cpu().numpy()
 
 
+class IterationGraphs:
+    """The device part of a Lloyd iteration as two CUDA graphs, replayed every iteration:
+    ``main`` = assign(cur) -> objective sums -> histogram -> vote (~15 kernel launches),
+    ``repair`` = the empty-cluster repair (~30 launches of the 12-digit radix select).
+    ``cur`` is a fixed (K, MP) centers buffer; the caller refreshes it with
+    ``cur.copy_(eng.new_centers)`` between replays.  Capture after one eager iteration
+    (lazy device info and kernel attributes are set up by then).  ``ev_assigned`` is an
+    external event node recorded after the assignment (per-iteration assign timing)."""
+
+    def __init__(self, eng: ShardEngine, cur: "torch.Tensor"):
+        import torch
+
+        self.eng, self.cur = eng, cur
+        self.ev_assigned = torch.cuda.Event(enable_timing=True, external=True)
+        lib = _lib.load()
+        self.main = torch.cuda.CUDAGraph()
+        l0 = lib.pqk_launch_count()
+        with torch.cuda.graph(self.main, capture_error_mode="thread_local"):
+            eng.assign(cur)
+            self.ev_assigned.record()
+            eng.objective()
+            eng.histogram()
+            eng.vote()
+        self.main_launches = int(lib.pqk_launch_count() - l0)
+        self.repair = torch.cuda.CUDAGraph()
+        l0 = lib.pqk_launch_count()
+        with torch.cuda.graph(self.repair, capture_error_mode="thread_local"):
+            eng.repair()
+        self.repair_launches = int(lib.pqk_launch_count() - l0)
+
+
 # ---------------------------------------------------------------------------
 # one-shot host helpers used by the public API
 def assign_host(codes: np.ndarray, centers: np.ndarray, tables: np.ndarray, *, device=None, want_sd=False):

@@ -127,3 +127,33 @@ def test_fit_long_codes_matches_oracle(pqk, oracle, m, n, k, iters):
     res = pqk.fit(codes, tables, k, max_iterations=iters, seed=m)
     ref = oracle.fit(codes, tables, k, max_iterations=iters, seed=m, scan=oracle.assign_c)
     _compare(res, ref)
+
+
+def test_graph_replay_equals_eager(pqk, oracle, monkeypatch):
+    """Iterations 2.. replay CUDA graphs (engine.IterationGraphs); same result as eager
+    launches and as the oracle, with repairs inside the replayed iterations."""
+    from paper_1709_03708_b200 import clustering, engine
+
+    tables = random_tables(4, 256, seed=21, sub_dim=8)
+    codes = mixture_codes(20_011, 4, 256, 50, seed=22)
+    k, iters, seed = 500, 8, 3
+    made = []
+    real = engine.IterationGraphs
+
+    def spy(*a, **kw):
+        g = real(*a, **kw)
+        made.append(g)
+        return g
+
+    monkeypatch.setattr(engine, "IterationGraphs", spy)
+    graphed = pqk.fit(codes, tables, k, iters, seed)
+    assert len(made) == 1 and made[0].main_launches > 0 and made[0].repair_launches > 0
+    monkeypatch.setattr(clustering, "USE_CUDA_GRAPHS", False)
+    eager = pqk.fit(codes, tables, k, iters, seed)
+    ref = oracle.fit(codes, tables, k, iters, seed, scan=oracle.assign_c)
+    for res in (graphed, eager):
+        np.testing.assert_array_equal(res.labels, ref["labels"])
+        np.testing.assert_array_equal(res.centers, ref["centers"])
+        assert [s.objective for s in res.trace] == [t["objective"] for t in ref["trace"]]
+        assert [s.repaired_clusters for s in res.trace] == [t["repaired"] for t in ref["trace"]]
+    assert sum(t["repaired"] for t in ref["trace"][1:]) > 0

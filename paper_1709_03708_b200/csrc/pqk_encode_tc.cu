@@ -81,12 +81,12 @@ extern "C" int pqk_tc_selftest(const void* d_a, const void* d_b, float* d_c, int
 // per subspace and split v = hi + lo into fp16 pairs (hi.hi + hi.lo [+ lo.hi when the
 // tile's x are not exactly fp16]); s^2|c_j|^2 and the row's s^2|x_r|^2 enter through
 // 16 extra K columns of the hi pass (three fp16 parts each, times an exact power of
-// two).  The epilogue therefore has no per-distance floating-point work: a key is
-// the accumulator's bits with the low 6 bits replaced by the column (one LOP3),
-// compared as signed int32 so that the (rare) negative values produced by rounding
-// next to a zero distance still sort below every positive value.  Best and runner-up
-// keys give a certificate: the winner is certified when the runner-up exceeds it by
-// more than twice a rigorous bound on |computed - exact| (split, skipped lo.lo term,
+// two).  The epilogue therefore has no per-distance floating-point work: accumulator
+// words compare as signed int32 (so that the rare negative values produced by rounding
+// next to a zero distance still sort below every positive value), and the best and
+// runner-up come from group (j / 16) and class (j % 16) minima, one 3-input min per
+// column.  They give a certificate: the winner is certified when the runner-up exceeds it
+// by more than twice a rigorous bound on |computed - exact| (split, skipped lo.lo term,
 // tensor-core accumulation).  Uncertified (vector, subspace) pairs are re-decided by
 // the exact float64 sequential sum (scipy cdist order) in encode_exact_kernel.
 //
@@ -94,9 +94,10 @@ extern "C" int pqk_tc_selftest(const void* d_a, const void* d_b, float* d_c, int
 //   warp 0   TMA producer: 2-D tensor-map loads of X[128 rows x dsub] per tile
 //   warp 1   TMEM allocator + single-thread tcgen05.mma issuer (2 accumulators of
 //            128 x 256 fp32 = all 512 TMEM columns, double-buffered)
-//   warps 2-17 transform (fp32 -> scaled fp16 hi/lo + extension columns in the UMMA
-//            K-major layout) and epilogue (tcgen05.ld, keys, argmin, certificate);
-//            warp w reads TMEM lanes 32*(w%4).. and columns [64h, 64h+64), h=(w-2)/4.
+//   warps 2-9 epilogue (tcgen05.ld, partition minima, certificate), whole rows: warp w
+//            reads TMEM lane quadrant w % 4 of accumulator (w - 2) / 4
+//   warps 10-17 transform (fp32 -> scaled fp16 hi/lo + extension columns in the UMMA
+//            K-major layout), 16 rows each
 // ===========================================================================
 #include <cuda.h>
 #include <cudaTypedefs.h>
@@ -154,7 +155,7 @@ struct EncParams {
   uint32_t flag_cap;
   int ntiles;        // 128-row tiles
   int tstride;       // CTAs per subspace
-  uint32_t keymask;  // ~31u, a run-time value so that key packing is one LOP3
+  uint32_t keymask;  // ~15u, a run-time value so that key packing is one LOP3
   uint32_t one;      // 1
 };
 
@@ -206,65 +207,70 @@ __device__ __forceinline__ uint32_t imad(uint32_t x, uint32_t one, uint32_t y) {
   return r;
 }
 
-// minimum of 32 values as a depth-4 tree of 3-input minima (independent operations for
-// instruction-level parallelism: one warp per row block must keep the ALU pipe busy)
-__device__ __forceinline__ int tree_min32(const uint32_t (&k)[32]) {
-  int t[11];
-#pragma unroll
-  for (int i = 0; i < 10; ++i) t[i] = imin3((int)k[3 * i], (int)k[3 * i + 1], (int)k[3 * i + 2]);
-  t[10] = min((int)k[30], (int)k[31]);
-  const int u0 = imin3(t[0], t[1], t[2]), u1 = imin3(t[3], t[4], t[5]), u2 = imin3(t[6], t[7], t[8]);
-  const int u3 = min(t[9], t[10]);
-  return imin3(u0, u1, min(u2, u3));
+// Best and runner-up of a row's 256 accumulator words by two partitions of the columns:
+// groups g = j / 16 and classes q = j % 16 (a group and a class share exactly one column).
+// Every column other than the best lies outside the best's group or outside its class,
+// so runner-up = min(second-smallest group minimum, second-smallest class minimum).
+// Words compare as signed int32 (raw fp32 bits: the rare negative values next to a zero
+// distance sort below every positive one; two negatives in the wrong order only make the
+// certificate fail).  Per column: half a 3-input min for its class, half for its group.
+__device__ __forceinline__ int tree_min16(const uint32_t (&k)[32], int o) {
+  const int t0 = imin3((int)k[o], (int)k[o + 1], (int)k[o + 2]);
+  const int t1 = imin3((int)k[o + 3], (int)k[o + 4], (int)k[o + 5]);
+  const int t2 = imin3((int)k[o + 6], (int)k[o + 7], (int)k[o + 8]);
+  const int t3 = imin3((int)k[o + 9], (int)k[o + 10], (int)k[o + 11]);
+  const int t4 = imin3((int)k[o + 12], (int)k[o + 13], (int)k[o + 14]);
+  return min(imin3(t0, t1, t2), imin3(t3, t4, (int)k[o + 15]));
 }
-__device__ __forceinline__ uint32_t tree_umin32(const uint32_t (&k)[32]) {
-  uint32_t t[11];
-#pragma unroll
-  for (int i = 0; i < 10; ++i) t[i] = umin3(k[3 * i], k[3 * i + 1], k[3 * i + 2]);
-  t[10] = min(k[30], k[31]);
-  const uint32_t u0 = umin3(t[0], t[1], t[2]), u1 = umin3(t[3], t[4], t[5]), u2 = umin3(t[6], t[7], t[8]);
-  const uint32_t u3 = min(t[9], t[10]);
-  return umin3(u0, u1, min(u2, u3));
+// smallest two group minima (G2 = G1 on a tie, so a tie never certifies) and G1's group
+__device__ __forceinline__ void fold_group(int v, int g, int& G1, int& G2, int& gi) {
+  gi = v < G1 ? g : gi;
+  G2 = min(G2, max(G1, v));
+  G1 = min(G1, v);
 }
-
-// best (signed key) and runner-up of 32 raw accumulator words of one row; keys carry the
-// column within the chunk in their low 5 bits
-__device__ __forceinline__ void chunk_best(uint32_t (&k)[32], uint32_t kmask, uint32_t one, int& bc, int& rc) {
+// one 32-column chunk c: groups 2c, 2c+1; classes q and q (columns q, q+16)
+__device__ __forceinline__ void chunk_fold(const uint32_t (&k)[32], int c, int (&cls)[16], int& G1, int& G2,
+                                           int& gi) {
 #pragma unroll
-  for (int j = 0; j < 32; ++j) k[j] = (k[j] & kmask) | (uint32_t)j;
-  bc = tree_min32(k);
-  // runner-up: keys are unique, so min over (k - (b + 1)) mod 2^32 maps the winner to
-  // 0xffffffff and every other key to k - b - 1, in signed-key order
-  const uint32_t nbp = ~(uint32_t)bc;  // -(b + 1)
+  for (int q = 0; q < 16; ++q) cls[q] = imin3(cls[q], (int)k[q], (int)k[q + 16]);
+  fold_group(tree_min16(k, 0), 2 * c, G1, G2, gi);
+  fold_group(tree_min16(k, 16), 2 * c + 1, G1, G2, gi);
+}
+// second-smallest class minimum (as a key truncated to 4 bits less, class in the low
+// bits: unique keys) and the class of the smallest
+__device__ __forceinline__ void class_best2(const int (&cls)[16], uint32_t kmask, uint32_t one, int& qb, int& Y) {
+  uint32_t ck[32];
 #pragma unroll
-  for (int j = 0; j < 32; ++j) k[j] = imad(k[j], one, nbp);
-  rc = (int)(tree_umin32(k) - nbp);
+  for (int q = 0; q < 16; ++q) ck[q] = ((uint32_t)cls[q] & kmask) | (uint32_t)q;
+  const int b = tree_min16(ck, 0);
+  qb = b & 15;
+  const uint32_t nbp = ~(uint32_t)b;  // -(b + 1): the winner maps to 0xffffffff
+#pragma unroll
+  for (int q = 0; q < 16; ++q) ck[q] = imad(ck[q], one, nbp);
+  const uint32_t t0 = umin3(ck[0], ck[1], ck[2]), t1 = umin3(ck[3], ck[4], ck[5]);
+  const uint32_t t2 = umin3(ck[6], ck[7], ck[8]), t3 = umin3(ck[9], ck[10], ck[11]);
+  const uint32_t t4 = umin3(ck[12], ck[13], ck[14]);
+  Y = (int)(min(umin3(t0, t1, t2), umin3(t3, t4, ck[15])) - nbp) & (int)kmask;
 }
 
 // Epilogue of one 128-row item for one epilogue warp (row n of TMEM lane quadrant q):
 // the 256 accumulator columns (two N=128 halves, signalled and released separately),
-// packed-key best / runner-up, certificate, code store or flag.
+// best / runner-up by the group x class partitions, certificate, code store or flag.
 __device__ __forceinline__ void epilogue_row(const EncParams& p, int m, int64_t n, uint32_t tacc, uint64_t* tfull2,
                                              uint64_t* tempty2, uint32_t ph, float4 st, float eps_main2,
                                              float eps_main3, float eps_ext, float cb, float cnm, float s1c,
                                              float sqrt_kp, int lane) {
-  const uint32_t kmask = p.keymask, kone = p.one;
-  int B = 0x7fffffff, R = 0x7fffffff, Bi = 0;
+  int cls[16];
+#pragma unroll
+  for (int q = 0; q < 16; ++q) cls[q] = 0x7fffffff;
+  int G1 = 0x7fffffff, G2 = 0x7fffffff, gi = 0;
   uint32_t ka[32], kb[32];
   tmem_ld32(tacc, ka);
 #pragma unroll
   for (int c = 0; c < kN / kChunk; c += 2) {
     tmem_wait32(ka);
     tmem_ld32(tacc + (uint32_t)((c + 1) * kChunk), kb);
-    int bc, rc;
-    chunk_best(ka, kmask, kone, bc, rc);
-    if ((bc & ~31) < (B & ~31)) {  // strictly smaller value: ties keep the earlier chunk
-      R = min(B, rc);
-      B = bc;
-      Bi = c;
-    } else {
-      R = min(R, bc);
-    }
+    chunk_fold(ka, c, cls, G1, G2, gi);
     tmem_wait32(kb);
     if (c + 2 == kN / kChunk / 2 || c + 2 == kN / kChunk) {  // a column half fully read
       tc::fence_before();
@@ -278,21 +284,16 @@ __device__ __forceinline__ void epilogue_row(const EncParams& p, int m, int64_t 
       }
       tmem_ld32(tacc + (uint32_t)((c + 2) * kChunk), ka);
     }
-    chunk_best(kb, kmask, kone, bc, rc);
-    if ((bc & ~31) < (B & ~31)) {
-      R = min(B, rc);
-      B = bc;
-      Bi = c + 1;
-    } else {
-      R = min(R, bc);
-    }
+    chunk_fold(kb, c + 1, cls, G1, G2, gi);
   }
   if (n < p.n) {
-    // keys dropped 5 mantissa bits: the value lies within 32 ulp <= 2^-18 |v| of the key
-    // value, above it for v >= 0 and below it for v < 0
-    const float wv = __int_as_float(B & ~31), rv = __int_as_float(R & ~31);
-    const float w_hi = wv >= 0.f ? wv * 1.00000762939453125f : wv;  // 1 + 2^-17
-    const float r_lo = rv >= 0.f ? rv : rv * 1.00000762939453125f;
+    int qb, Y;
+    class_best2(cls, p.keymask, p.one, qb, Y);
+    const int R = min(G2, Y);
+    // the best word is exact; R is exact (G2) or truncated by 4 mantissa bits (Y: within
+    // 16 ulp <= 2^-19 |v| of the value, below it for v >= 0, above it for v < 0)
+    const float w_hi = __int_as_float(G1), rv = __int_as_float(R);
+    const float r_lo = rv >= 0.f ? rv : rv * 1.00000762939453125f;  // 1 + 2^-17
     // rigorous bound on |computed - exact| of any D_rj (see header)
     const float P = st.y * cb * 1.001f;  // >= sum |split products|
     const float E = (st.w != 0.f ? eps_main3 : eps_main2) * P + eps_ext * (P + cnm + st.x) * 1.001f  //
@@ -302,7 +303,7 @@ __device__ __forceinline__ void epilogue_row(const EncParams& p, int m, int64_t 
                     + 1e-3f;
     const bool cert = st.z != 0.f && (r_lo - w_hi) > 2.0f * E * 1.0001f;
     if (cert) {
-      p.codes[n * p.stride + m] = (uint8_t)(kChunk * Bi + (B & 31));
+      p.codes[n * p.stride + m] = (uint8_t)(16 * gi + qb);
     } else {
       atomicAdd(&p.counters[0], 1u);
       const unsigned f = atomicAdd(&p.counters[2 + m], 1u);
@@ -1401,7 +1402,7 @@ int launch_encode_tc(const float* d_x, int64_t n, int d, const float* d_cw, int 
   ep.flag_cap = cap;
   ep.ntiles = (int)((n + kRows - 1) / kRows);
   ep.tstride = std::max(1, std::min(di.sms / m, ep.ntiles));  // CTAs per subspace
-  ep.keymask = ~31u;
+  ep.keymask = ~15u;
   ep.one = 1u;
   auto kern = encode_tc_kernel<KP>;
   PQK_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM));
@@ -1471,7 +1472,7 @@ int launch_encode_tck(const float* d_x, int64_t n, int d, const float* d_cw, int
   ep.flag_cap = cap;
   ep.ntiles = (int)((n + kRows - 1) / kRows);
   ep.tstride = std::max(1, std::min(di.sms / m, ep.ntiles));
-  ep.keymask = ~31u;
+  ep.keymask = ~15u;
   ep.one = 1u;
   PQK_CUDA_TRY(cudaFuncSetAttribute(encode_tck_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM));
   encode_tck_kernel<<<ep.tstride * m, kThreads, G::SMEM, stream>>>(map, ep);

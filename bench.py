@@ -686,6 +686,7 @@ def main() -> None:
         d2h = n_loc * 4 + k * m + 16 + _lib.STATS_LEN * 8
         out["e2e"] = {"value": n_total * k / e2e_s, "unit": "evals/s", "h2d_bytes_per_step": int(h2d),
                       "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_s * 1e3,
+                      "ms_steps": [round(t * 1e3, 3) for t in times],
                       "api": "pqk_lloyd_step_host (C-ABI, pinned host buffers)"}
         lib.pqk_host_release(local)
     elif not args.no_e2e:

@@ -68,6 +68,7 @@ struct HostCtx {
   cudaStream_t stream = nullptr;
   cudaStream_t copy_stream = nullptr;  // D2H of results that are final early (labels)
   cudaEvent_t assigned = nullptr;
+  cudaEvent_t codes_ready = nullptr;  // the codes' H2D (copy stream) has landed
   std::mutex mu;
   struct Buf {
     void* p = nullptr;
@@ -102,6 +103,7 @@ static int ctx_begin(int device, HostCtx*& ctx) {
     PQK_CUDA_TRY(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
     PQK_CUDA_TRY(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
     PQK_CUDA_TRY(cudaEventCreateWithFlags(&ctx->assigned, cudaEventDisableTiming));
+    PQK_CUDA_TRY(cudaEventCreateWithFlags(&ctx->codes_ready, cudaEventDisableTiming));
     ctx->init = true;
   }
   return PQK_OK;
@@ -189,17 +191,30 @@ static int upload_tables(HostCtx* c, const double* tables, int m, int l, int& fp
   return pqk_tables_to_f32((const double*)c->t64.p, m, l, e, (float*)c->t32.p, c->stream);
 }
 
-static int upload_codes(HostCtx* c, HostCtx::Buf& rawb, HostCtx::Buf& dst, const uint8_t* h, int64_t n, int m) {
+static int upload_codes(HostCtx* c, HostCtx::Buf& rawb, HostCtx::Buf& dst, const uint8_t* h, int64_t n, int m,
+                        cudaStream_t stream) {
   const int mp = padded_m(m);
   PQK_TRY(ensure(dst, (size_t)std::max<int64_t>(n, 1) * mp));
   if (n == 0) return PQK_OK;
   if (mp == m) {
-    PQK_CUDA_TRY(cudaMemcpyAsync(dst.p, h, (size_t)n * m, cudaMemcpyHostToDevice, c->stream));
+    PQK_CUDA_TRY(cudaMemcpyAsync(dst.p, h, (size_t)n * m, cudaMemcpyHostToDevice, stream));
     return PQK_OK;
   }
   PQK_TRY(ensure(rawb, (size_t)n * m));
-  PQK_CUDA_TRY(cudaMemcpyAsync(rawb.p, h, (size_t)n * m, cudaMemcpyHostToDevice, c->stream));
-  return pqk_pad_codes_device((const uint8_t*)rawb.p, n, m, (uint8_t*)dst.p, c->stream);
+  PQK_CUDA_TRY(cudaMemcpyAsync(rawb.p, h, (size_t)n * m, cudaMemcpyHostToDevice, stream));
+  return pqk_pad_codes_device((const uint8_t*)rawb.p, n, m, (uint8_t*)dst.p, stream);
+}
+static int upload_codes(HostCtx* c, HostCtx::Buf& rawb, HostCtx::Buf& dst, const uint8_t* h, int64_t n, int m) {
+  return upload_codes(c, rawb, dst, h, n, m, c->stream);
+}
+
+// The N codes go up on the copy stream first, so that their H2D overlaps the table
+// upload, its scale decision (one host sync on the main stream) and the center upload;
+// the main stream joins before the assignment.
+static int start_codes_upload(HostCtx* c, const uint8_t* h, int64_t n, int m) {
+  PQK_TRY(upload_codes(c, c->raw, c->codes, h, n, m, c->copy_stream));
+  PQK_CUDA_TRY(cudaEventRecord(c->codes_ready, c->copy_stream));
+  return PQK_OK;
 }
 
 static bool validate_codes_host(const uint8_t* codes, int64_t n, int m, int l) {
@@ -309,9 +324,10 @@ extern "C" int pqk_assign_host(const uint8_t* codes, int64_t n, int32_t m, const
   PQK_TRY(ctx_begin(device, c));
   std::lock_guard<std::mutex> lock(c->mu);
   int fp64_only = 0;
+  PQK_TRY(start_codes_upload(c, codes, n, m));
   PQK_TRY(upload_tables(c, tables, m, l, fp64_only));
-  PQK_TRY(upload_codes(c, c->raw, c->codes, codes, n, m));
-  PQK_TRY(upload_codes(c, c->raw, c->centers, centers, k, m));
+  PQK_TRY(upload_codes(c, c->centers_raw, c->centers, centers, k, m));
+  PQK_CUDA_TRY(cudaStreamWaitEvent(c->stream, c->codes_ready, 0));
   PQK_TRY(ensure(c->labels, (size_t)n * sizeof(uint32_t)));
   PQK_TRY(ensure(c->sd, (size_t)n * sizeof(double)));
   const size_t wsb = pqk_assign_workspace_bytes(n, k, m, l);
@@ -360,9 +376,10 @@ extern "C" int pqk_lloyd_step_host(const uint8_t* codes, int64_t n, int32_t m, c
   std::lock_guard<std::mutex> lock(c->mu);
   const int mp = padded_m(m);
   int fp64_only = 0;
+  PQK_TRY(start_codes_upload(c, codes, n, m));
   PQK_TRY(upload_tables(c, tables, m, l, fp64_only));
-  PQK_TRY(upload_codes(c, c->raw, c->codes, codes, n, m));
-  PQK_TRY(upload_codes(c, c->raw, c->centers, centers, k, m));
+  PQK_TRY(upload_codes(c, c->centers_raw, c->centers, centers, k, m));
+  PQK_CUDA_TRY(cudaStreamWaitEvent(c->stream, c->codes_ready, 0));
   PQK_TRY(ensure(c->labels, (size_t)n * sizeof(uint32_t)));
   PQK_TRY(ensure(c->sd, (size_t)n * sizeof(double)));
   const size_t wsb = pqk_assign_workspace_bytes(n, k, m, l);

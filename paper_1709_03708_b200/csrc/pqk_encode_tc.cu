@@ -420,22 +420,23 @@ __global__ void __launch_bounds__(kThreads, 1) encode_tc_kernel(const __grid_con
           tc::fence_after();
           const uint32_t tacc = tbase + (uint32_t)ab * kN + (uint32_t)hf * (kN / 2);
           const uint32_t b_hi = b_hi0 + (uint32_t)hf * 16u * sboE, b_lo = b_lo0 + (uint32_t)hf * 16u * sboP;
-          // hi . hi, hi . lo, [lo . hi], then the |c|^2 / |x|^2 extension block last, so that
-          // the large extension terms enter the accumulator in a single instruction
-#pragma unroll
-          for (int s = 0; s < KP / 16; ++s)
-            tc::mma_f16(tacc, tc::smem_desc(a_hi + s * 256, 128, sboE), tc::smem_desc(b_hi + s * 256, 128, sboE), idesc,
-                        s > 0 ? 1u : 0u);
+          // hi . lo, [lo . hi] first, while the accumulator is small (their truncation errors
+          // scale with it, <= 2^-9 of the main terms), then hi . hi, then the |c|^2 / |x|^2
+          // extension block last, so that the large extension terms enter in one instruction
 #pragma unroll
           for (int s = 0; s < KP / 16; ++s)
             tc::mma_f16(tacc, tc::smem_desc(a_hi + s * 256, 128, sboE), tc::smem_desc(b_lo + s * 256, 128, sboP), idesc,
-                        1u);
+                        s > 0 ? 1u : 0u);
           if (lo_any) {
 #pragma unroll
             for (int s = 0; s < KP / 16; ++s)
               tc::mma_f16(tacc, tc::smem_desc(a_lo + s * 256, 128, sboP), tc::smem_desc(b_hi + s * 256, 128, sboE),
                           idesc, 1u);
           }
+#pragma unroll
+          for (int s = 0; s < KP / 16; ++s)
+            tc::mma_f16(tacc, tc::smem_desc(a_hi + s * 256, 128, sboE), tc::smem_desc(b_hi + s * 256, 128, sboE), idesc,
+                        1u);
           tc::mma_f16(tacc, tc::smem_desc(a_hi + (KP / 16) * 256, 128, sboE),
                       tc::smem_desc(b_hi + (KP / 16) * 256, 128, sboE), idesc, 1u);
           tc::commit(&tfull[2 * ab + hf]);
@@ -451,12 +452,14 @@ __global__ void __launch_bounds__(kThreads, 1) encode_tc_kernel(const __grid_con
     const int e = ew >> 2;    // accumulator / item parity
     const int er = 32 * q + lane;
     // tensor-core accumulation model: an MMA instruction adds 16 products to the
-    // accumulator with error <= 17 * 2^-23 * max(|addend|); the main passes (2 KP/16
-    // instructions, 3 KP/16 for a row whose x is not exactly fp16: adding the exact zeros
-    // of lo . hi leaves an accumulator unchanged) have every addend and partial sum bounded
-    // by P, the extension instruction (7 nonzero addends) by P + |c|^2 + |x|^2
-    const float eps_main2 = (float)(17 * 2 * KP / 16) * 1.1920928955078125e-07f;
-    const float eps_main3 = (float)(17 * 3 * KP / 16) * 1.1920928955078125e-07f;
+    // accumulator with error <= 17 * 2^-23 * max(|addend|).  The lo passes run first: their
+    // products and partial sums are bounded by P_L <= 2^-9 P as |lo| <= 2^-11 |hi| (plus
+    // subnormal floors < 2^-24 (sqrt(KP) |s x| + S1c) P-units, far inside the 1e-3 term); the KP/16 hi . hi instructions then see
+    // addends <= P + P_L; the extension instruction (7 nonzero addends) P + |c|^2 + |x|^2.
+    // Total: 17 * 2^-23 * (KP/16) * (P + 3 P_L) <= 17 * (KP/16) * (1 + 3 * 2^-9) * 2^-23 * P,
+    // whether or not the tile runs the lo . hi pass.
+    const float eps_main2 = (float)(17 * KP / 16) * (1.0f + 3.0f / 512.0f) * 1.1920928955078125e-07f;
+    const float eps_main3 = eps_main2;
     const float eps_ext = 7.0f * 1.1920928955078125e-07f;
     const float cb = s_cst[CST_CB], cnm = s_cst[CST_CN], s1c = s_cst[CST_S1C];
     for (int w = e; w < items; w += 2) {

@@ -1,10 +1,10 @@
 """Dev diagnostic: measured tcgen05 fp16 -> fp32 accumulation error of the encoder's
 split-operand formulation against the error model used by its certificate.
 
-Builds, for one subspace, the encoder's A = [s x hi | s x hi | s x lo | ext] and
-B = [-2 s c hi | -2 s c lo | -2 s c hi | ext] rows (the same K order as the kernel:
-hi.hi, hi.lo, lo.hi, extension last), runs them through pqk_tc_selftest (one
-128 x 256 x K tile) and compares D with the exact s^2 |x - c|^2 + (x2 - s^2 |x|^2).
+Builds, for one subspace, the encoder's split operands in the kernel's K order
+(hi.lo, lo.hi, hi.hi, extension last; and the older hi-first order), runs them through
+pqk_tc_selftest (one 128 x 256 x K tile) and compares D with the exact MMA result and
+with s^2 |x - c|^2 + (x2 - s^2 |x|^2), each relative to its certificate model.
 
 usage: python tools/diag_tc_error.py [scale_x]
 """
@@ -62,92 +62,41 @@ A_ext[:, 3], A_ext[:, 4], A_ext[:, 5] = x_h, x_m, x_l
 B_ext = np.zeros((256, 16), np.float16)
 B_ext[:, 0], B_ext[:, 1], B_ext[:, 2] = c_h, c_m, c_l
 B_ext[:, 3:6] = np.float16(32768.0)
-A = np.concatenate([xh, xh, xl, A_ext], axis=1)
-B = np.concatenate([bh, bl, bh, B_ext], axis=1)
-k = A.shape[1]
-da = torch.from_numpy(np.ascontiguousarray(A)).to(dev)
-db = torch.from_numpy(np.ascontiguousarray(B)).to(dev)
-dc = torch.zeros((128, 256), dtype=torch.float32, device=dev)
-_lib.call("pqk_tc_selftest", C.c_void_p(da.data_ptr()), C.c_void_p(db.data_ptr()), C.c_void_p(dc.data_ptr()), k,
-          C.c_void_p(torch.cuda.current_stream(dev).cuda_stream))
-got = dc.cpu().numpy().astype(np.float64)
-# exact value of what the MMA should produce with exact fp16 products and exact sums
-exact_mma = A.astype(np.float64) @ B.astype(np.float64).T
-# value the certificate models: s^2 |x-c|^2 + (x2 - s^2|x|^2)
+def run_mma(A, B):
+    da = torch.from_numpy(np.ascontiguousarray(A)).to(dev)
+    db = torch.from_numpy(np.ascontiguousarray(B)).to(dev)
+    dc = torch.zeros((128, 256), dtype=torch.float32, device=dev)
+    _lib.call("pqk_tc_selftest", C.c_void_p(da.data_ptr()), C.c_void_p(db.data_ptr()), C.c_void_p(dc.data_ptr()),
+              A.shape[1], C.c_void_p(torch.cuda.current_stream(dev).cuda_stream))
+    return dc.cpu().numpy().astype(np.float64)
+
+
 x64 = x.astype(np.float64)
 c64 = c.astype(np.float64)
+# value the certificate models: s^2 |x-c|^2 + (x2 - s^2|x|^2)
 d_true = s * s * ((x64[:, None, :] - c64[None, :, :]) ** 2).sum(-1) + (x2.astype(np.float64) - s * s * (x64**2).sum(1))[:, None]
-acc_err = np.abs(got - exact_mma)
-tot_err = np.abs(got - d_true)
 X = np.linalg.norm(xs.astype(np.float64), axis=1)
 Cb = np.linalg.norm(bs.astype(np.float64), axis=1).max()
 P = X * Cb
 CN = cn.max()
-model_acc = 102 * 2**-23 * P + 7 * 2**-23 * (P + CN + x2)
-model = model_acc + 4 * 2**-23 * P
-for name, sl in (("integer rows", slice(0, 64)), ("float rows", slice(64, 128))):
-    ra = (acc_err[sl] / model_acc[sl, None]).max()
-    rt = (tot_err[sl] / model[sl, None]).max()
-    print(f"{name}: max accumulation error / model {ra:.3g}; max total error / model {rt:.3g}; "
-          f"max acc err {acc_err[sl].max():.4g}, median model {np.median(model[sl]):.4g}")
-
-
-def certify_like_kernel(D, x2u, X, cb, cnm, s1c, kp=32):
-    """The kernel's key packing, chunk merge and certificate on float32 accumulators D."""
-    bits = D.astype(np.float32).view(np.int32)
-    keys = (bits & ~31) | (np.arange(256) % 32)
-    masked = keys & ~31
-    order = np.argsort(keys, axis=1, kind="stable")
-    # kernel merges chunk bests with 'strictly smaller masked value' -> same as global key order
-    # except for masked-value ties across chunks; emulate directly
-    B = np.full(len(D), 0x7fffffff, np.int64)
-    R = np.full(len(D), 0x7fffffff, np.int64)
-    for c in range(8):
-        kc = keys[:, 32 * c: 32 * c + 32].astype(np.int64)
-        bc = kc.min(1)
-        srt = np.sort(kc, 1)
-        rc = srt[:, 1]
-        better = (bc & ~31) < (B & ~31)
-        R = np.where(better, np.minimum(B, rc), np.minimum(R, bc))
-        B = np.where(better, bc, B)
-    wv = (B & ~31).astype(np.int32).view(np.float32).astype(np.float64)
-    rv = (R & ~31).astype(np.int32).view(np.float32).astype(np.float64)
-    w_hi = wv + np.abs(wv) * 2**-17
-    r_lo = rv - np.abs(rv) * 2**-17
-    P = X * cb * 1.001
-    E = (17 * 3 * kp / 16) * 2**-23 * P + 7 * 2**-23 * (P + cnm + x2u) * 1.001 + 4 * 2**-23 * P + 2**-25 * (
-        np.sqrt(kp) * X + s1c) + 2**-30 * (cnm + x2u) + 1e-3
-    return (r_lo - w_hi) > 2 * E * 1.0001
-
-
-if __name__ == "__main__" and len(sys.argv) > 2:
-    # flag-rate emulation over many 128-row tiles of integer-valued rows
-    tiles = int(sys.argv[2])
-    cert_n = 0
-    for t in range(tiles):
-        xt = np.rint(np.random.default_rng(100 + t).standard_normal((128, ks)) * scale_x).astype(np.float32)
-        xs = (xt * s).astype(np.float32)
-        xh, xl = split(xs)
-        x2 = (xs.astype(np.float32) ** 2).sum(1, dtype=np.float32) * np.float32(1 + 40 * 2**-24)
-        xv = (x2 * 2.0**-15).astype(np.float32)
-        x_h = xv.astype(np.float16)
-        r1x = xv - x_h.astype(np.float32)
-        x_m = r1x.astype(np.float16)
-        x_l = (r1x - x_m.astype(np.float32)).astype(np.float16)
-        A_ext = np.zeros((128, 16), np.float16)
-        A_ext[:, 0:3] = np.float16(acn)
-        A_ext[:, 3], A_ext[:, 4], A_ext[:, 5] = x_h, x_m, x_l
-        lo_any = np.any(xl != 0)
-        A = np.concatenate([xh, xh] + ([xl] if lo_any else []) + [A_ext], axis=1)
-        Bm = np.concatenate([bh, bl] + ([bh] if lo_any else []) + [B_ext], axis=1)
-        da = torch.from_numpy(np.ascontiguousarray(A)).to(dev)
-        db = torch.from_numpy(np.ascontiguousarray(Bm)).to(dev)
-        dc = torch.zeros((128, 256), dtype=torch.float32, device=dev)
-        _lib.call("pqk_tc_selftest", C.c_void_p(da.data_ptr()), C.c_void_p(db.data_ptr()), C.c_void_p(dc.data_ptr()),
-                  A.shape[1], C.c_void_p(torch.cuda.current_stream(dev).cuda_stream))
-        D = dc.cpu().numpy()
-        X = np.sqrt(x2.astype(np.float64)) * 1.000002
-        cert = certify_like_kernel(D, x2.astype(np.float64), X, Cb * 1.0001, CN * 1.0001,
-                                   np.abs(bs).sum(1).max() * 1.0001)
-        cert_n += cert.sum()
-    print(f"emulated certificate: {tiles * 128 - cert_n} of {tiles * 128} rows flagged")
+n16 = ks // 16
+# kernel order (lo passes first, then hi . hi, extension last) and its model
+# 17 * 2^-23 * (KP/16) * (1 + 3 * 2^-9) * P; the older hi-first order with 17 * 3 * KP/16
+orders = {
+    "lo-first (kernel)": (np.concatenate([xh, xl, xh, A_ext], axis=1), np.concatenate([bl, bh, bh, B_ext], axis=1),
+                          17 * n16 * (1 + 3 / 512) * 2**-23 * P),
+    "hi-first (v2)": (np.concatenate([xh, xh, xl, A_ext], axis=1), np.concatenate([bh, bl, bh, B_ext], axis=1),
+                      17 * 3 * n16 * 2**-23 * P),
+}
+for oname, (A, B, main) in orders.items():
+    got = run_mma(A, B)
+    exact_mma = A.astype(np.float64) @ B.astype(np.float64).T  # exact fp16 products, exact sums
+    acc_err = np.abs(got - exact_mma)
+    tot_err = np.abs(got - d_true)
+    model_acc = main + 7 * 2**-23 * (P + CN + x2)
+    model = model_acc + 4 * 2**-23 * P
+    for name, sl in (("integer rows", slice(0, 64)), ("float rows", slice(64, 128))):
+        ra = (acc_err[sl] / model_acc[sl, None]).max()
+        rt = (tot_err[sl] / model[sl, None]).max()
+        print(f"{oname} {name}: max accumulation error / model {ra:.3g}; max total error / model {rt:.3g}; "
+              f"max acc err {acc_err[sl].max():.4g}, median model {np.median(model[sl]):.4g}")

@@ -146,6 +146,7 @@ struct Geo {
 struct EncParams {
   const uint8_t* bprep;  // [M][B_BYTES]: hi+ext (256 x KE) then lo (256 x KP), fp16 K-major
   const float* cst;      // [M][CST_LEN]
+  const float* bch;      // [M][kMaxChunks] K-streamed kernel: max_j |B_j| over each 32-column chunk
   int64_t n;
   int m, ks;
   uint8_t* codes;
@@ -297,6 +298,62 @@ __device__ __forceinline__ void epilogue_row(const EncParams& p, int m, int64_t 
     // rigorous bound on |computed - exact| of any D_rj (see header)
     const float P = st.y * cb * 1.001f;  // >= sum |split products|
     const float E = (st.w != 0.f ? eps_main3 : eps_main2) * P + eps_ext * (P + cnm + st.x) * 1.001f  //
+                    + 4.76837158203125e-07f * P                                 // 4 * 2^-23: split, lo.lo
+                    + 2.98023223876953125e-08f * (sqrt_kp * st.y + s1c)          // 2^-25: subnormal lo parts
+                    + 9.313225746154785e-10f * (cnm + st.x)                      // 2^-30: extension parts
+                    + 1e-3f;
+    const bool cert = st.z != 0.f && (r_lo - w_hi) > 2.0f * E * 1.0001f;
+    if (cert) {
+      p.codes[n * p.stride + m] = (uint8_t)(16 * gi + qb);
+    } else {
+      atomicAdd(&p.counters[0], 1u);
+      const unsigned f = atomicAdd(&p.counters[2 + m], 1u);
+      if (f < p.flag_cap)
+        p.flags[(size_t)m * p.flag_cap + f] = (uint32_t)n;
+      else
+        p.counters[1] = 1u;
+    }
+  }
+}
+
+// Epilogue of the K-streamed kernel: two accumulators, H (hi . hi + extension, columns
+// [0, 256)) and L (hi . lo + lo . hi, columns [256, 512)), summed per column (one fp32
+// rounding) before the same partition minima and certificate.  st.w carries the row's
+// prefix bound W = sum over chunks c of the running sum of |x_c| max_j |B_j,c| (bounds
+// every max |addend| of H's two hi . hi instructions per chunk).
+__device__ __forceinline__ void epilogue_row_split(const EncParams& p, int m, int64_t n, uint32_t tacc,
+                                                   uint64_t* tempty2, float4 st, float eps_h, float eps_l,
+                                                   float eps_ext, float cb, float cnm, float s1c, float sqrt_kp,
+                                                   int lane) {
+  int cls[16];
+#pragma unroll
+  for (int q = 0; q < 16; ++q) cls[q] = 0x7fffffff;
+  int G1 = 0x7fffffff, G2 = 0x7fffffff, gi = 0;
+  uint32_t ka[32], kb[32];
+#pragma unroll 1
+  for (int c = 0; c < kN / kChunk; ++c) {
+    tmem_ld32(tacc + (uint32_t)(c * kChunk), ka);
+    tmem_ld32(tacc + (uint32_t)(kN + c * kChunk), kb);
+    tmem_wait32(ka);
+    tmem_wait32(kb);
+#pragma unroll
+    for (int j = 0; j < 32; ++j) ka[j] = __float_as_uint(__fadd_rn(__uint_as_float(ka[j]), __uint_as_float(kb[j])));
+    if (c + 1 == kN / kChunk / 2 || c + 1 == kN / kChunk) {  // a column half (of H and L) fully read
+      tc::fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty2[c + 1 == kN / kChunk ? 1 : 0]);
+    }
+    chunk_fold(ka, c, cls, G1, G2, gi);
+  }
+  if (n < p.n) {
+    int qb, Y;
+    class_best2(cls, p.keymask, p.one, qb, Y);
+    const int R = min(G2, Y);
+    const float w_hi = __int_as_float(G1), rv = __int_as_float(R);
+    const float r_lo = rv >= 0.f ? rv : rv * 1.00000762939453125f;
+    const float P = st.y * cb * 1.001f;
+    const float W = fminf(st.w, (float)(p.ks / 32) * P);  // every prefix (32-column chunks) is also <= P
+    const float E = eps_h * W + eps_l * P + eps_ext * (P + cnm + st.x) * 1.001f  //
                     + 4.76837158203125e-07f * P                                 // 4 * 2^-23: split, lo.lo
                     + 2.98023223876953125e-08f * (sqrt_kp * st.y + s1c)          // 2^-25: subnormal lo parts
                     + 9.313225746154785e-10f * (cnm + st.x)                      // 2^-30: extension parts
@@ -819,6 +876,7 @@ __global__ void __launch_bounds__(256) encode_exact_kernel(const float* __restri
 // accumulation bound scaled by the instruction count (ks / 16 per pass).
 // ===========================================================================
 constexpr int kKC = 32;
+constexpr int kMaxChunks = 32;  // ks <= 1024
 constexpr int kXSt = 3, kBSt = 3, kASt = 2;
 
 struct GeoK {
@@ -837,7 +895,8 @@ struct GeoK {
   static constexpr int OFF_STATS = OFF_AEXT + 2 * A_EXT;
   static constexpr int OFF_LO = OFF_STATS + 4 * kRows * 16;
   static constexpr int OFF_CST = OFF_LO + kASt * kTrWarps * 4;
-  static constexpr int OFF_BAR = OFF_CST + CST_LEN * 4;  // uint64 [32]
+  static constexpr int OFF_BCH = OFF_CST + CST_LEN * 4;   // float [kMaxChunks]
+  static constexpr int OFF_BAR = OFF_BCH + kMaxChunks * 4;  // uint64 [32]
   static constexpr int OFF_TBASE = OFF_BAR + 32 * 8;
   static constexpr int SMEM = OFF_TBASE + 16 + 1024;
   __host__ __device__ static size_t bprep_bytes(int ks) { return (size_t)(ks / kKC) * B_CHUNK + B_EXT; }
@@ -856,6 +915,7 @@ __global__ void __launch_bounds__(kThreads, 1) encode_tck_kernel(const __grid_co
   float4* s_stats = reinterpret_cast<float4*>(smem + G::OFF_STATS);
   int* s_lo = reinterpret_cast<int*>(smem + G::OFF_LO);
   float* s_cst = reinterpret_cast<float*>(smem + G::OFF_CST);
+  float* s_bch = reinterpret_cast<float*>(smem + G::OFF_BCH);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + G::OFF_BAR);
   uint64_t* xfull = bars;         // [3]
   uint64_t* xempty = bars + 3;    // [3]
@@ -903,9 +963,10 @@ __global__ void __launch_bounds__(kThreads, 1) encode_tck_kernel(const __grid_co
   tc::fence_after();
   const uint32_t tbase = *s_tbase;
   if (tid == 0) {
-    mbar_arrive_expect_tx(bload, (uint32_t)G::B_EXT + CST_LEN * 4);
+    mbar_arrive_expect_tx(bload, (uint32_t)G::B_EXT + CST_LEN * 4 + kMaxChunks * 4);
     bulk_g2s(sBext, bprep + (size_t)nk * G::B_CHUNK, G::B_EXT, bload);
     bulk_g2s(s_cst, p.cst + (size_t)m * CST_LEN, CST_LEN * 4, bload);
+    bulk_g2s(s_bch, p.bch + (size_t)m * kMaxChunks, kMaxChunks * 4, bload);
   }
   mbar_wait(bload, 0);
   const int nchunks = items * nk;
@@ -927,15 +988,18 @@ __global__ void __launch_bounds__(kThreads, 1) encode_tck_kernel(const __grid_co
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer ----------------
+    // One item in flight: accumulator H = TMEM columns [0, 256) takes hi . hi and the
+    // extension block, L = [256, 512) the lo passes, so that the lo passes' truncation
+    // errors scale with L's small magnitude, and H's with its running prefix.
     if (lane == 0) {
       const uint32_t idesc = tc::idesc_f16_f32(kRows, kN);
       constexpr uint32_t sboC = (uint32_t)(kKC / 8) * 128, sboE = (uint32_t)(kExt / 8) * 128;
+      const uint32_t tH = tbase, tL = tbase + (uint32_t)kN;
       for (int w = 0; w < items; ++w) {
         const int ab = w & 1;
-        const uint32_t ph = (uint32_t)((w >> 1) & 1);
-        mbar_wait_spin(&tempty[2 * ab], ph ^ 1u);
-        mbar_wait_spin(&tempty[2 * ab + 1], ph ^ 1u);
-        const uint32_t tacc = tbase + (uint32_t)ab * kN;
+        const uint32_t ph = (uint32_t)(w & 1);
+        mbar_wait_spin(&tempty[0], ph ^ 1u);
+        mbar_wait_spin(&tempty[1], ph ^ 1u);
         for (int c = 0; c < nk; ++c) {
           const int g = w * nk + c;
           const int as = g % kASt, bs = g % kBSt;
@@ -949,50 +1013,53 @@ __global__ void __launch_bounds__(kThreads, 1) encode_tck_kernel(const __grid_co
           const uint32_t b_hi = smem_u32(sB + bs * G::B_CHUNK), b_lo = b_hi + G::B_HI;
 #pragma unroll
           for (int s = 0; s < kKC / 16; ++s)
-            tc::mma_f16(tacc, tc::smem_desc(a_hi + s * 256, 128, sboC), tc::smem_desc(b_hi + s * 256, 128, sboC), idesc,
+            tc::mma_f16(tL, tc::smem_desc(a_hi + s * 256, 128, sboC), tc::smem_desc(b_lo + s * 256, 128, sboC), idesc,
                         (c > 0 || s > 0) ? 1u : 0u);
-#pragma unroll
-          for (int s = 0; s < kKC / 16; ++s)
-            tc::mma_f16(tacc, tc::smem_desc(a_hi + s * 256, 128, sboC), tc::smem_desc(b_lo + s * 256, 128, sboC), idesc,
-                        1u);
           if (lo_any) {
 #pragma unroll
             for (int s = 0; s < kKC / 16; ++s)
-              tc::mma_f16(tacc, tc::smem_desc(a_lo + s * 256, 128, sboC), tc::smem_desc(b_hi + s * 256, 128, sboC),
+              tc::mma_f16(tL, tc::smem_desc(a_lo + s * 256, 128, sboC), tc::smem_desc(b_hi + s * 256, 128, sboC),
                           idesc, 1u);
           }
+#pragma unroll
+          for (int s = 0; s < kKC / 16; ++s)
+            tc::mma_f16(tH, tc::smem_desc(a_hi + s * 256, 128, sboC), tc::smem_desc(b_hi + s * 256, 128, sboC), idesc,
+                        (c > 0 || s > 0) ? 1u : 0u);
           tc::commit(&aempty[as]);
           tc::commit(&bempty[bs]);
         }
-        mbar_wait_spin(&aefull[ab], ph);
+        mbar_wait_spin(&aefull[ab], (uint32_t)((w >> 1) & 1));
         tc::fence_after();
-        tc::mma_f16(tacc, tc::smem_desc(smem_u32(sAext + ab * G::A_EXT), 128, sboE),
+        tc::mma_f16(tH, tc::smem_desc(smem_u32(sAext + ab * G::A_EXT), 128, sboE),
                     tc::smem_desc(smem_u32(sBext), 128, sboE), idesc, 1u);
         tc::commit(&aeempty[ab]);
-        tc::commit(&tfull[2 * ab]);
-        tc::commit(&tfull[2 * ab + 1]);
+        tc::commit(&tfull[0]);
+        tc::commit(&tfull[1]);
       }
     }
   } else if (warp < 2 + kEpiWarps) {
-    // ---------------- epilogue warps ----------------
+    // ---------------- epilogue warps (one item at a time: warps 2-5) ----------------
     const int ew = warp - 2;
-    const int q = warp & 3, e = ew >> 2;
+    const int q = warp & 3;
     const int er = 32 * q + lane;
-    // accumulation bound of encode_tc_kernel with ks / 16 instructions per pass
-    const float eps_main2 = (float)(17 * 2 * (ks / 16)) * 1.1920928955078125e-07f;
-    const float eps_main3 = (float)(17 * 3 * (ks / 16)) * 1.1920928955078125e-07f;
-    const float eps_ext = 7.0f * 1.1920928955078125e-07f;
+    // H: two hi . hi instructions per chunk with max |addend| <= the row's running prefix
+    // (sum W over chunks, st.w); L: 4 nk instructions with addends <= 2^-9 P
+    // (|lo| <= 2^-11 |hi|); the H + L addition rounds once (2^-24, folded into eps_ext)
+    const float eps_h = 2.0f * 17.0f * (1.0f + 3.0f / 512.0f) * 1.1920928955078125e-07f;
+    const float eps_l = (float)(4 * 17 * nk) * (1.0f / 512.0f) * 1.1920928955078125e-07f;
+    const float eps_ext = 7.5f * 1.1920928955078125e-07f;
     const float cb = s_cst[CST_CB], cnm = s_cst[CST_CN], s1c = s_cst[CST_S1C];
     const float sqrt_ks = sqrtf((float)ks);
-    for (int w = e; w < items; w += 2) {
-      const int t = t0 + w * p.tstride;
-      const uint32_t ph = (uint32_t)((w >> 1) & 1);
-      mbar_wait(&tfull[2 * e], ph);
-      tc::fence_after();
-      const float4 st = s_stats[(w & 3) * kRows + er];
-      const uint32_t tacc = tbase + (uint32_t)e * kN + ((uint32_t)(32 * q) << 16);
-      epilogue_row(p, m, (int64_t)t * kRows + er, tacc, &tfull[2 * e], &tempty[2 * e], ph, st, eps_main2, eps_main3,
-                   eps_ext, cb, cnm, s1c, sqrt_ks, lane);
+    if (ew < 4) {
+      for (int w = 0; w < items; ++w) {
+        const int t = t0 + w * p.tstride;
+        mbar_wait(&tfull[0], (uint32_t)(w & 1));
+        tc::fence_after();
+        const float4 st = s_stats[(w & 3) * kRows + er];
+        const uint32_t tacc = tbase + ((uint32_t)(32 * q) << 16);
+        epilogue_row_split(p, m, (int64_t)t * kRows + er, tacc, tempty, st, eps_h, eps_l, eps_ext, cb, cnm, s1c,
+                           sqrt_ks, lane);
+      }
     }
   } else {
     // ---------------- transform warps: 16 rows each (2 passes of 8), 8 columns per lane ----------------
@@ -1003,6 +1070,7 @@ __global__ void __launch_bounds__(kThreads, 1) encode_tck_kernel(const __grid_co
     const bool valid = s_cst[CST_VALID] != 0.f;
     for (int w = 0; w < items; ++w) {
       float x2[2] = {0.f, 0.f};
+      float wpre[2] = {0.f, 0.f}, run[2] = {0.f, 0.f};  // prefix bound: sum_c sum_{c'<=c} |x_c'| B_c'
       uint32_t lo_row[2] = {0u, 0u};
       for (int c = 0; c < nk; ++c) {
         const int g = w * nk + c;
@@ -1030,6 +1098,7 @@ __global__ void __launch_bounds__(kThreads, 1) encode_tck_kernel(const __grid_co
 #pragma unroll
         for (int ps = 0; ps < 2; ++ps) {
           uint32_t lr = 0;
+          float ec = 0.f;
 #pragma unroll
           for (int j = 0; j < 8; j += 2) {
             const float a0 = v[ps][j] * sc, a1 = v[ps][j + 1] * sc;
@@ -1039,8 +1108,14 @@ __global__ void __launch_bounds__(kThreads, 1) encode_tck_kernel(const __grid_co
             hw[ps][j / 2] = *reinterpret_cast<const uint32_t*>(&hh);
             lw[ps][j / 2] = *reinterpret_cast<const uint32_t*>(&ll);
             lr |= lw[ps][j / 2];
-            x2[ps] = fmaf(a0, a0, fmaf(a1, a1, x2[ps]));
+            ec = fmaf(a0, a0, fmaf(a1, a1, ec));
           }
+          x2[ps] += ec;
+          // the row's chunk energy (4 lanes per row), its norm rounded up, times max_j |B_j,c|
+          ec += __shfl_xor_sync(0xffffffffu, ec, 8);
+          ec += __shfl_xor_sync(0xffffffffu, ec, 16);
+          run[ps] = fmaf(sqrtf(ec) * 1.000001f, s_bch[c], run[ps]);
+          wpre[ps] += run[ps];
           lr &= 0x7fff7fffu;
           lo_row[ps] |= lr;
           lo_nz |= lr;
@@ -1090,7 +1165,8 @@ __global__ void __launch_bounds__(kThreads, 1) encode_tck_kernel(const __grid_co
           *reinterpret_cast<uint4*>(ae + tc::kmajor_off(r, 8, kExt)) = make_uint4(0u, 0u, 0u, 0u);
           float xn;
           asm("sqrt.approx.f32 %0, %1;" : "=f"(xn) : "f"(x2u));
-          s_stats[(w & 3) * kRows + r] = make_float4(x2u, xn * 1.000002f, ok ? 1.f : 0.f, lr ? 1.f : 0.f);
+          // w: the prefix bound with the hi/lo split's (1 + 2^-11)^2 and fp32 sum slack
+          s_stats[(w & 3) * kRows + r] = make_float4(x2u, xn * 1.000002f, ok ? 1.f : 0.f, wpre[ps] * 1.002f);
         }
       }
       tc::fence_proxy_async();
@@ -1109,8 +1185,10 @@ __global__ void __launch_bounds__(kThreads, 1) encode_tck_kernel(const __grid_co
 // Codebook preparation for the K-streamed kernel: per subspace, B chunks [hi | lo] of 32
 // columns then the extension block (same values as encode_prep_kernel).
 __global__ void __launch_bounds__(256) encode_prep_k_kernel(const float* __restrict__ cw, int m, int l, int ks,
-                                                           uint8_t* __restrict__ bprep, float* __restrict__ cst) {
+                                                           uint8_t* __restrict__ bprep, float* __restrict__ cst,
+                                                           float* __restrict__ bch) {
   __shared__ float red[8], rb[8], rc[8], r1s[8];
+  __shared__ unsigned int s_bmax[kMaxChunks];
   __shared__ int bad[8];
   __shared__ double redd[8];
   __shared__ float s_sc;
@@ -1152,7 +1230,9 @@ __global__ void __launch_bounds__(256) encode_prep_k_kernel(const float* __restr
   const float sc = s_sc;
   const bool cb_ok = !s_bad;
   uint8_t* base = bprep + (size_t)mm * GeoK::bprep_bytes(ks);
-  double cn = 0.0, nb2 = 0.0, s1 = 0.0;
+  if (row < kMaxChunks) s_bmax[row] = 0u;
+  __syncthreads();
+  double cn = 0.0, nb2 = 0.0, s1 = 0.0, nbc = 0.0;
   for (int k = 0; k < ks; ++k) {
     const float cv = (real && cb_ok) ? c[k] * sc : 0.f;
     const float bv = -2.0f * cv;
@@ -1164,7 +1244,14 @@ __global__ void __launch_bounds__(256) encode_prep_k_kernel(const float* __restr
     cn += (double)cv * (double)cv;
     nb2 += (double)bv * (double)bv;
     s1 += fabs((double)bv);
+    nbc += (double)bv * (double)bv;
+    if (k % kKC == kKC - 1) {  // chunk norm, rounded up (non-negative floats order as uint)
+      atomicMax(&s_bmax[k / kKC], __float_as_uint((float)sqrt(nbc) * 1.0001f));
+      nbc = 0.0;
+    }
   }
+  __syncthreads();
+  if (row < ks / kKC) bch[(size_t)mm * kMaxChunks + row] = __uint_as_float(s_bmax[row]);
   double cmx = cn;
   for (int o = 16; o > 0; o >>= 1) cmx = fmax(cmx, __shfl_xor_sync(0xffffffffu, cmx, o));
   if (lane == 0) redd[warp] = cmx;
@@ -1431,8 +1518,9 @@ int launch_encode_tck(const float* d_x, int64_t n, int d, const float* d_cw, int
   EncWS& ws = enc_workspace(stream);
   const size_t b_bytes = (size_t)m * G::bprep_bytes(ks);
   const uint32_t cap = (uint32_t)std::min<int64_t>(n, n / 4 + 4096);  // flagged rows per subspace
+  const size_t bch_bytes = align_up((size_t)m * kMaxChunks * 4, 256);
   const size_t need = align_up(b_bytes, 256) + align_up((size_t)m * CST_LEN * 4, 256) +
-                      align_up((size_t)m * cap * 4, 256) + align_up((size_t)(m + 2) * 4, 256);
+                      align_up((size_t)m * cap * 4, 256) + align_up((size_t)(m + 2) * 4, 256) + bch_bytes;
   if (ws.bytes < need) {
     if (ws.p) cudaFree(ws.p);
     ws.p = nullptr;
@@ -1446,6 +1534,7 @@ int launch_encode_tck(const float* d_x, int64_t n, int d, const float* d_cw, int
   uint32_t* flags = reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(cst) + align_up((size_t)m * CST_LEN * 4, 256));
   unsigned int* counters =
       reinterpret_cast<unsigned int*>(reinterpret_cast<char*>(flags) + align_up((size_t)m * cap * 4, 256));
+  float* bch = reinterpret_cast<float*>(reinterpret_cast<char*>(counters) + align_up((size_t)(m + 2) * 4, 256));
 
   CUtensorMap map;
   auto encoder = tensor_map_encoder();
@@ -1460,11 +1549,12 @@ int launch_encode_tck(const float* d_x, int64_t n, int d, const float* d_cw, int
   if (cr != CUDA_SUCCESS) return fail(PQK_ECUDA, "cuTensorMapEncodeTiled failed");
 
   PQK_CUDA_TRY(cudaMemsetAsync(counters, 0, (size_t)(m + 2) * 4, stream));
-  encode_prep_k_kernel<<<m, 256, 0, stream>>>(d_cw, m, l, ks, bprep, cst);
+  encode_prep_k_kernel<<<m, 256, 0, stream>>>(d_cw, m, l, ks, bprep, cst, bch);
   PQK_LAUNCH_CHECK("encode_prep_k_kernel");
   EncParams ep{};
   ep.bprep = bprep;
   ep.cst = cst;
+  ep.bch = bch;
   ep.n = n;
   ep.m = m;
   ep.ks = ks;

@@ -54,7 +54,7 @@ typedef enum {
 /* Stats slots written by the device entry points (int64 array of PQK_STATS_LEN). */
 enum {
   PQK_STAT_UNIQUE_CENTERS = 0, /* distinct center codes after dedup                 */
-  PQK_STAT_FLAGGED = 1,        /* codes whose fp32 winner was not certified (fp64 rescan) */
+  PQK_STAT_FLAGGED = 1,        /* codes the first-tier scan did not certify          */
   PQK_STAT_NNZ_TOTAL = 2,      /* sum of histogram support sizes over filled (k,m)  */
   PQK_STAT_EMPTY = 3,          /* empty clusters repaired                           */
   PQK_STAT_FILLED = 4,         /* clusters with >=1 member                          */
@@ -62,6 +62,8 @@ enum {
   PQK_STAT_ENCODE_FLAGGED = 6, /* encoder (vector,m) pairs recomputed in fp64       */
   PQK_STAT_NCHUNKS = 7,        /* center chunks streamed by the assignment scan     */
   PQK_STAT_VOTE_FP64 = 8,      /* (k,m) votes not certified by the fp32 filter      */
+  PQK_STAT_FLAGGED_FP64 = 9,   /* codes decided by the exact fp64 rescan            */
+  PQK_STAT_LOOKUP_BYTES = 10,  /* bytes per table lookup of the first-tier scan (2 or 4) */
   PQK_STATS_LEN = 24           /* slots 0..15 public, 16..23 scratch accumulators   */
 };
 
@@ -101,6 +103,15 @@ int pqk_pad_codes_device(const uint8_t* d_raw, int64_t n, int32_t m, uint8_t* d_
  * in float64 ascending-m order with lowest index on ties, and sd_sq[n] the float64
  * distance to that center, bit-identical to the reference. */
 size_t pqk_assign_workspace_bytes(int64_t n, int64_t k, int32_t m, int32_t l);
+/* Scan tiers of pqk_assign_device.  Mode 0 (default): a 16-bit fixed-point first tier
+ * (2-byte table lookups, exact integer sums, certified against the quantisation error)
+ * for padded M <= 16 and problems of >= 2^31 lookups, then the fp32 scan over the
+ * uncertified list when it is long (>= 1024 codes per SM) and the exact fp64 rescan for
+ * the rest.  Mode 1: the fp32 scan first.  Mode 2: the 16-bit tier at any size.  Mode
+ * 3: as 2 with the fp32 list tier for any list length.  Labels and sd_sq are identical
+ * in every mode (process-wide setting, for A/B measurement and tests). */
+int pqk_set_scan_mode(int32_t mode);
+int32_t pqk_get_scan_mode(void);
 int pqk_assign_device(const uint8_t* d_codes, int64_t n, int32_t m, int32_t l,
                       const uint8_t* d_centers, int64_t k,
                       const double* d_t64, const float* d_t32, int32_t fp64_only,

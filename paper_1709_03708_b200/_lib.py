@@ -20,6 +20,8 @@ PQK_OK, PQK_EINVAL, PQK_ECUDA, PQK_ENOMEM, PQK_EUNSUPPORTED = range(5)
 
 STAT_UNIQUE_CENTERS = 0
 STAT_FLAGGED = 1
+STAT_FLAGGED_FP64 = 9
+STAT_LOOKUP_BYTES = 10
 STAT_NNZ_TOTAL = 2
 STAT_EMPTY = 3
 STAT_FILLED = 4
@@ -40,6 +42,8 @@ SIGNATURES: dict[str, tuple] = {
     "pqk_last_error": (C.c_char_p, []),
     "pqk_device_info": (C.c_int, [_i32, C.POINTER(_i32), C.POINTER(_i32)]),
     "pqk_padded_m": (_i32, [_i32]),
+    "pqk_set_scan_mode": (C.c_int, [_i32]),
+    "pqk_get_scan_mode": (_i32, []),
     "pqk_launch_count": (_i64, []),
     "pqk_set_profile_events": (C.c_int, [_p, _p]),
     "pqk_table_scale": (C.c_int, [_p, _i64, C.POINTER(_i32), C.POINTER(_i32)]),

@@ -39,6 +39,7 @@
 #include <cstdio>
 
 #include "pqk_common.cuh"
+#include "pqk_hscan.cuh"
 
 namespace pqk {
 
@@ -204,6 +205,12 @@ struct ScanParams {
   int32_t* flag_count;
   int64_t pass_size;
   int64_t npasses;
+  // list mode (second filter tier): scan the codes list[0 .. *list_count), but only when
+  // *list_count >= list_min (smaller lists go to the exact rescan); pass sizes derived
+  // on the device so the launch needs no host sync
+  const int32_t* list;
+  const int32_t* list_count;
+  int32_t list_min;
 };
 
 template <int W>
@@ -260,7 +267,20 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) scan_kernel(const ScanParams
   const int nchunks = p.counters[2];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t G = gridDim.x;
-  const int64_t my_passes = (p.npasses > blockIdx.x) ? (p.npasses - blockIdx.x + G - 1) / G : 0;
+  int n;
+  int pass_size;
+  int64_t npasses;
+  if (p.list) {
+    n = *p.list_count;
+    if (n < p.list_min || n == 0) return;
+    pass_size = (int)min((int64_t)OWN * C, ((int64_t)n + G - 1) / G);
+    npasses = ((int64_t)n + pass_size - 1) / pass_size;
+  } else {
+    n = (int)p.n;
+    pass_size = (int)p.pass_size;
+    npasses = p.npasses;
+  }
+  const int64_t my_passes = (npasses > blockIdx.x) ? (npasses - blockIdx.x + G - 1) / G : 0;
 
   if (threadIdx.x == 0) {
 #pragma unroll
@@ -298,8 +318,6 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) scan_kernel(const ScanParams
 #pragma unroll
   for (int i = 0; i < MP; ++i) lc[i] = (uint32_t)(((c + i) % MP) * (KC * 4) + h * 16);
   const uint32_t stage0 = smem_u32(stages);
-  const int n = (int)p.n;
-  const int pass_size = (int)p.pass_size;
 
   uint32_t g = 0;
   for (int pi = 0; pi < (int)my_passes; ++pi) {
@@ -309,10 +327,13 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) scan_kernel(const ScanParams
 
     uint32_t cw[C][W];
     uint32_t bk[C], sk[C], bc[C];
+    int rid[C];  // code row (list mode: list[position])
 #pragma unroll
     for (int j = 0; j < C; ++j) {
-      const int idx = my0 + j * OWN;
-      load_rotated<W>(p.codes, idx, idx < end, c, cw[j]);
+      const int pos = my0 + j * OWN;
+      const int idx = (p.list && pos < end) ? __ldg(&p.list[pos]) : pos;
+      rid[j] = idx;
+      load_rotated<W>(p.codes, idx, pos < end, c, cw[j]);
       bk[j] = 0xffffffffu;
       sk[j] = 0xffffffffu;
       bc[j] = 0u;
@@ -383,8 +404,8 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) scan_kernel(const ScanParams
         }
         s = ns;
       }
-      const int idx = my0 + j * OWN;
-      if (h == 0 && idx < end) {
+      const int idx = rid[j];
+      if (h == 0 && my0 + j * OWN < end) {
         const uint32_t sm = s & ~3u;
         bool cert;
         if (sm >= 0x7f800000u) {
@@ -417,11 +438,13 @@ __global__ void rescan_kernel(const uint8_t* __restrict__ codes, int64_t n, int 
                               const uint8_t* __restrict__ ucodes, const int32_t* __restrict__ counters,
                               const int32_t* __restrict__ flags, const int32_t* __restrict__ flag_count,
                               const int32_t* __restrict__ pos2idx, const double* __restrict__ t64,
-                              uint32_t* __restrict__ labels, double* __restrict__ sd_sq, int all_mode) {
+                              uint32_t* __restrict__ labels, double* __restrict__ sd_sq, int all_mode,
+                              int32_t max_count) {
   const int lane = threadIdx.x & 31;
   const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t nf = all_mode ? n : (int64_t)(*flag_count);
+  if (!all_mode && nf >= max_count) return;  // the list went to the fp32 list scan
   const int U = counters[0];
   for (int64_t w = gw; w < nf; w += nw) {
     const int64_t idx = all_mode ? w : (int64_t)flags[w];
@@ -459,11 +482,12 @@ __global__ void __launch_bounds__(256) rescan_cta_kernel(
     const uint8_t* __restrict__ codes, int64_t n, int mp, int m, int l, const uint8_t* __restrict__ ucodes,
     const int32_t* __restrict__ counters, const int32_t* __restrict__ flags, const int32_t* __restrict__ flag_count,
     const int32_t* __restrict__ pos2idx, const double* __restrict__ t64, uint32_t* __restrict__ labels,
-    double* __restrict__ sd_sq, int all_mode) {
+    double* __restrict__ sd_sq, int all_mode, int32_t max_count) {
   extern __shared__ double s_rows[];  // m * l
   __shared__ double s_best[8];
   __shared__ int s_bu[8];
   const int64_t nf = all_mode ? n : (int64_t)(*flag_count);
+  if (!all_mode && nf >= max_count) return;  // the list went to the fp32 list scan
   const int U = counters[0];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int64_t f = blockIdx.x; f < nf; f += gridDim.x) {
@@ -513,10 +537,14 @@ __global__ void __launch_bounds__(256) rescan_cta_kernel(
 }
 
 // first window sets the statistics, later windows add their flagged codes
-__global__ void assign_stats_kernel(const int32_t* __restrict__ counters, int64_t* __restrict__ stats, int first) {
+// kc16 > 0: the 16-bit first tier ran (chunks of kc16 centres, 2-byte lookups)
+__global__ void assign_stats_kernel(const int32_t* __restrict__ counters, int64_t* __restrict__ stats, int first,
+                                    int kc16) {
   stats[PQK_STAT_UNIQUE_CENTERS] = counters[0];
   stats[PQK_STAT_FLAGGED] = (first ? 0 : stats[PQK_STAT_FLAGGED]) + counters[1];
-  stats[PQK_STAT_NCHUNKS] = counters[2];
+  stats[PQK_STAT_FLAGGED_FP64] = (first ? 0 : stats[PQK_STAT_FLAGGED_FP64]) + (kc16 ? counters[3] : counters[1]);
+  stats[PQK_STAT_NCHUNKS] = kc16 ? (counters[0] + kc16 - 1) / kc16 : counters[2];
+  stats[PQK_STAT_LOOKUP_BYTES] = kc16 ? 2 : 4;
 }
 
 __global__ void paired_distance_kernel(const uint8_t* __restrict__ a, const uint8_t* __restrict__ b,
@@ -558,6 +586,11 @@ struct AssignWS {
   int32_t* counters;
   uint32_t hash_size;
   size_t total;
+  // 16-bit fixed-point first tier
+  h16::Scale* scale;
+  uint16_t* t16;
+  uint4* q16;
+  int32_t* flags2;
 };
 
 // Rows per scan window: the scan and the flag list index rows of a window in 32 bits;
@@ -587,6 +620,13 @@ static AssignWS assign_ws_layout(void* base, int64_t n, int64_t k, int mp, int l
   const size_t o_uc = take((size_t)k * mp, 256);
   const size_t o_q = take((size_t)nchunks_max * l * mp * kc * sizeof(float), 1024);
   const size_t o_fl = take((size_t)std::max<int64_t>(std::min(n, kScanWindow), 1) * sizeof(int32_t), 256);
+  const int kc16 = h16::kcFor(mp);
+  const bool h16_ok = mp <= 16;
+  const size_t o_sc = take(sizeof(h16::Scale), 256);
+  const size_t o_t16 = take(h16_ok ? (size_t)mp * l * l * sizeof(uint16_t) : 0, 256);
+  const size_t o_q16 = take(h16_ok ? (size_t)((k + kc16 - 1) / kc16) * l * mp * kc16 * sizeof(uint16_t) : 0, 1024);
+  const size_t o_fl2 =
+      take(h16_ok ? (size_t)std::max<int64_t>(std::min(n, kScanWindow), 1) * sizeof(int32_t) : 0, 256);
   w.total = align_up(off, 256);
   char* b = static_cast<char*>(base);
   if (b) {
@@ -598,6 +638,10 @@ static AssignWS assign_ws_layout(void* base, int64_t n, int64_t k, int mp, int l
     w.ucodes = reinterpret_cast<uint8_t*>(b + o_uc);
     w.q = reinterpret_cast<float*>(b + o_q);
     w.flags = reinterpret_cast<int32_t*>(b + o_fl);
+    w.scale = reinterpret_cast<h16::Scale*>(b + o_sc);
+    w.t16 = reinterpret_cast<uint16_t*>(b + o_t16);
+    w.q16 = reinterpret_cast<uint4*>(b + o_q16);
+    w.flags2 = reinterpret_cast<int32_t*>(b + o_fl2);
   }
   return w;
 }
@@ -607,16 +651,17 @@ static int launch_scan_c(int c_need, const ScanParams& p, int grid, int l, cudaS
   if constexpr (sizeof...(Cs) > 0) {
     if (c_need > C) return launch_scan_c<MP, KC, NW, S, Cs...>(c_need, p, grid, l, stream);
   }
+  const bool prof = p.list == nullptr;  // bench events bracket the first-tier scan only
   const DevInfo& di = dev_info();
   const size_t smem = 128 + (size_t)S * l * MP * KC * 4;
   if ((int)smem > di.smem_optin) return fail(PQK_EUNSUPPORTED, "assignment chunk ring exceeds shared memory");
   auto kern = scan_kernel<MP, KC, C, NW, S>;
   PQK_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   ProfileEvents& pe = profile_events();
-  if (pe.before) PQK_CUDA_TRY(record_profile_event(pe.before, stream));
+  if (prof && pe.before) PQK_CUDA_TRY(record_profile_event(pe.before, stream));
   kern<<<grid, (NW + 1) * 32, smem, stream>>>(p);
   PQK_LAUNCH_CHECK("scan_kernel");
-  if (pe.after) PQK_CUDA_TRY(record_profile_event(pe.after, stream));
+  if (prof && pe.after) PQK_CUDA_TRY(record_profile_event(pe.after, stream));
   return PQK_OK;
 }
 
@@ -649,11 +694,77 @@ static int launch_scan(const ScanParams& base_params, int l, cudaStream_t stream
   return launch_scan_c<MP, KC, NW, S, Cs...>(c_need, p, grid, l, stream);
 }
 
+// Second tier: the fp32 scan over a device-side list (runs only when the list holds at
+// least list_min codes; pass sizes derived on the device).  Largest register variant.
+template <int MP, int KC, int NW, int S, int... Cs>
+static int launch_scan_list(const ScanParams& p, int l, cudaStream_t stream) {
+  constexpr int CMAX = std::max({Cs...});
+  return launch_scan_c<MP, KC, NW, S, Cs...>(CMAX, p, dev_info().sms, l, stream);
+}
+
+// ---------------------------------------------------------------------------
+// 16-bit first tier (pqk_hscan.cuh)
+template <int MP, int KC, int NW, int S, int C, int... Cs>
+static int launch_hscan_c(int c_need, const h16::HScanParams& p, int grid, int l, cudaStream_t stream) {
+  if constexpr (sizeof...(Cs) > 0) {
+    if (c_need > C) return launch_hscan_c<MP, KC, NW, S, Cs...>(c_need, p, grid, l, stream);
+  }
+  const DevInfo& di = dev_info();
+  const size_t smem = 128 + (size_t)S * 256 * MP * KC * 2;  // ring stride: 256 rows (immediate offsets)
+  if ((int)smem > di.smem_optin) return fail(PQK_EUNSUPPORTED, "assignment chunk ring exceeds shared memory");
+  auto kern = h16::hscan_kernel<MP, KC, C, NW, S>;
+  PQK_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  ProfileEvents& pe = profile_events();
+  if (pe.before) PQK_CUDA_TRY(record_profile_event(pe.before, stream));
+  kern<<<grid, (NW + 1) * 32, smem, stream>>>(p);
+  PQK_LAUNCH_CHECK("hscan_kernel");
+  if (pe.after) PQK_CUDA_TRY(record_profile_event(pe.after, stream));
+  return PQK_OK;
+}
+
+template <int MP, int KC, int NW, int S, int... Cs>
+static int launch_hscan(const h16::HScanParams& base_params, int l, cudaStream_t stream) {
+  constexpr int H = KC / 8;
+  constexpr int OWN = NW * (32 / H);
+  constexpr int CMAX = std::max({Cs...});
+  constexpr int NB = OWN * CMAX;
+  const DevInfo& di = dev_info();
+  h16::HScanParams p = base_params;
+  const int64_t n = p.n;
+  const int64_t G = di.sms;
+  const int64_t per_cta = std::max<int64_t>(1, (n + G * NB - 1) / (G * NB));
+  int64_t npasses = G * per_cta;
+  int64_t pass_size = (n + npasses - 1) / npasses;
+  const int64_t min_pass = std::max<int64_t>(1, NB / 4);
+  if (pass_size < min_pass) {
+    pass_size = min_pass;
+    npasses = (n + pass_size - 1) / pass_size;
+  }
+  p.pass_size = pass_size;
+  p.npasses = npasses;
+  const int grid = (int)std::min<int64_t>(G, npasses);
+  if (grid <= 0) return PQK_OK;
+  const int c_need = (int)((pass_size + OWN - 1) / OWN);
+  return launch_hscan_c<MP, KC, NW, S, Cs...>(c_need, p, grid, l, stream);
+}
+
+// 0: 16-bit first tier where it pays off (default); 1: fp32 scan only; 2: 16-bit first tier
+// whenever supported; 3: as 2, and the fp32 list tier for any list length (tests)
+static int g_scan_mode = 0;
+
 }  // namespace pqk
 
 using namespace pqk;
 
 extern "C" int32_t pqk_padded_m(int32_t m) { return padded_m(m); }
+
+extern "C" int pqk_set_scan_mode(int32_t mode) {
+  if (mode < 0 || mode > 3) return fail(PQK_EINVAL, "pqk_set_scan_mode: mode must be in [0, 3]");
+  g_scan_mode = mode;
+  return PQK_OK;
+}
+
+extern "C" int32_t pqk_get_scan_mode(void) { return g_scan_mode; }
 
 extern "C" int pqk_tables_to_f32(const double* d_t64, int32_t m, int32_t l, int32_t exp2, float* d_t32,
                                  void* stream) {
@@ -696,6 +807,11 @@ extern "C" int pqk_assign_device(const uint8_t* d_codes, int64_t n, int32_t m, i
   if (!d_codes || !d_centers || !d_t64 || !d_labels || !d_sd_sq || !d_ws)
     return fail(PQK_EINVAL, "pqk_assign_device: null pointer");
   const bool fast = !fp64_only && mp <= 32 && d_t32 != nullptr;
+  const int kc16 = h16::kcFor(mp);
+  // the 16-bit tier pays off above ~2^31 lookups (its per-call table preparation and
+  // finalisation cost tens of microseconds); smaller problems run the fp32 scan
+  const bool use16 = fast && g_scan_mode != 1 && mp <= 16 && (k + kc16 - 1) / kc16 <= 65535 &&
+                     (g_scan_mode >= 2 || (double)n * (double)k * (double)m >= 2147483648.0);
   AssignWS w = assign_ws_layout(d_ws, n, k, mp, l);
   if (ws_bytes < w.total) return fail(PQK_EINVAL, "pqk_assign_device: workspace too small");
 
@@ -725,6 +841,44 @@ extern "C" int pqk_assign_device(const uint8_t* d_codes, int64_t n, int32_t m, i
     }
     PQK_LAUNCH_CHECK("qbuild_kernel");
   }
+  if (use16) {
+    // 16-bit fixed-point tables (scale from the table maximum) and their chunks
+    const int qmax = h16::qmax_for(m);
+    PQK_CUDA_TRY(cudaMemsetAsync(w.scale, 0, sizeof(h16::Scale), stream));
+    const int64_t cnt = (int64_t)m * l * l;
+    h16::table_max_kernel<<<(int)std::min<int64_t>((cnt + 255) / 256, (int64_t)di.sms * 4), 256, 0, stream>>>(
+        d_t64, cnt, w.scale);
+    PQK_LAUNCH_CHECK("table_max_kernel");
+    {
+      static bool attr16[64] = {};
+      int dev = 0;
+      cudaGetDevice(&dev);
+      if (!attr16[dev & 63]) {
+        PQK_CUDA_TRY(cudaFuncSetAttribute(h16::scale_sample_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          96 * 1024));
+        attr16[dev & 63] = true;
+      }
+      h16::scale_sample_kernel<<<h16::kScaleSample, 256, (size_t)m * l * sizeof(double), stream>>>(
+          d_codes, n, mp, m, l, w.ucodes, w.counters, d_t64, w.scale);
+      PQK_LAUNCH_CHECK("scale_sample_kernel");
+    }
+    const int64_t cntp = (int64_t)mp * l * l;
+    h16::table_quantize_kernel<<<(int)std::min<int64_t>((cntp + 255) / 256, (int64_t)di.sms * 8), 256, 0,
+                                 stream>>>(d_t64, m, l, mp, qmax, w.scale, w.t16);
+    PQK_LAUNCH_CHECK("table_quantize_kernel");
+    const int64_t units = ((k + kc16 - 1) / kc16) * l * mp * (kc16 / 8);
+    const int qgrid = (int)std::min<int64_t>((units + 255) / 256, (int64_t)di.sms * 16);
+    switch (mp) {
+      case 4: h16::qbuild16_kernel<4, 16><<<qgrid, 256, 0, stream>>>(w.t16, l, m, qmax, w.ucodes, w.counters, w.q16); break;
+      case 8: h16::qbuild16_kernel<8, 8><<<qgrid, 256, 0, stream>>>(w.t16, l, m, qmax, w.ucodes, w.counters, w.q16); break;
+      case 16: h16::qbuild16_kernel<16, 8><<<qgrid, 256, 0, stream>>>(w.t16, l, m, qmax, w.ucodes, w.counters, w.q16); break;
+    }
+    PQK_LAUNCH_CHECK("qbuild16_kernel");
+  }
+  // list tier threshold: below it the exact rescan is cheaper than streaming every chunk
+  // (fp32 list scan: every CTA streams all chunks, so it only beats the exact rescan,
+  // whose cost is per code, for lists of ~1000 codes per SM and more)
+  const int32_t list_min = g_scan_mode == 3 ? 0 : di.sms * 1024;
   const size_t rows_bytes = (size_t)m * l * sizeof(double);
   const bool cta_rescan = rows_bytes <= 96 * 1024;
   if (cta_rescan) {
@@ -742,6 +896,71 @@ extern "C" int pqk_assign_device(const uint8_t* d_codes, int64_t n, int32_t m, i
     uint32_t* labels = d_labels + w0;
     double* sd_sq = d_sd_sq + w0;
     if (w0 > 0) PQK_CUDA_TRY(cudaMemsetAsync(w.counters + 1, 0, sizeof(int32_t), stream));
+    if (w0 > 0) PQK_CUDA_TRY(cudaMemsetAsync(w.counters + 3, 0, sizeof(int32_t), stream));
+    if (use16) {
+      // 3a. 16-bit first tier over every code
+      h16::HScanParams hp{};
+      hp.codes = codes;
+      hp.n = wn;
+      hp.q = w.q16;
+      hp.l = l;
+      hp.m = m;
+      hp.counters = w.counters;
+      hp.pos2idx = w.pos2idx;
+      hp.ucodes = w.ucodes;
+      hp.t64 = d_t64;
+      hp.sc = w.scale;
+      hp.labels = labels;
+      hp.sd_sq = sd_sq;
+      hp.flags = w.flags;
+      hp.flag_count = w.counters + 1;
+      int rc = PQK_OK;
+      switch (mp) {
+        case 4: rc = launch_hscan<4, 16, 11, 4, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15, 16>(hp, l, stream); break;
+        case 8: rc = launch_hscan<8, 8, 11, 4, 1, 2, 3, 4, 5, 6, 7, 8>(hp, l, stream); break;
+        case 16: rc = launch_hscan<16, 8, 11, 3, 1, 2, 3, 4>(hp, l, stream); break;
+      }
+      if (rc != PQK_OK) return rc;
+      // 3b. fp32 tier over the uncertified list when it is long
+      ScanParams sp{};
+      sp.codes = codes;
+      sp.n = 0;
+      sp.q = w.q;
+      sp.l = l;
+      sp.m = m;
+      sp.counters = w.counters;
+      sp.pos2idx = w.pos2idx;
+      sp.ucodes = w.ucodes;
+      sp.t64 = d_t64;
+      sp.cert_factor = 1.0 + 4.0 * (2.0 * m) * ldexp(1.0, -24);
+      sp.labels = labels;
+      sp.sd_sq = sd_sq;
+      sp.flags = w.flags2;
+      sp.flag_count = w.counters + 3;
+      sp.list = w.flags;
+      sp.list_count = w.counters + 1;
+      sp.list_min = list_min;
+      switch (mp) {
+        case 4: rc = launch_scan_list<4, 8, 11, 4, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14>(sp, l, stream); break;
+        case 8: rc = launch_scan_list<8, 4, 11, 4, 1, 2, 3, 4, 5, 6, 7, 8>(sp, l, stream); break;
+        case 16: rc = launch_scan_list<16, 4, 11, 3, 1, 2, 3, 4>(sp, l, stream); break;
+      }
+      if (rc != PQK_OK) return rc;
+      // 4. exact rescans: the short first-tier list, then what the fp32 tier left
+      rescan_cta_kernel<<<di.sms * 2, 256, rows_bytes, stream>>>(codes, wn, mp, m, l, w.ucodes, w.counters, w.flags,
+                                                                w.counters + 1, w.pos2idx, d_t64, labels, sd_sq, 0,
+                                                                list_min);
+      PQK_LAUNCH_CHECK("rescan_cta_kernel");
+      rescan_cta_kernel<<<di.sms * 2, 256, rows_bytes, stream>>>(codes, wn, mp, m, l, w.ucodes, w.counters,
+                                                                w.flags2, w.counters + 3, w.pos2idx, d_t64, labels,
+                                                                sd_sq, 0, 0x7fffffff);
+      PQK_LAUNCH_CHECK("rescan_cta_kernel");
+      if (d_stats) {
+        assign_stats_kernel<<<1, 1, 0, stream>>>(w.counters, d_stats, w0 == 0, kc16);
+        PQK_LAUNCH_CHECK("assign_stats_kernel");
+      }
+      continue;
+    }
     if (fast) {
       // 3. scan
       ScanParams sp{};
@@ -773,17 +992,17 @@ extern "C" int pqk_assign_device(const uint8_t* d_codes, int64_t n, int32_t m, i
       const int grid = (int)std::min<int64_t>(fast ? (int64_t)di.sms * 2 : wn, (int64_t)di.sms * 8);
       rescan_cta_kernel<<<std::max(grid, 1), 256, rows_bytes, stream>>>(
           codes, wn, mp, m, l, w.ucodes, w.counters, w.flags, w.counters + 1, w.pos2idx, d_t64, labels, sd_sq,
-          fast ? 0 : 1);
+          fast ? 0 : 1, 0x7fffffff);
       PQK_LAUNCH_CHECK("rescan_cta_kernel");
     } else {
       const int64_t warps = fast ? (int64_t)di.sms * 32 : std::min<int64_t>(wn, (int64_t)di.sms * 64);
       const int grid = (int)std::max<int64_t>(1, (warps * 32 + 255) / 256);
       rescan_kernel<<<grid, 256, 0, stream>>>(codes, wn, mp, m, l, w.ucodes, w.counters, w.flags, w.counters + 1,
-                                              w.pos2idx, d_t64, labels, sd_sq, fast ? 0 : 1);
+                                              w.pos2idx, d_t64, labels, sd_sq, fast ? 0 : 1, 0x7fffffff);
       PQK_LAUNCH_CHECK("rescan_kernel");
     }
     if (d_stats) {
-      assign_stats_kernel<<<1, 1, 0, stream>>>(w.counters, d_stats, w0 == 0);
+      assign_stats_kernel<<<1, 1, 0, stream>>>(w.counters, d_stats, w0 == 0, 0);
       PQK_LAUNCH_CHECK("assign_stats_kernel");
     }
   }

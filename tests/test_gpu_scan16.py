@@ -1,0 +1,126 @@
+"""GPU parity of the 16-bit fixed-point first tier of the assignment (pqk_hscan.cuh).
+
+The default mode engages the 16-bit tier only above 2^31 lookups, so the small cases
+below force it (scan mode 2) and also force the fp32 list tier for any list length
+(mode 3), then compare labels and sd_sq byte for byte with the oracle's linear scan
+(clustering.py:167-197: float64, ascending m, lowest index on ties) and with the fp32
+path (mode 1).  Cases: random tables at every supported width, lattice tables with
+massive exact ties, duplicated centres, tables spanning huge scales (saturated
+entries), clustered codes, partial last chunks, a fit, and a multi-pass size.
+"""
+
+import numpy as np
+import pytest
+
+from helpers import lattice_tables, mixture_codes, random_tables
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_1709_03708_b200 import _lib
+
+    lib = _lib.load()
+    yield lib
+    _lib.check(lib.pqk_set_scan_mode(0), "scan mode")
+
+
+def _assign(lib, mode, codes, centers, tables):
+    from paper_1709_03708_b200 import _lib, engine
+
+    _lib.check(lib.pqk_set_scan_mode(mode), "scan mode")
+    try:
+        return engine.assign_host(codes, centers, tables, want_sd=True)
+    finally:
+        _lib.check(lib.pqk_set_scan_mode(0), "scan mode")
+
+
+def _check(lib, oracle, codes, centers, tables, modes=(2, 3)):
+    expect = oracle.assign_c(codes, centers, tables)
+    exp_sd = oracle.paired_distance_sq(tables, codes.astype(np.int64), centers[expect].astype(np.int64))
+    for mode in modes:
+        labels, sd = _assign(lib, mode, codes, centers, tables)
+        np.testing.assert_array_equal(labels, expect, err_msg=f"mode {mode}")
+        assert sd.tobytes() == exp_sd.tobytes(), f"mode {mode}"
+
+
+def test_scan_mode_abi(lib):
+    from paper_1709_03708_b200 import _lib
+
+    assert lib.pqk_get_scan_mode() == 0
+    assert lib.pqk_set_scan_mode(7) == _lib.PQK_EINVAL
+    assert lib.pqk_get_scan_mode() == 0
+
+
+@pytest.mark.parametrize("m", [1, 2, 3, 4, 5, 8, 12, 16])
+@pytest.mark.parametrize("l_count", [4, 256])
+def test_random_tables_widths(lib, oracle, m, l_count):
+    rng = np.random.default_rng(77 * m + l_count)
+    tables = random_tables(m, l_count, seed=3 * m + l_count)
+    codes = rng.integers(0, l_count, size=(3000, m)).astype(np.uint8)
+    centers = rng.integers(0, l_count, size=(203, m)).astype(np.uint8)  # partial last chunk
+    _check(lib, oracle, codes, centers, tables)
+
+
+@pytest.mark.parametrize("trial", range(6))
+def test_lattice_ties_duplicates(lib, oracle, trial):
+    rng = np.random.default_rng(9100 + trial)
+    m = int(rng.choice([1, 2, 4, 8]))
+    tables = lattice_tables(m, 16)
+    codes = rng.integers(0, 16, size=(4000, m)).astype(np.uint8)
+    centers = codes[rng.integers(0, 4000, size=150)].copy()
+    centers[rng.integers(0, 150, size=50)] = centers[3]
+    _check(lib, oracle, codes, centers, tables)
+
+
+@pytest.mark.parametrize("span", [1e-30, 1e6, 1e30])
+def test_wide_dynamic_range(lib, oracle, span):
+    """Tables mixing tiny and huge distances: most entries saturate or round to 0."""
+    rng = np.random.default_rng(int(np.log10(span)) + 50)
+    m, l_count = 4, 64
+    book = rng.standard_normal((m, l_count, 2)) * np.where(rng.random((m, l_count, 1)) < 0.1, span, 1.0)
+    from oracle import pqk_oracle as O
+
+    tables = O.build_distance_tables(book.astype(np.float32))
+    if not np.all(np.isfinite(tables)):
+        pytest.skip("float32 overflow in the codebook")
+    codes = rng.integers(0, l_count, size=(3000, m)).astype(np.uint8)
+    centers = rng.integers(0, l_count, size=(120, m)).astype(np.uint8)
+    _check(lib, oracle, codes, centers, tables)
+
+
+@pytest.mark.parametrize("m", [4, 8, 16])
+def test_clustered_codes_multi_pass(lib, oracle, m):
+    """Enough codes for several persistent passes per CTA and centres near the codes."""
+    rng = np.random.default_rng(m)
+    l_count = 256
+    tables = random_tables(m, l_count, seed=11 * m, sub_dim=4)
+    codes = mixture_codes(60_000 if m < 16 else 30_000, m, l_count, 400, seed=m)
+    centers = codes[rng.choice(len(codes), size=1000, replace=False)].copy()
+    _check(lib, oracle, codes, centers, tables, modes=(1, 2, 3))
+
+
+def test_single_center_and_k_equals_n(lib, oracle):
+    rng = np.random.default_rng(5)
+    tables = random_tables(4, 32, seed=5)
+    codes = rng.integers(0, 32, size=(500, 4)).astype(np.uint8)
+    _check(lib, oracle, codes, codes[:1].copy(), tables)
+    _check(lib, oracle, codes, codes.copy(), tables)
+
+
+def test_fit_parity_forced(lib, oracle):
+    from paper_1709_03708_b200 import _lib
+    import paper_1709_03708_b200 as pqk
+
+    tables = random_tables(4, 256, seed=8, sub_dim=4)
+    codes = mixture_codes(20_000, 4, 256, 300, seed=8)
+    _lib.check(lib.pqk_set_scan_mode(2), "scan mode")
+    try:
+        res = pqk.fit(codes, tables, 200, max_iterations=5, seed=3)
+    finally:
+        _lib.check(lib.pqk_set_scan_mode(0), "scan mode")
+    ref = oracle.fit(codes, tables, 200, max_iterations=5, seed=3, scan=oracle.assign_c)
+    np.testing.assert_array_equal(res.labels, ref["labels"])
+    np.testing.assert_array_equal(res.centers, ref["centers"])
+    assert [s.objective for s in res.trace] == [t["objective"] for t in ref["trace"]]

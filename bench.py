@@ -416,6 +416,7 @@ def main() -> None:
             cur, _ = step(cur)
         torch.cuda.synchronize(dev)
         step_ms, scan_ms, uniq, flagged, vote_fp64, vote_dd = [], [], [], [], [], []
+        flagged64, lookup_b = [], []
         launches0 = lib.pqk_launch_count()
         graph_launches[0] = 0
         with ClockSampler(local) as clocks:
@@ -434,6 +435,8 @@ def main() -> None:
                 scan_ms.append(ev_scan0.elapsed_time(ev_scan1))
                 uniq.append(int(st[_lib.STAT_UNIQUE_CENTERS]))
                 flagged.append(int(st[_lib.STAT_FLAGGED]))
+                flagged64.append(int(st[_lib.STAT_FLAGGED_FP64]))
+                lookup_b.append(int(st[_lib.STAT_LOOKUP_BYTES]))
                 vote_fp64.append(int(st[_lib.STAT_VOTE_FP64]))
                 vote_dd.append(int(st[_lib.STAT_VOTE_EXACT]))
         launches = lib.pqk_launch_count() - launches0 + graph_launches[0]
@@ -449,7 +452,9 @@ def main() -> None:
 
     # roofline of the dominant kernel (assignment scan): shared-memory lookups
     u = int(np.median(uniq))
-    lookup_bytes = n_loc * u * m * 4  # algorithmic: one 4-byte table lookup per (code, center, subspace)
+    lb = int(np.median(lookup_b)) or 4  # 2: 16-bit first tier (uint16 tables), 4: fp32 scan
+    lookup_bytes = n_loc * u * m * lb  # algorithmic: one table lookup per (code, center, subspace)
+    scan_name = "hscan_kernel (16-bit fixed-point tables)" if lb == 2 else "scan_kernel (fp32 tables)"
     scan_s = float(np.mean(scan_ms)) / 1e3
     sm_count = torch.cuda.get_device_properties(dev).multi_processor_count
     clk = clocks.summary()
@@ -480,6 +485,7 @@ def main() -> None:
         "data": "synthetic",
         "config": {"workload": cfg["workload"], "n": n_total, "k": k, "m": m, "l": l_count,
                    "unique_centers": u, "flagged_codes_per_iter": int(np.median(flagged)),
+                   "fp64_rescan_codes_per_iter": int(np.median(flagged64)),
                    "votes_fp64_per_iter": int(np.median(vote_fp64)), "votes_dd_per_iter": int(np.median(vote_dd)),
                    "l2": "flushed (512 MB write) between timed iterations",
                    "step": "assign+certify+objective+histogram+allreduce+vote+repair",
@@ -487,7 +493,7 @@ def main() -> None:
                    "parallelism": f"codes sharded dp{world}"},
         "roofline": {"bound": "smem", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic,
-                     "note": f"scan_kernel: {n_loc}x{u}x{m} 4-byte lookups per launch / {scan_s * 1e3:.3f} ms; peak = "
+                     "note": f"{scan_name}: {n_loc}x{u}x{m} {lb}-byte lookups per launch / {scan_s * 1e3:.3f} ms; peak = "
                              f"{sm_count} SMs x 128 B/clk x {peak_clock:.0f} MHz (architectural, not in "
                              "MEASURED_PEAKS.json)",
                      "scan_ms": scan_s * 1e3, "scan_share_of_step": scan_s * 1e3 / ms_per_step},

@@ -164,7 +164,9 @@ __global__ void dedup_compact_kernel(const uint8_t* __restrict__ cs, int k, int 
 // restricted-table chunks
 template <int MP, int KC>
 __global__ void qbuild_kernel(const float* __restrict__ t32, int l, const uint8_t* __restrict__ ucodes,
-                              const int32_t* __restrict__ counters, float4* __restrict__ q) {
+                              const int32_t* __restrict__ counters, float4* __restrict__ q,
+                              const int32_t* __restrict__ gate = nullptr, int32_t gate_min = 0) {
+  if (gate && *gate < gate_min) return;  // the fp32 list tier will not run
   const int U = counters[0];
   const int nchunks = (U + KC - 1) / KC;
   constexpr int Q4 = KC / 4;
@@ -501,13 +503,34 @@ __global__ void __launch_bounds__(256) rescan_cta_kernel(
     __syncthreads();
     double best = __longlong_as_double(0x7ff0000000000000LL);
     int bu = 0x7fffffff;
-    for (int u = tid; u < U; u += blockDim.x) {
-      const uint8_t* cc = ucodes + (size_t)u * mp;
-      double d = 0.0;
-      for (int mm = 0; mm < m; ++mm) d = dadd(d, s_rows[mm * l + cc[mm]]);
-      if (d < best) {
-        best = d;
-        bu = u;
+    // 4 centres per thread per step (independent code loads and add chains), visited in
+    // ascending index order per thread, so that ties keep the lowest index
+    const int bd = (int)blockDim.x;
+    for (int u0 = tid; u0 < U; u0 += 4 * bd) {
+      double d[4] = {0.0, 0.0, 0.0, 0.0};
+      for (int w = 0; 4 * w < m; ++w) {
+        uint32_t cw[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int u = u0 + q * bd;
+          cw[q] = u < U ? __ldg(reinterpret_cast<const uint32_t*>(ucodes + (size_t)u * mp) + w) : 0u;
+        }
+#pragma unroll
+        for (int bb = 0; bb < 4; ++bb) {
+          const int mm = 4 * w + bb;
+          if (mm < m) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) d[q] = dadd(d[q], s_rows[mm * l + ((cw[q] >> (8 * bb)) & 0xffu)]);
+          }
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int u = u0 + q * bd;
+        if (u < U && d[q] < best) {
+          best = d[q];
+          bu = u;
+        }
       }
     }
 #pragma unroll
@@ -539,10 +562,13 @@ __global__ void __launch_bounds__(256) rescan_cta_kernel(
 // first window sets the statistics, later windows add their flagged codes
 // kc16 > 0: the 16-bit first tier ran (chunks of kc16 centres, 2-byte lookups)
 __global__ void assign_stats_kernel(const int32_t* __restrict__ counters, int64_t* __restrict__ stats, int first,
-                                    int kc16) {
+                                    int kc16, int32_t list_min) {
   stats[PQK_STAT_UNIQUE_CENTERS] = counters[0];
   stats[PQK_STAT_FLAGGED] = (first ? 0 : stats[PQK_STAT_FLAGGED]) + counters[1];
-  stats[PQK_STAT_FLAGGED_FP64] = (first ? 0 : stats[PQK_STAT_FLAGGED_FP64]) + (kc16 ? counters[3] : counters[1]);
+  // codes decided by the exact rescan: the first-tier list when short, else what the
+  // fp32 list tier left
+  const int32_t exact = !kc16 ? counters[1] : (counters[1] < list_min ? counters[1] : counters[3]);
+  stats[PQK_STAT_FLAGGED_FP64] = (first ? 0 : stats[PQK_STAT_FLAGGED_FP64]) + exact;
   stats[PQK_STAT_NCHUNKS] = kc16 ? (counters[0] + kc16 - 1) / kc16 : counters[2];
   stats[PQK_STAT_LOOKUP_BYTES] = kc16 ? 2 : 4;
 }
@@ -591,6 +617,7 @@ struct AssignWS {
   uint16_t* t16;
   uint4* q16;
   int32_t* flags2;
+  uint2* keys16;
 };
 
 // Rows per scan window: the scan and the flag list index rows of a window in 32 bits;
@@ -627,6 +654,8 @@ static AssignWS assign_ws_layout(void* base, int64_t n, int64_t k, int mp, int l
   const size_t o_q16 = take(h16_ok ? (size_t)((k + kc16 - 1) / kc16) * l * mp * kc16 * sizeof(uint16_t) : 0, 1024);
   const size_t o_fl2 =
       take(h16_ok ? (size_t)std::max<int64_t>(std::min(n, kScanWindow), 1) * sizeof(int32_t) : 0, 256);
+  const size_t o_k16 =
+      take(h16_ok ? (size_t)std::max<int64_t>(std::min(n, kScanWindow), 1) * sizeof(uint2) : 0, 256);
   w.total = align_up(off, 256);
   char* b = static_cast<char*>(base);
   if (b) {
@@ -642,6 +671,7 @@ static AssignWS assign_ws_layout(void* base, int64_t n, int64_t k, int mp, int l
     w.t16 = reinterpret_cast<uint16_t*>(b + o_t16);
     w.q16 = reinterpret_cast<uint4*>(b + o_q16);
     w.flags2 = reinterpret_cast<int32_t*>(b + o_fl2);
+    w.keys16 = reinterpret_cast<uint2*>(b + o_k16);
   }
   return w;
 }
@@ -705,9 +735,10 @@ static int launch_scan_list(const ScanParams& p, int l, cudaStream_t stream) {
 // ---------------------------------------------------------------------------
 // 16-bit first tier (pqk_hscan.cuh)
 template <int MP, int KC, int NW, int S, int C, int... Cs>
-static int launch_hscan_c(int c_need, const h16::HScanParams& p, int grid, int l, cudaStream_t stream) {
+static int launch_hscan_c(int c_need, const h16::HScanParams& p, uint2* keys, int grid, int l,
+                          cudaStream_t stream) {
   if constexpr (sizeof...(Cs) > 0) {
-    if (c_need > C) return launch_hscan_c<MP, KC, NW, S, Cs...>(c_need, p, grid, l, stream);
+    if (c_need > C) return launch_hscan_c<MP, KC, NW, S, Cs...>(c_need, p, keys, grid, l, stream);
   }
   const DevInfo& di = dev_info();
   const size_t smem = 128 + (size_t)S * 256 * MP * KC * 2;  // ring stride: 256 rows (immediate offsets)
@@ -716,14 +747,17 @@ static int launch_hscan_c(int c_need, const h16::HScanParams& p, int grid, int l
   PQK_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   ProfileEvents& pe = profile_events();
   if (pe.before) PQK_CUDA_TRY(record_profile_event(pe.before, stream));
-  kern<<<grid, (NW + 1) * 32, smem, stream>>>(p);
+  kern<<<grid, (NW + 1) * 32, smem, stream>>>(p, keys);
   PQK_LAUNCH_CHECK("hscan_kernel");
   if (pe.after) PQK_CUDA_TRY(record_profile_event(pe.after, stream));
+  const int fgrid = (int)std::min<int64_t>((p.n + 255) / 256, (int64_t)di.sms * 64);
+  h16::hfinal_kernel<MP, KC><<<std::max(fgrid, 1), 256, 0, stream>>>(p, keys);
+  PQK_LAUNCH_CHECK("hfinal_kernel");
   return PQK_OK;
 }
 
 template <int MP, int KC, int NW, int S, int... Cs>
-static int launch_hscan(const h16::HScanParams& base_params, int l, cudaStream_t stream) {
+static int launch_hscan(const h16::HScanParams& base_params, uint2* keys, int l, cudaStream_t stream) {
   constexpr int H = KC / 8;
   constexpr int OWN = NW * (32 / H);
   constexpr int CMAX = std::max({Cs...});
@@ -745,7 +779,7 @@ static int launch_hscan(const h16::HScanParams& base_params, int l, cudaStream_t
   const int grid = (int)std::min<int64_t>(G, npasses);
   if (grid <= 0) return PQK_OK;
   const int c_need = (int)((pass_size + OWN - 1) / OWN);
-  return launch_hscan_c<MP, KC, NW, S, Cs...>(c_need, p, grid, l, stream);
+  return launch_hscan_c<MP, KC, NW, S, Cs...>(c_need, p, keys, grid, l, stream);
 }
 
 // 0: 16-bit first tier where it pays off (default); 1: fp32 scan only; 2: 16-bit first tier
@@ -828,18 +862,25 @@ extern "C" int pqk_assign_device(const uint8_t* d_codes, int64_t n, int32_t m, i
   PQK_LAUNCH_CHECK("dedup_compact_kernel");
 
   const DevInfo& di = dev_info();
-  if (fast) {
-    // 2. restricted-table chunks
+  // 2. fp32 restricted-table chunks (16-bit path: built inside the window loop, only
+  //    when the first tier leaves a list long enough for the fp32 list tier)
+  auto qbuild32 = [&](const int32_t* gate, int32_t gate_min) -> int {
     const int kc = kc_for(mp);
     const int64_t units = ((k + kc - 1) / kc) * l * mp * (kc / 4);
     const int qgrid = (int)std::min<int64_t>((units + 255) / 256, (int64_t)di.sms * 16);
+    float4* q4 = (float4*)w.q;
     switch (mp) {
-      case 4: qbuild_kernel<4, 8><<<qgrid, 256, 0, stream>>>(d_t32, l, w.ucodes, w.counters, (float4*)w.q); break;
-      case 8: qbuild_kernel<8, 4><<<qgrid, 256, 0, stream>>>(d_t32, l, w.ucodes, w.counters, (float4*)w.q); break;
-      case 16: qbuild_kernel<16, 4><<<qgrid, 256, 0, stream>>>(d_t32, l, w.ucodes, w.counters, (float4*)w.q); break;
-      case 32: qbuild_kernel<32, 4><<<qgrid, 256, 0, stream>>>(d_t32, l, w.ucodes, w.counters, (float4*)w.q); break;
+      case 4: qbuild_kernel<4, 8><<<qgrid, 256, 0, stream>>>(d_t32, l, w.ucodes, w.counters, q4, gate, gate_min); break;
+      case 8: qbuild_kernel<8, 4><<<qgrid, 256, 0, stream>>>(d_t32, l, w.ucodes, w.counters, q4, gate, gate_min); break;
+      case 16: qbuild_kernel<16, 4><<<qgrid, 256, 0, stream>>>(d_t32, l, w.ucodes, w.counters, q4, gate, gate_min); break;
+      case 32: qbuild_kernel<32, 4><<<qgrid, 256, 0, stream>>>(d_t32, l, w.ucodes, w.counters, q4, gate, gate_min); break;
     }
     PQK_LAUNCH_CHECK("qbuild_kernel");
+    return PQK_OK;
+  };
+  if (fast && !use16) {
+    const int rc = qbuild32(nullptr, 0);
+    if (rc != PQK_OK) return rc;
   }
   if (use16) {
     // 16-bit fixed-point tables (scale from the table maximum) and their chunks
@@ -916,12 +957,14 @@ extern "C" int pqk_assign_device(const uint8_t* d_codes, int64_t n, int32_t m, i
       hp.flag_count = w.counters + 1;
       int rc = PQK_OK;
       switch (mp) {
-        case 4: rc = launch_hscan<4, 16, 11, 4, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15, 16>(hp, l, stream); break;
-        case 8: rc = launch_hscan<8, 8, 11, 4, 1, 2, 3, 4, 5, 6, 7, 8>(hp, l, stream); break;
-        case 16: rc = launch_hscan<16, 8, 11, 3, 1, 2, 3, 4>(hp, l, stream); break;
+        case 4: rc = launch_hscan<4, 16, 11, 4, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15, 16>(hp, w.keys16, l, stream); break;
+        case 8: rc = launch_hscan<8, 8, 11, 4, 1, 2, 3, 4, 5, 6, 7, 8>(hp, w.keys16, l, stream); break;
+        case 16: rc = launch_hscan<16, 8, 11, 3, 1, 2, 3, 4>(hp, w.keys16, l, stream); break;
       }
       if (rc != PQK_OK) return rc;
       // 3b. fp32 tier over the uncertified list when it is long
+      rc = qbuild32(w.counters + 1, list_min);
+      if (rc != PQK_OK) return rc;
       ScanParams sp{};
       sp.codes = codes;
       sp.n = 0;
@@ -947,7 +990,7 @@ extern "C" int pqk_assign_device(const uint8_t* d_codes, int64_t n, int32_t m, i
       }
       if (rc != PQK_OK) return rc;
       // 4. exact rescans: the short first-tier list, then what the fp32 tier left
-      rescan_cta_kernel<<<di.sms * 2, 256, rows_bytes, stream>>>(codes, wn, mp, m, l, w.ucodes, w.counters, w.flags,
+      rescan_cta_kernel<<<di.sms * 8, 256, rows_bytes, stream>>>(codes, wn, mp, m, l, w.ucodes, w.counters, w.flags,
                                                                 w.counters + 1, w.pos2idx, d_t64, labels, sd_sq, 0,
                                                                 list_min);
       PQK_LAUNCH_CHECK("rescan_cta_kernel");
@@ -956,7 +999,7 @@ extern "C" int pqk_assign_device(const uint8_t* d_codes, int64_t n, int32_t m, i
                                                                 sd_sq, 0, 0x7fffffff);
       PQK_LAUNCH_CHECK("rescan_cta_kernel");
       if (d_stats) {
-        assign_stats_kernel<<<1, 1, 0, stream>>>(w.counters, d_stats, w0 == 0, kc16);
+        assign_stats_kernel<<<1, 1, 0, stream>>>(w.counters, d_stats, w0 == 0, kc16, list_min);
         PQK_LAUNCH_CHECK("assign_stats_kernel");
       }
       continue;
@@ -1002,7 +1045,7 @@ extern "C" int pqk_assign_device(const uint8_t* d_codes, int64_t n, int32_t m, i
       PQK_LAUNCH_CHECK("rescan_kernel");
     }
     if (d_stats) {
-      assign_stats_kernel<<<1, 1, 0, stream>>>(w.counters, d_stats, w0 == 0, 0);
+      assign_stats_kernel<<<1, 1, 0, stream>>>(w.counters, d_stats, w0 == 0, 0, 0);
       PQK_LAUNCH_CHECK("assign_stats_kernel");
     }
   }

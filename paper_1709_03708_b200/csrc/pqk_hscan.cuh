@@ -11,7 +11,7 @@
 //     s * D(u) >= Q(u) - M/2 - 0.01      (D = exact float64 reference sum).
 // The scale s = QMAX / t_hi resolves the distances that decide assignments:
 // t_hi = min(max(T), 2 x the largest per-subspace term of the nearest centre over a
-// sample of 256 codes).  Entries above t_hi saturate; the bound above still holds, and
+// sample of 128 codes).  Entries above t_hi saturate; the bound above still holds, and
 // a code whose decision involves saturated terms simply fails its certificate.
 //
 // Keys.  Each lane holds 8 centers of a KC-center chunk as 4 packed registers.  Per
@@ -19,7 +19,7 @@
 // key (value << 16 | chunk); it tracks the smallest key B and the second-smallest S
 // over chunks — no per-centre index bookkeeping in the loop.
 //
-// Finalisation (per code).  c* = chunk of the smallest key.  The chunk is re-read from
+// Finalisation (per code, hfinal_kernel).  c* = chunk of the smallest key.  The chunk is re-read from
 // the global table copy, its centres with Q(u) <= Q_min + M + 1 are re-evaluated
 // exactly in float64 (ascending m, __dadd_rn) and the smallest, lowest index on ties,
 // is the candidate winner w* with distance d*.  Every other centre of chunk c* has
@@ -59,7 +59,7 @@ struct Scale {
   unsigned long long termbits;  // largest nearest-centre term over the code sample (float64 bits)
 };
 
-constexpr int kScaleSample = 256;
+constexpr int kScaleSample = 128;
 
 // Scale heuristic (never affects correctness): for kScaleSample evenly spaced codes,
 // the nearest distinct centre (float64 sums over the staged table rows, first minimum)
@@ -247,69 +247,80 @@ __device__ __forceinline__ void load_code_rot(const uint8_t* __restrict__ codes,
   for (int k = 0; k < W; ++k) out[k] = __funnelshift_r(u[k], u[(k + 1) % W], 8 * rb);
 }
 
-// Finalisation of one code (all lanes of the warp call it: H = 2 lanes share a code).
+// Finalisation, one thread per code (a separate, fully parallel kernel: its dependent
+// global loads would otherwise stall every warp of the scan at the end of each pass).
+// keys[i] = (B, Sg): B = (Q << 16 | chunk) of the smallest chunk minimum, Sg the lower
+// bound of every centre outside chunk(B) (~0: none).
 template <int MP, int KC>
-__device__ __noinline__ void finalize_code(const HScanParams& p, int idx, bool valid, uint32_t k0, uint32_t s0,
-                                           int h, int U, double s_q, bool bad) {
-  constexpr int H = KC / 8;
+__global__ void __launch_bounds__(256, 4) hfinal_kernel(const HScanParams p, const uint2* __restrict__ keys) {
+  constexpr int G8 = KC / 8;  // uint4 groups of 8 centres per (chunk, row, subspace)
+  const int U = p.counters[0];
   const int m = p.m;
-  uint32_t k1 = 0xffffffffu, s1 = 0xffffffffu;
-  if constexpr (H == 2) {
-    k1 = __shfl_xor_sync(0xffffffffu, k0, 1);
-    s1 = __shfl_xor_sync(0xffffffffu, s0, 1);
-  }
-  const uint32_t cstar = min(k0, k1) & 0xffffu;
-  const uint32_t sg = min(((k0 & 0xffffu) == cstar) ? s0 : k0, ((k1 & 0xffffu) == cstar) ? s1 : k1);
-  // re-read chunk c* (this lane's 8 centres) and sum exactly as in the loop
-  const uint8_t* xc = p.codes + (size_t)(valid ? idx : 0) * MP;
-  uint32_t r[4] = {0u, 0u, 0u, 0u};
-  if (valid) {
-    for (int mm = 0; mm < m; ++mm) {
-      const uint4 w = __ldg(p.q + (((size_t)cstar * p.l + xc[mm]) * MP + mm) * H + h);
-      r[0] += w.x;
-      r[1] += w.y;
-      r[2] += w.z;
-      r[3] += w.w;
-    }
-  }
-  const int u0 = (int)cstar * KC + h * 8;
-  uint32_t qmin = 0xffffffffu;
+  const double s_q = p.sc->s;
+  const bool bad = p.sc->bad != 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < p.n; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint2 kv = keys[i];
+    const uint32_t cstar = kv.x & 0xffffu, sg = kv.y;
+    const uint8_t* xc = p.codes + (size_t)i * MP;
+    uint32_t xb[MP / 4];
 #pragma unroll
-  for (int e = 0; e < 8; ++e) {
-    const uint32_t qe = (e & 1) ? (r[e >> 1] >> 16) : (r[e >> 1] & 0xffffu);
-    if (u0 + e < U) qmin = min(qmin, qe);
-  }
-  if constexpr (H == 2) qmin = min(qmin, __shfl_xor_sync(0xffffffffu, qmin, 1));
-  double best = __longlong_as_double(0x7ff0000000000000LL);
-  int bu = 0x7fffffff;
-  uint32_t qn = 0xffffffffu;  // smallest sum of a non-candidate centre of chunk c* (none: ~0)
-  if (valid) {
-#pragma unroll 1
-    for (int e = 0; e < 8; ++e) {
-      const uint32_t qe = (e & 1) ? (r[e >> 1] >> 16) : (r[e >> 1] & 0xffffu);
+    for (int w = 0; w < MP / 4; ++w) xb[w] = __ldg(reinterpret_cast<const uint32_t*>(xc) + w);
+    // the KC exact sums of chunk c* (as in the scan)
+    uint32_t r[G8][4];
+#pragma unroll
+    for (int g = 0; g < G8; ++g) r[g][0] = r[g][1] = r[g][2] = r[g][3] = 0u;
+#pragma unroll
+    for (int mm = 0; mm < MP; ++mm) {
+      if (mm < m) {
+        const uint32_t x = (xb[mm >> 2] >> (8 * (mm & 3))) & 0xffu;
+#pragma unroll
+        for (int g = 0; g < G8; ++g) {
+          const uint4 w = __ldg(p.q + (((size_t)cstar * p.l + x) * MP + mm) * G8 + g);
+          r[g][0] += w.x;
+          r[g][1] += w.y;
+          r[g][2] += w.z;
+          r[g][3] += w.w;
+        }
+      }
+    }
+    const int u0 = (int)cstar * KC;
+    uint32_t qmin = 0xffffffffu;
+#pragma unroll
+    for (int e = 0; e < KC; ++e) {
+      const uint32_t w = r[e >> 3][(e & 7) >> 1];
+      const uint32_t qe = (e & 1) ? (w >> 16) : (w & 0xffffu);
+      if (u0 + e < U) qmin = min(qmin, qe);
+    }
+    double best = __longlong_as_double(0x7ff0000000000000LL);
+    int bu = 0x7fffffff;
+    uint32_t qn = 0xffffffffu;  // smallest sum of a non-candidate centre of chunk c* (none: ~0)
+#pragma unroll
+    for (int e = 0; e < KC; ++e) {
+      const uint32_t w = r[e >> 3][(e & 7) >> 1];
+      const uint32_t qe = (e & 1) ? (w >> 16) : (w & 0xffffu);
       const int u = u0 + e;
-      if (u < U && qe > qmin + (uint32_t)m + 1u) qn = min(qn, qe);
-      if (u < U && qe <= qmin + (uint32_t)m + 1u) {
-        const uint8_t* cc = p.ucodes + (size_t)u * MP;
+      if (u >= U) continue;
+      if (qe > qmin + (uint32_t)m + 1u) {
+        qn = min(qn, qe);
+      } else {
+        uint32_t cb[MP / 4];
+#pragma unroll
+        for (int w = 0; w < MP / 4; ++w) cb[w] = __ldg(reinterpret_cast<const uint32_t*>(p.ucodes + (size_t)u * MP) + w);
         double d = 0.0;
-        for (int mm = 0; mm < m; ++mm) d = dadd(d, __ldg(&p.t64[((size_t)mm * p.l + xc[mm]) * p.l + cc[mm]]));
+#pragma unroll
+        for (int mm = 0; mm < MP; ++mm) {
+          if (mm < m) {
+            const uint32_t x = (xb[mm >> 2] >> (8 * (mm & 3))) & 0xffu;
+            const uint32_t c = (cb[mm >> 2] >> (8 * (mm & 3))) & 0xffu;
+            d = dadd(d, __ldg(&p.t64[((size_t)mm * p.l + x) * p.l + c]));
+          }
+        }
         if (d < best) {  // ascending u: ties keep the lower index
           best = d;
           bu = u;
         }
       }
     }
-  }
-  if constexpr (H == 2) {
-    const double ob = __shfl_xor_sync(0xffffffffu, best, 1);
-    const int ou = __shfl_xor_sync(0xffffffffu, bu, 1);
-    if (ob < best || (ob == best && ou < bu)) {
-      best = ob;
-      bu = ou;
-    }
-    qn = min(qn, __shfl_xor_sync(0xffffffffu, qn, 1));
-  }
-  if (h == 0 && valid) {
     bool cert = !bad && bu != 0x7fffffff;
     // lower bound of every centre other than the candidates: other chunks (Sg) and the
     // non-candidates of c* (Qn); ~0 = no such centre
@@ -319,11 +330,11 @@ __device__ __noinline__ void finalize_code(const HScanParams& p, int idx, bool v
       cert = lo > best * s_q * (1.0 + 0x1p-40);
     }
     if (cert) {
-      p.labels[idx] = (uint32_t)__ldg(&p.pos2idx[bu]);
-      p.sd_sq[idx] = best;
+      p.labels[i] = (uint32_t)__ldg(&p.pos2idx[bu]);
+      p.sd_sq[i] = best;
     } else {
       const int f = atomicAdd(p.flag_count, 1);
-      p.flags[f] = idx;
+      p.flags[f] = (int32_t)i;
     }
   }
 }
@@ -335,7 +346,7 @@ __device__ __noinline__ void finalize_code(const HScanParams& p, int idx, bool v
 // phase are P consecutive ones: disjoint banks whatever the code bytes (4 wavefronts per
 // LDS.128, as in the fp32 scan).
 template <int MP, int KC, int C, int NW, int S>
-__global__ void __launch_bounds__((NW + 1) * 32, 1) hscan_kernel(const HScanParams p) {
+__global__ void __launch_bounds__((NW + 1) * 32, 1) hscan_kernel(const HScanParams p, uint2* __restrict__ keys) {
   constexpr int H = KC / 8;
   constexpr int OWN_W = 32 / H;
   constexpr int OWN = NW * OWN_W;
@@ -395,8 +406,6 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) hscan_kernel(const HScanPara
   const uint32_t stage0 = smem_u32(stages);
   const int n = (int)p.n;
   const int pass_size = (int)p.pass_size;
-  const double s_q = p.sc->s;
-  const bool bad = p.sc->bad != 0;
 
   uint32_t bits = 0;
   for (int pi = 0; pi < (int)my_passes; ++pi) {
@@ -455,10 +464,21 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) hscan_kernel(const HScanPara
     }
     }
 
-    // ---------------- finalize (unrolled: the keys stay in registers) ----------------
+    // ---------------- end of pass: merge the code's lanes, store (B, Sg) ----------------
 #pragma unroll
-    for (int j = 0; j < C; ++j)
-      finalize_code<MP, KC>(p, my0 + j * OWN, my0 + j * OWN < end, bk[j], sk[j], h, U, s_q, bad);
+    for (int j = 0; j < C; ++j) {
+      const uint32_t k0 = bk[j], s0 = sk[j];
+      uint32_t k1 = 0xffffffffu, s1 = 0xffffffffu;
+      if constexpr (H == 2) {
+        k1 = __shfl_xor_sync(0xffffffffu, k0, 1);
+        s1 = __shfl_xor_sync(0xffffffffu, s0, 1);
+      }
+      const uint32_t kb = min(k0, k1);
+      const uint32_t cstar = kb & 0xffffu;
+      const uint32_t sg = min(((k0 & 0xffffu) == cstar) ? s0 : k0, ((k1 & 0xffffu) == cstar) ? s1 : k1);
+      const int idx = my0 + j * OWN;
+      if (h == 0 && idx < end) keys[idx] = make_uint2(kb, sg);
+    }
   }
 }
 

@@ -82,14 +82,29 @@ __global__ void __launch_bounds__(256) scale_sample_kernel(const uint8_t* __rest
   __syncthreads();
   double best = __longlong_as_double(0x7ff0000000000000LL);
   int bu = 0x7fffffff;
-  for (int u = tid; u < U; u += blockDim.x) {
-    const uint8_t* cc = ucodes + (size_t)u * mp;
-    double d = 0.0;
-    for (int mm = 0; mm < m; ++mm) d += s_rows[mm * l + cc[mm]];
-    if (d < best) {
-      best = d;
-      bu = u;
+  const int bd = (int)blockDim.x;
+  for (int u0 = tid; u0 < U; u0 += 4 * bd) {  // 4 independent centres per step
+    double d[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int w = 0; 4 * w < m; ++w) {
+      uint32_t cw[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int u = u0 + q * bd;
+        cw[q] = u < U ? __ldg(reinterpret_cast<const uint32_t*>(ucodes + (size_t)u * mp) + w) : 0u;
+      }
+#pragma unroll
+      for (int bb = 0; bb < 4; ++bb)
+        if (4 * w + bb < m) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) d[q] += s_rows[(4 * w + bb) * l + ((cw[q] >> (8 * bb)) & 0xffu)];
+        }
     }
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (u0 + q * bd < U && d[q] < best) {
+        best = d[q];
+        bu = u0 + q * bd;
+      }
   }
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) {

@@ -27,15 +27,33 @@ namespace pqk {
 // ---------------------------------------------------------------------------
 // histogram
 __global__ void histogram_kernel(const uint8_t* __restrict__ codes, int64_t n, int mp, int m, int l,
-                                 const uint32_t* __restrict__ labels, uint32_t* __restrict__ hist,
-                                 uint32_t* __restrict__ counts) {
+                                 const uint32_t* __restrict__ labels, uint32_t* __restrict__ hist) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t k = labels[i];
-    const uint8_t* x = codes + i * mp;
-    atomicAdd(&counts[k], 1u);
+    const uint32_t* x = reinterpret_cast<const uint32_t*>(codes + i * mp);  // mp is a multiple of 4
     uint32_t* hk = hist + k * m * l;
-    for (int mm = 0; mm < m; ++mm) atomicAdd(&hk[mm * l + x[mm]], 1u);
+    for (int w = 0; 4 * w < m; ++w) {
+      const uint32_t cw = __ldg(x + w);
+#pragma unroll
+      for (int b = 0; b < 4; ++b)
+        if (4 * w + b < m) atomicAdd(&hk[(4 * w + b) * l + ((cw >> (8 * b)) & 0xffu)], 1u);
+    }
   }
+}
+
+// counts[k] = sum_s hist[k][0][s] (clustering.py:458's bincount): one warp per cluster,
+// no contended per-cluster atomics in the histogram pass
+__global__ void counts_from_hist_kernel(const uint32_t* __restrict__ hist, int64_t k, int m, int l,
+                                        uint32_t* __restrict__ counts) {
+  const int lane = threadIdx.x & 31;
+  const int64_t kk = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (kk >= k) return;
+  const uint32_t* row = hist + kk * m * l;
+  uint32_t c = 0;
+  for (int s = lane; s < l; s += 32) c += row[s];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if (lane == 0) counts[kk] = c;
 }
 
 // ---------------------------------------------------------------------------
@@ -619,12 +637,14 @@ extern "C" int pqk_histogram_device(const uint8_t* d_codes, int64_t n, int32_t m
   if (mp == 0 || l < 1 || l > kMaxL || k < 1 || n < 0) return fail(PQK_EINVAL, "pqk_histogram_device: bad arguments");
   if (n > (int64_t)UINT32_MAX) return fail(PQK_EUNSUPPORTED, "pqk_histogram_device: n must be < 2^32 (uint32 counts)");
   PQK_CUDA_TRY(cudaMemsetAsync(d_hist, 0, (size_t)k * m * l * sizeof(int32_t), stream));
-  PQK_CUDA_TRY(cudaMemsetAsync(d_counts, 0, (size_t)k * sizeof(int32_t), stream));
-  if (n == 0) return PQK_OK;
-  const DevInfo& di = dev_info();
-  const int grid = (int)std::min<int64_t>((n + 255) / 256, (int64_t)di.sms * 8);
-  histogram_kernel<<<grid, 256, 0, stream>>>(d_codes, n, mp, m, l, d_labels, d_hist, d_counts);
-  PQK_LAUNCH_CHECK("histogram_kernel");
+  if (n > 0) {
+    const DevInfo& di = dev_info();
+    const int grid = (int)std::min<int64_t>((n + 255) / 256, (int64_t)di.sms * 8);
+    histogram_kernel<<<grid, 256, 0, stream>>>(d_codes, n, mp, m, l, d_labels, d_hist);
+    PQK_LAUNCH_CHECK("histogram_kernel");
+  }
+  counts_from_hist_kernel<<<(unsigned)((k * 32 + 255) / 256), 256, 0, stream>>>(d_hist, k, m, l, d_counts);
+  PQK_LAUNCH_CHECK("counts_from_hist_kernel");
   return PQK_OK;
 }
 

@@ -299,41 +299,46 @@ __global__ void __launch_bounds__(256, 4) hfinal_kernel(const HScanParams p, con
       }
     }
     const int u0 = (int)cstar * KC;
-    uint32_t qmin = 0xffffffffu;
+    const int nreal = min(KC, U - u0);  // real centres of chunk c* (the last chunk is partial)
+    uint32_t qv[KC];
 #pragma unroll
     for (int e = 0; e < KC; ++e) {
       const uint32_t w = r[e >> 3][(e & 7) >> 1];
-      const uint32_t qe = (e & 1) ? (w >> 16) : (w & 0xffffu);
-      if (u0 + e < U) qmin = min(qmin, qe);
+      qv[e] = (e < nreal) ? ((e & 1) ? (w >> 16) : (w & 0xffffu)) : 0xffffffffu;
+    }
+    uint32_t qmin = qv[0];
+#pragma unroll
+    for (int e = 1; e < KC; ++e) qmin = min(qmin, qv[e]);
+    // candidates: within M + 1 units of the chunk minimum; the rest bound from below (Qn)
+    const uint32_t lim = qmin + (uint32_t)m + 1u;
+    uint32_t cand = 0u, qn = 0xffffffffu;  // qn: smallest non-candidate sum (none: ~0)
+#pragma unroll
+    for (int e = 0; e < KC; ++e) {
+      const bool c = qv[e] <= lim;
+      cand |= (c ? 1u : 0u) << e;
+      if (!c) qn = min(qn, qv[e]);  // padding (~0) never lowers qn
     }
     double best = __longlong_as_double(0x7ff0000000000000LL);
     int bu = 0x7fffffff;
-    uint32_t qn = 0xffffffffu;  // smallest sum of a non-candidate centre of chunk c* (none: ~0)
-#pragma unroll
-    for (int e = 0; e < KC; ++e) {
-      const uint32_t w = r[e >> 3][(e & 7) >> 1];
-      const uint32_t qe = (e & 1) ? (w >> 16) : (w & 0xffffu);
+    while (cand) {  // ascending centre index: ties keep the lower one
+      const int e = __ffs(cand) - 1;
+      cand &= cand - 1u;
       const int u = u0 + e;
-      if (u >= U) continue;
-      if (qe > qmin + (uint32_t)m + 1u) {
-        qn = min(qn, qe);
-      } else {
-        uint32_t cb[MP / 4];
+      uint32_t cb[MP / 4];
 #pragma unroll
-        for (int w = 0; w < MP / 4; ++w) cb[w] = __ldg(reinterpret_cast<const uint32_t*>(p.ucodes + (size_t)u * MP) + w);
-        double d = 0.0;
+      for (int w = 0; w < MP / 4; ++w) cb[w] = __ldg(reinterpret_cast<const uint32_t*>(p.ucodes + (size_t)u * MP) + w);
+      double d = 0.0;
 #pragma unroll
-        for (int mm = 0; mm < MP; ++mm) {
-          if (mm < m) {
-            const uint32_t x = (xb[mm >> 2] >> (8 * (mm & 3))) & 0xffu;
-            const uint32_t c = (cb[mm >> 2] >> (8 * (mm & 3))) & 0xffu;
-            d = dadd(d, __ldg(&p.t64[((size_t)mm * p.l + x) * p.l + c]));
-          }
+      for (int mm = 0; mm < MP; ++mm) {
+        if (mm < m) {
+          const uint32_t x = (xb[mm >> 2] >> (8 * (mm & 3))) & 0xffu;
+          const uint32_t c = (cb[mm >> 2] >> (8 * (mm & 3))) & 0xffu;
+          d = dadd(d, __ldg(&p.t64[((size_t)mm * p.l + x) * p.l + c]));
         }
-        if (d < best) {  // ascending u: ties keep the lower index
-          best = d;
-          bu = u;
-        }
+      }
+      if (d < best) {
+        best = d;
+        bu = u;
       }
     }
     bool cert = !bad && bu != 0x7fffffff;

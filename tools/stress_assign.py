@@ -2,7 +2,9 @@
 short fit against the oracle: lattice (integer) tables with massive ties, duplicated
 centers, tiny/huge table scales, all code widths.
 
-usage: python tools/stress_assign.py [seconds]"""
+usage: python tools/stress_assign.py [seconds] [scan_mode]
+  scan_mode: 0 default tiers, 1 fp32 first, 2 16-bit first tier at any size, 3 as 2 with
+  the fp32 list tier for any list length (pqk_set_scan_mode)"""
 import sys
 import time
 
@@ -13,6 +15,10 @@ import paper_1709_03708_b200 as pqk  # noqa: E402
 from oracle import pqk_oracle as O  # noqa: E402
 
 budget = float(sys.argv[1]) if len(sys.argv) > 1 else 120.0
+mode = int(sys.argv[2]) if len(sys.argv) > 2 else 0
+from paper_1709_03708_b200 import _lib  # noqa: E402
+
+_lib.check(_lib.load().pqk_set_scan_mode(mode), "scan mode")
 rng = np.random.default_rng(int(time.time()) + 1)
 t0 = time.time()
 cases = 0
@@ -49,4 +55,4 @@ while time.time() - t0 < budget:
         if not (np.array_equal(res.labels, ref["labels"]) and np.array_equal(res.centers, ref["centers"])):
             print("FIT MISMATCH", dict(m=m, l=l_count, kind=kind, n=n, k=k), flush=True)
             sys.exit(1)
-print(f"ok: {cases} assignment cases in {time.time() - t0:.0f}s")
+print(f"ok: {cases} assignment cases in {time.time() - t0:.0f}s (scan mode {mode})")

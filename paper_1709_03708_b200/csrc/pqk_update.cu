@@ -16,6 +16,8 @@
 //   objective : clustering.py:448-449, float(np.mean(np.sqrt(sd))) and
 //               float(np.mean(sd)), evaluated with numpy's pairwise-summation tree so
 //               the sums (and hence the exact-equality stop rule at :450) match.
+#include <cuda_fp16.h>
+
 #include <algorithm>
 #include <cmath>
 
@@ -120,10 +122,40 @@ __device__ __forceinline__ void warp_best(Best& b) {
   for (int o = 16; o > 0; o >>= 1) b = merge_best(b, shfl_best(b, o));
 }
 
+// fp16 copy of the fp32 filter tables for the vote's first stage (half the L2 bytes per
+// support row): block per subspace, T16 = fp16(T32 * 2^f) with max * 2^f < 2^15.
+__global__ void __launch_bounds__(1024) vote_t16_kernel(const float* __restrict__ t32, int l, __half* __restrict__ t16) {
+  __shared__ float s_red[32];
+  __shared__ int s_f;
+  const float* src = t32 + (size_t)blockIdx.x * l * l;
+  __half* dst = t16 + (size_t)blockIdx.x * l * l;
+  const int ll = l * l;
+  float mx = 0.0f;
+  for (int i = threadIdx.x; i < ll; i += blockDim.x) mx = fmaxf(mx, src[i]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float v = s_red[threadIdx.x];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if (threadIdx.x == 0) {
+      int ex = 0;
+      frexpf(v, &ex);  // v in [2^(ex-1), 2^ex)
+      s_f = v > 0.0f ? 15 - ex : 0;
+    }
+  }
+  __syncthreads();
+  const int f = s_f;
+  for (int i = threadIdx.x; i < ll; i += blockDim.x) dst[i] = __float2half_rn(ldexpf(src[i], f));
+}
+
 __global__ void __launch_bounds__(32 * kVoteWarps) vote_kernel(const uint32_t* __restrict__ hist,
                                                                const uint32_t* __restrict__ counts, int64_t k, int m,
                                                                int l, int mp, const double* __restrict__ t64,
                                                                const float* __restrict__ t32,
+                                                               const __half* __restrict__ t16,
                                                                uint8_t* __restrict__ newc,
                                                                unsigned long long* __restrict__ acc) {
   __shared__ int s_s[kVoteWarps][kMaxL];
@@ -152,7 +184,40 @@ __global__ void __launch_bounds__(32 * kVoteWarps) vote_kernel(const uint32_t* _
   __syncwarp();
   if (lane == 0) atomicAdd(&acc[0], (unsigned long long)nnz);
   const double inf = __longlong_as_double(0x7ff0000000000000LL);
-  if (t32) {
+  if (t16) {
+    // stage 1 (l = 256): fp16 tables, fp32 FMA.  Lane owns columns 8 lane .. 8 lane + 7 (one
+    // 16-byte load per support row).  Per product the table entry carries relative error
+    // <= 2^-11 + 2^-23 (fp16 and fp32 roundings) plus 2^-25 absolute (fp16 subnormals);
+    // the FMA chain adds <= (nnz + 1) 2^-24 relative.  With H = sum of the counts,
+    // |v~_j - v_j| <= eps v~_j + 2^-24 H, eps = 2^-11 + (nnz + 4) 2^-24 + 2^-20; the
+    // winner is certified when v~_2 - v~_1 > eps (v~_1 + v~_2) + 2^-23 H.
+    const __half* th = t16 + (size_t)mm * l * l;
+    float v[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = 0.0f;
+    for (int j = 0; j < nnz; ++j) {
+      const float h = __uint2float_rn(sh[j]);
+      const uint4 raw = __ldg(reinterpret_cast<const uint4*>(th + (size_t)ss[j] * l) + lane);
+      const __half2* hp = reinterpret_cast<const __half2*>(&raw);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float2 f2 = __half22float2(hp[i]);
+        v[2 * i] = __fmaf_rn(h, f2.x, v[2 * i]);
+        v[2 * i + 1] = __fmaf_rn(h, f2.y, v[2 * i + 1]);
+      }
+    }
+    Best b{inf, 0, inf};
+#pragma unroll
+    for (int i = 0; i < 8; ++i) b = merge_best(b, Best{(double)v[i], 8 * lane + i, inf});
+    warp_best(b);
+    const double eps = 4.8828125e-04 + (double)(nnz + 4) * 5.9604644775390625e-08 + 9.5367431640625e-07;
+    const double hsum = (double)counts[kk];
+    if ((b.v2 - b.v1) > eps * (b.v1 + b.v2) + 1.1920928955078125e-07 * hsum) {
+      if (lane == 0) newc[kk * mp + mm] = (uint8_t)b.l1;
+      return;
+    }
+    if (lane == 0) atomicAdd(&acc[3], 1ull);
+  } else if (t32) {
     const float* tf = t32 + (size_t)mm * l * l;
     float v[8];
 #pragma unroll
@@ -629,6 +694,7 @@ static int run_select(const double* d_sd, int64_t n, int64_t base, const int64_t
 
 using namespace pqk;
 
+
 extern "C" int pqk_histogram_device(const uint8_t* d_codes, int64_t n, int32_t m, int32_t l,
                                     const uint32_t* d_labels, int64_t k, uint32_t* d_hist, uint32_t* d_counts,
                                     void* stream_) {
@@ -659,9 +725,28 @@ extern "C" int pqk_vote_device(const uint32_t* d_hist, const uint32_t* d_counts,
   unsigned long long* acc = reinterpret_cast<unsigned long long*>(d_stats + 16);
   PQK_CUDA_TRY(cudaMemsetAsync(acc, 0, 4 * sizeof(unsigned long long), stream));
   PQK_CUDA_TRY(cudaMemsetAsync(d_new_centers, 0, (size_t)k * mp, stream));
+  // fp16 first-stage tables, rebuilt every call (the tables may differ between calls) in
+  // stream-ordered memory (cudaMallocAsync: also valid inside a CUDA-graph capture)
+  __half* t16 = nullptr;
+  if (d_t32 && l == 256) {
+    static bool pool_kept[64] = {};
+    int dev = 0;
+    PQK_CUDA_TRY(cudaGetDevice(&dev));
+    if (!pool_kept[dev & 63]) {  // keep freed blocks in the pool (no OS round trip per call)
+      cudaMemPool_t pool;
+      PQK_CUDA_TRY(cudaDeviceGetDefaultMemPool(&pool, dev));
+      uint64_t keep = UINT64_MAX;
+      PQK_CUDA_TRY(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+      pool_kept[dev & 63] = true;
+    }
+    PQK_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&t16), (size_t)m * l * l * sizeof(__half), stream));
+    vote_t16_kernel<<<m, 1024, 0, stream>>>(d_t32, l, t16);
+    PQK_LAUNCH_CHECK("vote_t16_kernel");
+  }
   vote_kernel<<<(unsigned)((k * m + kVoteWarps - 1) / kVoteWarps), 32 * kVoteWarps, 0, stream>>>(
-      d_hist, d_counts, k, m, l, mp, d_t64, d_t32, d_new_centers, acc);
+      d_hist, d_counts, k, m, l, mp, d_t64, d_t32, t16, d_new_centers, acc);
   PQK_LAUNCH_CHECK("vote_kernel");
+  if (t16) PQK_CUDA_TRY(cudaFreeAsync(t16, stream));
   empties_kernel<<<(unsigned)((k + 1023) / 1024), 1024, 0, stream>>>(d_counts, k, acc);
   PQK_LAUNCH_CHECK("empties_kernel");
   vote_stats_kernel<<<1, 1, 0, stream>>>(k, acc, d_stats);

@@ -170,9 +170,11 @@ __global__ void __launch_bounds__(32 * kVoteWarps) vote_kernel(const uint32_t* _
   uint32_t* sh = s_h[warp];
   const uint32_t* hrow = hist + (kk * m + mm) * l;
   int nnz = 0;
+  unsigned long long hs = 0;  // sum of this row's counts (the fp16 stage's absolute term)
   for (int base = 0; base < l; base += 32) {
     const int s = base + lane;
     const uint32_t h = (s < l) ? hrow[s] : 0u;
+    hs += h;
     const unsigned bal = __ballot_sync(0xffffffffu, h != 0);
     if (h) {
       const int pos = nnz + __popc(bal & ((1u << lane) - 1u));
@@ -211,7 +213,10 @@ __global__ void __launch_bounds__(32 * kVoteWarps) vote_kernel(const uint32_t* _
     for (int i = 0; i < 8; ++i) b = merge_best(b, Best{(double)v[i], 8 * lane + i, inf});
     warp_best(b);
     const double eps = 4.8828125e-04 + (double)(nnz + 4) * 5.9604644775390625e-08 + 9.5367431640625e-07;
-    const double hsum = (double)counts[kk];
+    unsigned long long ht = hs;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ht += __shfl_xor_sync(0xffffffffu, ht, o);
+    const double hsum = (double)ht;
     if ((b.v2 - b.v1) > eps * (b.v1 + b.v2) + 1.1920928955078125e-07 * hsum) {
       if (lane == 0) newc[kk * mp + mm] = (uint8_t)b.l1;
       return;

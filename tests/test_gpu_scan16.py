@@ -124,3 +124,30 @@ def test_fit_parity_forced(lib, oracle):
     np.testing.assert_array_equal(res.labels, ref["labels"])
     np.testing.assert_array_equal(res.centers, ref["centers"])
     assert [s.objective for s in res.trace] == [t["objective"] for t in ref["trace"]]
+
+
+@pytest.mark.parametrize("kind", ["random", "lattice", "scaled", "heavy"])
+def test_vote_fp16_stage(oracle, kind):
+    """The vote's fp16 first stage (L = 256) decides the exact-arithmetic argmin
+    (clustering.py:349-354, lowest j on ties) or hands over to the fp64 stages."""
+    from paper_1709_03708_b200 import engine
+
+    rng = np.random.default_rng({"random": 1, "lattice": 2, "scaled": 3, "heavy": 4}[kind])
+    m, l_count, k = 2, 256, 600
+    if kind == "lattice":
+        tables = lattice_tables(m, l_count)  # integer distances: exact ties are common
+    else:
+        tables = random_tables(m, l_count, seed=17, sub_dim=3)
+        if kind == "scaled":
+            tables = tables * 1e-30
+    hist = np.zeros((k, m, l_count), dtype=np.int64)
+    for kk in range(k):
+        for mm in range(m):
+            nnz = int(rng.integers(1, 40))
+            sup = rng.choice(l_count, size=nnz, replace=False)
+            hi = 10**6 if kind == "heavy" else 50
+            hist[kk, mm, sup] = rng.integers(1, hi, size=nnz)
+    got = engine.vote_host(hist, tables)
+    for kk in range(k):
+        for mm in range(m):
+            assert got[kk, mm] == oracle.vote_argmin(hist[kk, mm], tables[mm]), (kk, mm)

@@ -3,7 +3,7 @@
 the per-assign time of each mode, the first-tier scan kernel time (profile events) and
 the flagged counts.  Also runs a few Lloyd iterations per mode and compares centres.
 
-usage: python tools/diag_scan16.py [c1|c2|c3s|c4s|c5s] [reps]
+usage: python tools/diag_scan16.py [c1|c2|c3s|c4s|c5s] [reps] [mode_a (default 0)]
   c3s/c4s/c5s: the config's codes at a reduced N (same K, M) so the run stays short."""
 import sys
 import time
@@ -18,6 +18,7 @@ from paper_1709_03708_b200.pq import PQCodebook, build_distance_tables  # noqa: 
 
 cfgn = sys.argv[1] if len(sys.argv) > 1 else "c2"
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 5
+mode_a = int(sys.argv[3]) if len(sys.argv) > 3 else 0  # 2: force the 16-bit tier (small configs)
 base = cfgn.rstrip("s")
 cfg = dict(bench.CONFIGS[base])
 n = {"c3s": 1_000_000, "c4s": 4_000_000, "c5s": 2_000_000}.get(cfgn, cfg["n"])
@@ -82,7 +83,7 @@ def run(mode, centers_host):
 ok = True
 cur_centers = centers0
 for it in range(3):
-    r0 = run(0, cur_centers)
+    r0 = run(mode_a, cur_centers)
     r1 = run(1, cur_centers)
     same = bool(torch.equal(r0[0], r1[0]) and torch.equal(r0[1].view(torch.int64), r1[1].view(torch.int64)))
     ok &= same

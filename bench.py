@@ -489,7 +489,9 @@ def main() -> None:
                    "votes_fp64_per_iter": int(np.median(vote_fp64)), "votes_dd_per_iter": int(np.median(vote_dd)),
                    "l2": "flushed (512 MB write) between timed iterations",
                    "step": "assign+certify+objective+histogram+allreduce+vote+repair",
-                   "launch": "eager" if (use_dist or args.no_graphs) else "cuda graphs (after first warm-up step)",
+                   "launch": ("eager" if args.no_graphs else
+                              "cuda graphs per phase (assign+objective+histogram, vote), collectives between"
+                              if use_dist else "cuda graphs (after first warm-up step)"),
                    "parallelism": f"codes sharded dp{world}"},
         "roofline": {"bound": "smem", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic,

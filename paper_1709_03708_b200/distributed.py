@@ -67,7 +67,12 @@ class GpuShardBackend:
         return self.engine_mod.upload_codes(centers, self.m, self.dev)
 
     def assign(self, centers_dev) -> None:
+        if not hasattr(self, "_ev"):
+            self._ev = [torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True, external=True),
+                        torch.cuda.Event(enable_timing=True)]
+        self._ev[0].record()
         self.eng.assign(centers_dev)
+        self._ev[1].record()
 
     def sync(self) -> None:
         torch.cuda.current_stream(self.dev).synchronize()
@@ -78,7 +83,63 @@ class GpuShardBackend:
 
     def vote(self) -> np.ndarray:
         self.eng.vote()
+        self._ev[2].record()
         return self.eng.stats_host()
+
+    # -- CUDA-graph phases (the driver uses them when present) ------------------
+    # local_phase = assign -> objective partials -> histogram (no communication);
+    # update_phase = vote.  The first call of each runs eagerly (lazy set-up), the next
+    # one captures a graph that later calls replay; the collectives stay outside.
+    def local_phase(self, centers_dev):
+        if not hasattr(self, "_ev"):
+            # _ev[1] is recorded inside the captured graph: an external event node fires on replay
+            self._ev = [torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True, external=True),
+                        torch.cuda.Event(enable_timing=True)]
+        if self.n == 0:
+            self.assign(centers_dev)
+            return self.objective_tensor(), *self.histogram()
+        g = getattr(self, "_graph_local", None)
+        if g is None:
+            self._ev[0].record()
+            self.eng.assign(centers_dev)
+            self._ev[1].record()
+            self.eng.objective()
+            self.eng.histogram()
+            if getattr(self, "_local_eager_done", False):
+                self._cur = centers_dev.clone()
+                self._graph_local = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(self._graph_local, capture_error_mode="thread_local"):
+                    self.eng.assign(self._cur)
+                    self._ev[1].record()
+                    self.eng.objective()
+                    self.eng.histogram()
+                # the capture did not run the work: this iteration's results come from the
+                # eager launches above
+            self._local_eager_done = True
+        else:
+            self._cur.copy_(centers_dev)
+            self._ev[0].record()
+            g.replay()
+        return self.eng.obj, self.eng.hist, self.eng.counts
+
+    def update_phase(self) -> np.ndarray:
+        g = getattr(self, "_graph_update", None)
+        if g is None:
+            self.eng.vote()
+            if getattr(self, "_update_eager_done", False):
+                self._graph_update = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(self._graph_update, capture_error_mode="thread_local"):
+                    self.eng.vote()
+            self._update_eager_done = True
+        else:
+            g.replay()
+        self._ev[2].record()
+        return self.eng.stats  # on the device: the driver reads it with the objective partials
+
+    def step_seconds(self) -> tuple[float, float]:
+        """Device time of the last assign and of everything after it up to the vote
+        (CUDA events; valid once vote()'s host read has synchronised)."""
+        return self._ev[0].elapsed_time(self._ev[1]) / 1e3, self._ev[1].elapsed_time(self._ev[2]) / 1e3
 
     def counts_host(self) -> np.ndarray:
         return self.eng.counts.cpu().numpy()
@@ -175,23 +236,42 @@ class DistributedLloyd:
 
     def iteration(self, centers_dev, previous: float | None) -> tuple[StepStats, object, bool]:
         """One Lloyd iteration; returns (stats, next centers, stopped)."""
+        # Everything up to the vote is queued without a host sync (the GPU never idles
+        # between the scan and the update); the one host read is the vote's stats.  The
+        # update is computed even on the stopping iteration and then discarded (the
+        # reference stops before updating, clustering.py:450-452: same results).
         t0 = time.perf_counter()
-        self.b.assign(centers_dev)
-        self.b.sync()
-        assign_seconds = time.perf_counter() - t0
-        parts = self._gather(self.b.objective_tensor()).cpu().numpy()
+        if hasattr(self.b, "local_phase"):  # GPU backend: CUDA-graph phases
+            obj_t, hist, counts = self.b.local_phase(centers_dev)
+        else:
+            self.b.assign(centers_dev)
+            obj_t = self.b.objective_tensor()
+            hist, counts = self.b.histogram()
+        parts_t = self._gather(obj_t)  # stream-ordered collectives
+        if self.world > 1:
+            dist.all_reduce(hist, op=dist.ReduceOp.SUM, group=self.group)
+            dist.all_reduce(counts, op=dist.ReduceOp.SUM, group=self.group)
+        if hasattr(self.b, "update_phase"):
+            # one device->host read for the objective partials and the vote stats
+            st_dev = self.b.update_phase()
+            both = torch.cat([parts_t.reshape(-1).view(torch.int64), st_dev.reshape(-1)]).cpu().numpy()
+            np_parts = both[: parts_t.numel()].view(np.float64).reshape(parts_t.shape)
+            stats = both[parts_t.numel():]
+            parts = np_parts
+        else:
+            stats = self.b.vote()
+            parts = parts_t.cpu().numpy()
+        t1 = time.perf_counter()
+        if hasattr(self.b, "step_seconds"):
+            assign_seconds, vote_seconds = self.b.step_seconds()
+        else:
+            assign_seconds, vote_seconds = t1 - t0, 0.0
         s1 = tree_combine(self.n_total, list(parts[:, 0]))
         s2 = tree_combine(self.n_total, list(parts[:, 1]))
         objective = float(np.float64(s1) / self.n_total)
         objective_sq = float(np.float64(s2) / self.n_total)
         if previous is not None and objective == previous:
             return StepStats(objective, objective_sq, 0, 0, 0, assign_seconds, 0.0), centers_dev, True
-        t1 = time.perf_counter()
-        hist, counts = self.b.histogram()
-        if self.world > 1:
-            dist.all_reduce(hist, op=dist.ReduceOp.SUM, group=self.group)
-            dist.all_reduce(counts, op=dist.ReduceOp.SUM, group=self.group)
-        stats = self.b.vote()
         empty_n = int(stats[3])
         if empty_n:
             counts_h = self.b.counts_host()
@@ -203,8 +283,9 @@ class DistributedLloyd:
             _, _, rows = merge_candidates([(gk, gi, gr)], empty_n)
             self.b.apply_repair(empty, rows)
         nxt = self.b.take_new_centers()
-        self.b.sync()
-        update_seconds = time.perf_counter() - t1
+        if empty_n:
+            self.b.sync()
+        update_seconds = vote_seconds + (time.perf_counter() - t1)
         st = StepStats(objective, objective_sq, empty_n, int(stats[4]), int(stats[2]), assign_seconds, update_seconds)
         return st, nxt, False
 

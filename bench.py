@@ -359,7 +359,7 @@ def main() -> None:
 
     offset, length = shard_bounds(n_total, world, rank)
     assert length == n_loc, (length, n_loc)
-    backend = GpuShardBackend(codes_host, offset, tables, k, device=local)
+    backend = GpuShardBackend(codes_host, offset, tables, k, device=local, graphs=not args.no_graphs)
     drv = DistributedLloyd(backend, n_total, k, m) if use_dist else None
     if use_dist:
         centers0 = drv.init_centers(SEED, codes_host)

@@ -50,9 +50,11 @@ class StepStats:
 class GpuShardBackend:
     """Backend over :class:`engine.ShardEngine` (sm_100a kernels)."""
 
-    def __init__(self, codes_local: np.ndarray, offset: int, tables: np.ndarray, k: int, device=None):
+    def __init__(self, codes_local: np.ndarray, offset: int, tables: np.ndarray, k: int, device=None, *,
+                 graphs: bool = True):
         from . import engine
 
+        self.graphs = graphs
         self.engine_mod = engine
         self.dev = engine.device_of(device)
         self.m = tables.shape[0]
@@ -105,7 +107,7 @@ class GpuShardBackend:
             self._ev[1].record()
             self.eng.objective()
             self.eng.histogram()
-            if getattr(self, "_local_eager_done", False):
+            if self.graphs and getattr(self, "_local_eager_done", False):
                 self._cur = centers_dev.clone()
                 self._graph_local = torch.cuda.CUDAGraph()
                 with torch.cuda.graph(self._graph_local, capture_error_mode="thread_local"):
@@ -126,7 +128,7 @@ class GpuShardBackend:
         g = getattr(self, "_graph_update", None)
         if g is None:
             self.eng.vote()
-            if getattr(self, "_update_eager_done", False):
+            if self.graphs and getattr(self, "_update_eager_done", False):
                 self._graph_update = torch.cuda.CUDAGraph()
                 with torch.cuda.graph(self._graph_update, capture_error_mode="thread_local"):
                     self.eng.vote()

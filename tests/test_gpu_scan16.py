@@ -151,3 +151,29 @@ def test_vote_fp16_stage(oracle, kind):
     for kk in range(k):
         for mm in range(m):
             assert got[kk, mm] == oracle.vote_argmin(hist[kk, mm], tables[mm]), (kk, mm)
+
+
+def test_default_mode_large_problem_uses_16bit_tier(lib, oracle):
+    """Default mode at >= 2^31 lookups: the 16-bit tier runs (2-byte lookups in the stats)
+    and labels / sd_sq still equal the oracle's linear scan on clustered codes."""
+    import torch
+
+    from paper_1709_03708_b200 import _lib, engine
+
+    rng = np.random.default_rng(31)
+    m, l_count = 4, 256
+    tables = random_tables(m, l_count, seed=31, sub_dim=8)
+    codes = mixture_codes(700_000, m, l_count, 3000, seed=31)
+    centers = codes[rng.choice(len(codes), size=800, replace=False)].copy()
+    assert len(codes) * len(centers) * m >= 2**31
+    dev = engine.device_of()
+    dt = engine.device_tables(tables, dev)
+    with torch.cuda.device(dev):
+        eng = engine.ShardEngine(engine.upload_codes(codes, m, dev), dt, len(centers), dev)
+        eng.assign(engine.upload_codes(centers, m, dev))
+        labels, sd = eng.labels_host(), eng.sd_host()
+        st = eng.stats.cpu().numpy()
+    assert int(st[_lib.STAT_LOOKUP_BYTES]) == 2
+    expect, exp_sd = oracle.assign_c(codes, centers, tables, want_sd=True)
+    np.testing.assert_array_equal(labels, expect)
+    assert sd.tobytes() == exp_sd.tobytes()

@@ -106,7 +106,7 @@ size_t pqk_assign_workspace_bytes(int64_t n, int64_t k, int32_t m, int32_t l);
 /* Scan tiers of pqk_assign_device.  Mode 0 (default): a 16-bit fixed-point first tier
  * (2-byte table lookups, exact integer sums, certified against the quantisation error)
  * for padded M <= 16 and problems of >= 2^31 lookups, then the fp32 scan over the
- * uncertified list when it is long (>= 1024 codes per SM) and the exact fp64 rescan for
+ * uncertified list when it is long (>= 256 codes per SM) and the exact fp64 rescan for
  * the rest.  Mode 1: the fp32 scan first.  Mode 2: the 16-bit tier at any size.  Mode
  * 3: as 2 with the fp32 list tier for any list length.  Labels and sd_sq are identical
  * in every mode (process-wide setting, for A/B measurement and tests). */

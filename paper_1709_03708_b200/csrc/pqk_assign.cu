@@ -251,7 +251,7 @@ __device__ __forceinline__ void load_rotated(const uint8_t* __restrict__ codes, 
   for (int k = 0; k < W; ++k) out[k] = __funnelshift_r(u[k], u[(k + 1) % W], 8 * rb);
 }
 
-template <int MP, int KC, int C, int NW, int S>
+template <int MP, int KC, int C, int NW, int S, bool LIST = false>
 __global__ void __launch_bounds__((NW + 1) * 32, 1) scan_kernel(const ScanParams p) {
   constexpr int H = KC / 4;       // lanes per code
   constexpr int OWN_W = 32 / H;   // code owners per warp
@@ -341,6 +341,13 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) scan_kernel(const ScanParams
       bc[j] = 0u;
     }
 
+    // list tier: slots past the end of this warp's share of the list are skipped
+    // (warp-uniform), so a short list costs its codes, not the full register capacity
+    int jact = C;
+    if (LIST) {
+      const int rem = end - (base + warp * OWN_W);
+      jact = rem <= 0 ? 0 : min(C, (rem + OWN - 1) / OWN);
+    }
     for (int t = 0; t < nchunks; ++t, ++g) {
       const int st = (int)(g % S);
       const uint32_t ph = (g / S) & 1u;
@@ -356,7 +363,8 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) scan_kernel(const ScanParams
         buf[0][i] = lds128(__byte_perm(cw[0][i >> 2], 0u, 0x4440u | (uint32_t)(i & 3)) * ROW + lcs[i]);
 #pragma unroll
       for (int j = 0; j < C; ++j) {
-        if (j + 1 < C) {
+        if (LIST && j >= jact) break;
+        if (j + 1 < C && (!LIST || j + 1 < jact)) {
 #pragma unroll
           for (int i = 0; i < MP; ++i)
             buf[(j + 1) & 1][i] =
@@ -686,6 +694,9 @@ static int launch_scan_c(int c_need, const ScanParams& p, int grid, int l, cudaS
   const size_t smem = 128 + (size_t)S * l * MP * KC * 4;
   if ((int)smem > di.smem_optin) return fail(PQK_EUNSUPPORTED, "assignment chunk ring exceeds shared memory");
   auto kern = scan_kernel<MP, KC, C, NW, S>;
+  if constexpr (sizeof...(Cs) == 0) {  // the largest variant also serves the list tier
+    if (p.list) kern = scan_kernel<MP, KC, C, NW, S, true>;
+  }
   PQK_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   ProfileEvents& pe = profile_events();
   if (prof && pe.before) PQK_CUDA_TRY(record_profile_event(pe.before, stream));
@@ -917,9 +928,9 @@ extern "C" int pqk_assign_device(const uint8_t* d_codes, int64_t n, int32_t m, i
     PQK_LAUNCH_CHECK("qbuild16_kernel");
   }
   // list tier threshold: below it the exact rescan is cheaper than streaming every chunk
-  // (fp32 list scan: every CTA streams all chunks, so it only beats the exact rescan,
-  // whose cost is per code, for lists of ~1000 codes per SM and more)
-  const int32_t list_min = g_scan_mode == 3 ? 0 : di.sms * 1024;
+  // (fp32 list scan: every CTA streams all chunks, a fixed cost, so it only beats the
+  // exact rescan, whose cost is per code, for lists of ~250 codes per SM and more)
+  const int32_t list_min = g_scan_mode == 3 ? 0 : di.sms * 256;
   const size_t rows_bytes = (size_t)m * l * sizeof(double);
   const bool cta_rescan = rows_bytes <= 96 * 1024;
   if (cta_rescan) {

@@ -43,6 +43,169 @@ __global__ void histogram_kernel(const uint8_t* __restrict__ codes, int64_t n, i
   }
 }
 
+// ---------------------------------------------------------------------------
+// cluster-tiled histogram.  At configs 4/5 the K x M x L table (410 MB / 1.64 GB) is far
+// larger than L2, so every random global atomic of histogram_kernel costs a DRAM sector
+// round trip (config 4 shard: 15.7 ms, 1% of HBM).  Instead the codes are bucketed by
+// cluster tile (T consecutive clusters, T*M*L*4 B of shared memory) with a two-pass
+// counting sort, and one CTA per tile counts its members in shared memory and writes
+// its dense slab of the table (zeros included: no memset).  Counts are integers, so
+// the result is bit-identical to the atomic kernel whatever the order.
+constexpr int kHistTileBytes = 96 * 1024;    // 2 CTAs per SM in the tile pass
+constexpr int kHistMaxBuckets = 40 * 1024;   // shared-memory cursors of the bucket passes
+constexpr int kHistThreads = 512;
+
+// pass 1: cnt[c][b] = members of bucket b among CTA c's contiguous element range
+__global__ void __launch_bounds__(kHistThreads) hbin_count_kernel(const uint32_t* __restrict__ labels, int64_t n,
+                                                                  int64_t per_cta, uint32_t tile, int nb,
+                                                                  uint32_t* __restrict__ cnt) {
+  extern __shared__ uint32_t sc[];
+  for (int b = threadIdx.x; b < nb; b += blockDim.x) sc[b] = 0;
+  __syncthreads();
+  const int64_t lo = blockIdx.x * per_cta, hi = min(n, lo + per_cta);
+  for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) atomicAdd(&sc[__ldg(labels + i) / tile], 1u);
+  __syncthreads();
+  for (int b = threadIdx.x; b < nb; b += blockDim.x) cnt[(int64_t)blockIdx.x * nb + b] = sc[b];
+}
+
+// thread per bucket: cnt[c][b] -> exclusive prefix over c, tot[b] = bucket size
+__global__ void hbin_colscan_kernel(uint32_t* __restrict__ cnt, int ctas, int nb, uint32_t* __restrict__ tot) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= nb) return;
+  uint32_t run = 0;
+#pragma unroll 8
+  for (int c = 0; c < ctas; ++c) {
+    const uint32_t v = cnt[(int64_t)c * nb + b];
+    cnt[(int64_t)c * nb + b] = run;
+    run += v;
+  }
+  tot[b] = run;
+}
+
+// one CTA: base[b] = exclusive prefix of tot over buckets, base[nb] = n (in place: tot -> base)
+__global__ void __launch_bounds__(1024) hbin_scan_kernel(uint32_t* __restrict__ tot, int nb) {
+  __shared__ uint32_t warp_sum[32];
+  const int per = (nb + 1023) / 1024;
+  const int lo = threadIdx.x * per, hi = min(nb, lo + per);
+  uint32_t s = 0;
+  for (int b = lo; b < hi; ++b) s += tot[b];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  uint32_t incl = s;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  if (lane == 31) warp_sum[wid] = incl;
+  __syncthreads();
+  if (wid == 0) {
+    uint32_t w = warp_sum[lane], wi = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(0xffffffffu, wi, o);
+      if (lane >= o) wi += t;
+    }
+    warp_sum[lane] = wi - w;
+  }
+  __syncthreads();
+  uint32_t run = warp_sum[wid] + incl - s;
+  for (int b = lo; b < hi; ++b) {
+    const uint32_t v = tot[b];
+    tot[b] = run;
+    run += v;
+  }
+  if (threadIdx.x == 1023) tot[nb] = run;
+}
+
+// pass 2: scatter records (code words, tile-local label word) into bucket order; CTA c
+// writes into its reserved run base[b] + cnt[c][b] of every bucket.  Every (CTA, bucket)
+// run is an open L2 line until it fills, so the host sizes the CTA count to keep
+// ctas x buckets x 128 B near the L2 size (a spilled partial line costs a DRAM
+// read-modify-write: 8x the algorithmic traffic at config 4 with 296 CTAs).
+__global__ void __launch_bounds__(1024) hbin_scatter_kernel(
+    const uint8_t* __restrict__ codes, int mw, const uint32_t* __restrict__ labels, int64_t n, int64_t per_cta,
+    uint32_t tile, int nb, const uint32_t* __restrict__ cnt, const uint32_t* __restrict__ base,
+    uint32_t* __restrict__ rec) {
+  extern __shared__ uint32_t cur[];
+  for (int b = threadIdx.x; b < nb; b += blockDim.x) cur[b] = base[b] + cnt[(int64_t)blockIdx.x * nb + b];
+  __syncthreads();
+  const int64_t lo = blockIdx.x * per_cta, hi = min(n, lo + per_cta);
+  const uint32_t* cw = reinterpret_cast<const uint32_t*>(codes);
+  const int rw = mw + 1;
+  if (mw == 1) {  // 4-byte codes: one 8-byte record store
+    uint2* rec2 = reinterpret_cast<uint2*>(rec);
+    constexpr int U = 4;
+    for (int64_t i0 = lo + threadIdx.x; i0 < hi; i0 += (int64_t)U * blockDim.x) {
+      uint32_t k[U], c[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t i = i0 + (int64_t)u * blockDim.x;
+        k[u] = i < hi ? __ldg(labels + i) : 0xffffffffu;
+        c[u] = i < hi ? __ldg(cw + i) : 0u;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (k[u] == 0xffffffffu) continue;
+        const uint32_t b = k[u] / tile;
+        const uint32_t p = atomicAdd(&cur[b], 1u);
+        rec2[p] = make_uint2(c[u], k[u] - b * tile);
+      }
+    }
+    return;
+  }
+  for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+    const uint32_t k = __ldg(labels + i);
+    const uint32_t b = k / tile;
+    const uint32_t p = atomicAdd(&cur[b], 1u);
+    uint32_t* r = rec + (int64_t)p * rw;
+    for (int w = 0; w < mw; ++w) r[w] = __ldg(cw + i * mw + w);
+    r[mw] = k - b * tile;
+  }
+}
+
+// pass 3: one CTA per cluster tile — shared-memory counts, dense slab write, counts[k]
+__global__ void __launch_bounds__(kHistThreads) hbin_tile_kernel(
+    const uint32_t* __restrict__ rec, int mw, const uint32_t* __restrict__ base,
+    int tile, int64_t k, int m, int l, uint32_t* __restrict__ hist, uint32_t* __restrict__ counts) {
+  extern __shared__ uint32_t sh[];
+  const int b = blockIdx.x;
+  const int64_t k0 = (int64_t)b * tile;
+  const int tk = (int)min((int64_t)tile, k - k0);
+  const int row = m * l;  // entries per cluster
+  const int ent = tk * row;
+  for (int e = threadIdx.x; e < ent; e += blockDim.x) sh[e] = 0;
+  __syncthreads();
+  const uint32_t lo = base[b], hi = base[b + 1];
+  const int rw = mw + 1;
+  for (int64_t p = lo + threadIdx.x; p < hi; p += blockDim.x) {
+    const uint32_t* r = rec + p * rw;
+    uint32_t* hk = sh + (int)r[mw] * row;
+    for (int w = 0; 4 * w < m; ++w) {
+      const uint32_t c = r[w];
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (4 * w + q < m) atomicAdd(&hk[(4 * w + q) * l + ((c >> (8 * q)) & 0xffu)], 1u);
+    }
+  }
+  __syncthreads();
+  uint32_t* dst = hist + k0 * row;
+  if ((row & 3) == 0) {
+    const uint4* s4 = reinterpret_cast<const uint4*>(sh);
+    uint4* d4 = reinterpret_cast<uint4*>(dst);
+    for (int e = threadIdx.x; e < ent / 4; e += blockDim.x) d4[e] = s4[e];
+  } else {
+    for (int e = threadIdx.x; e < ent; e += blockDim.x) dst[e] = sh[e];
+  }
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int t = wid; t < tk; t += blockDim.x >> 5) {
+    uint32_t c = 0;
+    for (int s = lane; s < l; s += 32) c += sh[t * row + s];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if (lane == 0) counts[k0 + t] = c;
+  }
+}
+
 // counts[k] = sum_s hist[k][0][s] (clustering.py:458's bincount): one warp per cluster,
 // no contended per-cluster atomics in the histogram pass
 __global__ void counts_from_hist_kernel(const uint32_t* __restrict__ hist, int64_t k, int m, int l,
@@ -699,6 +862,23 @@ static int run_select(const double* d_sd, int64_t n, int64_t base, const int64_t
 
 using namespace pqk;
 
+// stream-ordered allocations (cudaMallocAsync: valid inside a CUDA-graph capture) keep
+// their freed blocks in the device's default pool (no OS round trip per call)
+static int keep_default_pool() {
+  static bool kept[64] = {};
+  int dev = 0;
+  PQK_CUDA_TRY(cudaGetDevice(&dev));
+  if (!kept[dev & 63]) {
+    cudaMemPool_t pool;
+    PQK_CUDA_TRY(cudaDeviceGetDefaultMemPool(&pool, dev));
+    uint64_t keep = UINT64_MAX;
+    PQK_CUDA_TRY(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+    kept[dev & 63] = true;
+  }
+  return PQK_OK;
+}
+
+
 
 extern "C" int pqk_histogram_device(const uint8_t* d_codes, int64_t n, int32_t m, int32_t l,
                                     const uint32_t* d_labels, int64_t k, uint32_t* d_hist, uint32_t* d_counts,
@@ -707,6 +887,62 @@ extern "C" int pqk_histogram_device(const uint8_t* d_codes, int64_t n, int32_t m
   const int mp = padded_m(m);
   if (mp == 0 || l < 1 || l > kMaxL || k < 1 || n < 0) return fail(PQK_EINVAL, "pqk_histogram_device: bad arguments");
   if (n > (int64_t)UINT32_MAX) return fail(PQK_EUNSUPPORTED, "pqk_histogram_device: n must be < 2^32 (uint32 counts)");
+  const int tile = std::min(255, std::max(1, kHistTileBytes / (m * l * 4)));
+  const int64_t nb = (k + tile - 1) / tile;
+  // PQK_HIST_MODE=atomic|tiled forces a path (tests, tools/diag_hist.py); by default tables
+  // that stay L2 resident (config 2's 41 MB) use the plain atomics, which are faster there
+  static const int mode = [] {
+    const char* e = getenv("PQK_HIST_MODE");
+    return !e ? 0 : (e[0] == 'a' ? 1 : (e[0] == 't' ? 2 : 0));
+  }();
+  const bool small_table = (double)k * m * l * 4 <= 64.0 * (1 << 20);
+  const bool tiled_ok = nb <= kHistMaxBuckets && (int64_t)m * l * 4 <= kHistTileBytes;
+  if (tiled_ok && (mode == 2 || (mode == 0 && !small_table))) {
+    const DevInfo& di = dev_info();
+    const int nbi = (int)nb;
+    // open-line budget of the scatter: ctas x buckets x 128 B <= frontier
+    static const double frontier = [] {
+      const char* e = getenv("PQK_HIST_FRONTIER_MB");
+      return (e ? atof(e) : 96.0) * (1 << 20);
+    }();
+    // (measured at config 4, 4167 buckets: 47 CTAs 4.7 ms scatter, 188 CTAs 3.9 ms, 296 CTAs
+    // 8.1 ms with 13 GB of DRAM read-modify-write; the scatter is store-transaction bound)
+    const int ctas = (int)std::max<int64_t>(di.sms, std::min<int64_t>(di.sms * 2, (int64_t)(frontier / (128.0 * nbi))));
+    const int mw = mp / 4;
+    const int64_t per_cta = std::max<int64_t>((n + ctas - 1) / ctas, 1);
+    const size_t cnt_b = align_up((size_t)ctas * nbi * 4, 256), base_b = align_up((size_t)(nbi + 1) * 4, 256);
+    const size_t rec_b = align_up((size_t)std::max<int64_t>(n, 1) * (mw + 1) * 4, 256);
+    { const int _rc = keep_default_pool(); if (_rc != PQK_OK) return _rc; }
+    uint8_t* ws = nullptr;
+    PQK_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&ws), cnt_b + base_b + rec_b, stream));
+    uint32_t* cnt = reinterpret_cast<uint32_t*>(ws);
+    uint32_t* base = reinterpret_cast<uint32_t*>(ws + cnt_b);
+    uint32_t* rec = reinterpret_cast<uint32_t*>(ws + cnt_b + base_b);
+    const size_t sm_nb = (size_t)nbi * 4;
+    static int smem_set[64] = {};
+    int dev = 0;
+    PQK_CUDA_TRY(cudaGetDevice(&dev));
+    if (!smem_set[dev & 63]) {
+      PQK_CUDA_TRY(cudaFuncSetAttribute(hbin_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kHistMaxBuckets * 4));
+      PQK_CUDA_TRY(cudaFuncSetAttribute(hbin_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kHistMaxBuckets * 4));
+      PQK_CUDA_TRY(cudaFuncSetAttribute(hbin_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kHistTileBytes));
+      smem_set[dev & 63] = 1;
+    }
+    hbin_count_kernel<<<ctas, kHistThreads, sm_nb, stream>>>(d_labels, n, per_cta, (uint32_t)tile, nbi, cnt);
+    PQK_LAUNCH_CHECK("hbin_count_kernel");
+    hbin_colscan_kernel<<<(nbi + 255) / 256, 256, 0, stream>>>(cnt, ctas, nbi, base);
+    PQK_LAUNCH_CHECK("hbin_colscan_kernel");
+    hbin_scan_kernel<<<1, 1024, 0, stream>>>(base, nbi);
+    PQK_LAUNCH_CHECK("hbin_scan_kernel");
+    hbin_scatter_kernel<<<ctas, 1024, sm_nb, stream>>>(d_codes, mw, d_labels, n, per_cta, (uint32_t)tile, nbi, cnt,
+                                                       base, rec);
+    PQK_LAUNCH_CHECK("hbin_scatter_kernel");
+    hbin_tile_kernel<<<nbi, kHistThreads, (size_t)tile * m * l * 4, stream>>>(rec, mw, base, tile, k, m, l, d_hist,
+                                                                             d_counts);
+    PQK_LAUNCH_CHECK("hbin_tile_kernel");
+    PQK_CUDA_TRY(cudaFreeAsync(ws, stream));
+    return PQK_OK;
+  }
   PQK_CUDA_TRY(cudaMemsetAsync(d_hist, 0, (size_t)k * m * l * sizeof(int32_t), stream));
   if (n > 0) {
     const DevInfo& di = dev_info();
@@ -734,16 +970,7 @@ extern "C" int pqk_vote_device(const uint32_t* d_hist, const uint32_t* d_counts,
   // stream-ordered memory (cudaMallocAsync: also valid inside a CUDA-graph capture)
   __half* t16 = nullptr;
   if (d_t32 && l == 256) {
-    static bool pool_kept[64] = {};
-    int dev = 0;
-    PQK_CUDA_TRY(cudaGetDevice(&dev));
-    if (!pool_kept[dev & 63]) {  // keep freed blocks in the pool (no OS round trip per call)
-      cudaMemPool_t pool;
-      PQK_CUDA_TRY(cudaDeviceGetDefaultMemPool(&pool, dev));
-      uint64_t keep = UINT64_MAX;
-      PQK_CUDA_TRY(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
-      pool_kept[dev & 63] = true;
-    }
+    { const int _rc = keep_default_pool(); if (_rc != PQK_OK) return _rc; }
     PQK_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&t16), (size_t)m * l * l * sizeof(__half), stream));
     vote_t16_kernel<<<m, 1024, 0, stream>>>(d_t32, l, t16);
     PQK_LAUNCH_CHECK("vote_t16_kernel");

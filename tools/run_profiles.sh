@@ -3,7 +3,7 @@
 # the config-2 launch list and one ncu --set full capture of the first-tier scan kernel.
 # Each ncu command runs only after the same command exited 0 without ncu.
 set -u
-out=gpurun_out/prof
+out=gpurun_out/${PROF_OUT:-prof}
 mkdir -p $out
 for c in c2 c1 c5 c3 c4; do
   steps=5; [ $c = c4 ] && steps=2

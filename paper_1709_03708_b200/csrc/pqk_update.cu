@@ -286,15 +286,22 @@ __device__ __forceinline__ void warp_best(Best& b) {
 }
 
 // fp16 copy of the fp32 filter tables for the vote's first stage (half the L2 bytes per
-// support row): block per subspace, T16 = fp16(T32 * 2^f) with max * 2^f < 2^15.
+// support row): T16 = fp16(T32 * 2^f) with max * 2^f < 2^15 per subspace.  Grid
+// (kT16Slices, m): every block of a subspace reduces the whole subspace maximum (256 KB of
+// L2 reads, float4) and converts its slice (one block per subspace took 49 us per call).
+constexpr int kT16Slices = 32;
 __global__ void __launch_bounds__(1024) vote_t16_kernel(const float* __restrict__ t32, int l, __half* __restrict__ t16) {
   __shared__ float s_red[32];
   __shared__ int s_f;
-  const float* src = t32 + (size_t)blockIdx.x * l * l;
-  __half* dst = t16 + (size_t)blockIdx.x * l * l;
-  const int ll = l * l;
+  const float* src = t32 + (size_t)blockIdx.y * l * l;
+  __half* dst = t16 + (size_t)blockIdx.y * l * l;
+  const int ll = l * l;  // l == 256: a multiple of 4 * kT16Slices
   float mx = 0.0f;
-  for (int i = threadIdx.x; i < ll; i += blockDim.x) mx = fmaxf(mx, src[i]);
+  const float4* s4 = reinterpret_cast<const float4*>(src);
+  for (int i = threadIdx.x; i < ll / 4; i += blockDim.x) {
+    const float4 v = __ldg(s4 + i);
+    mx = fmaxf(fmaxf(mx, fmaxf(v.x, v.y)), fmaxf(v.z, v.w));
+  }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
   if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = mx;
@@ -311,7 +318,9 @@ __global__ void __launch_bounds__(1024) vote_t16_kernel(const float* __restrict_
   }
   __syncthreads();
   const int f = s_f;
-  for (int i = threadIdx.x; i < ll; i += blockDim.x) dst[i] = __float2half_rn(ldexpf(src[i], f));
+  const int per = ll / kT16Slices;
+  for (int i = blockIdx.x * per + threadIdx.x; i < (blockIdx.x + 1) * per; i += blockDim.x)
+    dst[i] = __float2half_rn(ldexpf(src[i], f));
 }
 
 __global__ void __launch_bounds__(32 * kVoteWarps) vote_kernel(const uint32_t* __restrict__ hist,
@@ -972,7 +981,7 @@ extern "C" int pqk_vote_device(const uint32_t* d_hist, const uint32_t* d_counts,
   if (d_t32 && l == 256) {
     { const int _rc = keep_default_pool(); if (_rc != PQK_OK) return _rc; }
     PQK_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&t16), (size_t)m * l * l * sizeof(__half), stream));
-    vote_t16_kernel<<<m, 1024, 0, stream>>>(d_t32, l, t16);
+    vote_t16_kernel<<<dim3(kT16Slices, m), 1024, 0, stream>>>(d_t32, l, t16);
     PQK_LAUNCH_CHECK("vote_t16_kernel");
   }
   vote_kernel<<<(unsigned)((k * m + kVoteWarps - 1) / kVoteWarps), 32 * kVoteWarps, 0, stream>>>(

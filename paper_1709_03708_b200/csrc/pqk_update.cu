@@ -323,11 +323,115 @@ __global__ void __launch_bounds__(1024) vote_t16_kernel(const float* __restrict_
     dst[i] = __float2half_rn(ldexpf(src[i], f));
 }
 
+// fp16 first stage with the subspace's table staged in shared memory (l = 256).  Grid
+// (CTAs per subspace, m): a CTA copies T16[m] (128 KB) once and its 32 warps vote rows
+// (k, m) of a contiguous k range, so every support row is a conflict-free 512-byte
+// shared read instead of an L2 read (the L2-bound warp-per-row kernel took 96 us at
+// config 2).  Same arithmetic and certificate as vote_kernel's fp16 stage; rows it
+// cannot certify are left to vote_kernel (done[row] = 0), which goes straight to fp64.
+constexpr int kV16Warps = 32;
+constexpr size_t kV16Smem = 256 * 256 * sizeof(__half) + (size_t)kV16Warps * 256 * 8;
+__global__ void __launch_bounds__(32 * kV16Warps, 1) vote16_smem_kernel(
+    const uint32_t* __restrict__ hist, const uint32_t* __restrict__ counts, int64_t k, int m, int mp,
+    const __half* __restrict__ t16, int64_t rows_per_cta, uint8_t* __restrict__ newc, uint8_t* __restrict__ done,
+    unsigned long long* __restrict__ acc) {
+  constexpr int l = 256;
+  extern __shared__ __align__(16) uint8_t v16_smem[];
+  __half* th = reinterpret_cast<__half*>(v16_smem);
+  int* s_s_all = reinterpret_cast<int*>(v16_smem + 256 * 256 * sizeof(__half));
+  uint32_t* s_h_all = reinterpret_cast<uint32_t*>(s_s_all + kV16Warps * 256);
+  __shared__ unsigned long long s_acc[2];
+  const int mm = blockIdx.y;
+  {
+    const uint4* src = reinterpret_cast<const uint4*>(t16 + (size_t)mm * l * l);
+    uint4* dst = reinterpret_cast<uint4*>(th);
+    for (int i = threadIdx.x; i < l * l / 8; i += blockDim.x) dst[i] = __ldg(src + i);
+    if (threadIdx.x < 2) s_acc[threadIdx.x] = 0;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int* ss = s_s_all + warp * 256;
+  uint32_t* sh = s_h_all + warp * 256;
+  const int64_t k_lo = blockIdx.x * rows_per_cta, k_hi = min(k, k_lo + rows_per_cta);
+  const double inf = __longlong_as_double(0x7ff0000000000000LL);
+  unsigned long long my_nnz = 0, my_fail = 0;
+  for (int64_t kk = k_lo + warp; kk < k_hi; kk += kV16Warps) {
+    const int64_t gw = (int64_t)mm * k + kk;
+    if (counts[kk] == 0) {
+      if (lane == 0) done[gw] = 1;
+      continue;
+    }
+    const uint32_t* hrow = hist + (kk * m + mm) * l;
+    uint32_t hv[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) hv[i] = hrow[32 * i + lane];
+    int nnz = 0;
+    unsigned long long hs = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const uint32_t h = hv[i];
+      hs += h;
+      const unsigned bal = __ballot_sync(0xffffffffu, h != 0);
+      if (h) {
+        const int pos = nnz + __popc(bal & ((1u << lane) - 1u));
+        ss[pos] = 32 * i + lane;
+        sh[pos] = h;
+      }
+      nnz += __popc(bal);
+    }
+    __syncwarp();
+    float v[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = 0.0f;
+    for (int j = 0; j < nnz; ++j) {
+      const float h = __uint2float_rn(sh[j]);
+      const uint4 raw = *(reinterpret_cast<const uint4*>(th + ss[j] * l) + lane);
+      const __half2* hp = reinterpret_cast<const __half2*>(&raw);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float2 f2 = __half22float2(hp[i]);
+        v[2 * i] = __fmaf_rn(h, f2.x, v[2 * i]);
+        v[2 * i + 1] = __fmaf_rn(h, f2.y, v[2 * i + 1]);
+      }
+    }
+    __syncwarp();  // ss/sh are rewritten by the next row
+    Best b{inf, 0, inf};
+#pragma unroll
+    for (int i = 0; i < 8; ++i) b = merge_best(b, Best{(double)v[i], 8 * lane + i, inf});
+    warp_best(b);
+    const double eps = 4.8828125e-04 + (double)(nnz + 4) * 5.9604644775390625e-08 + 9.5367431640625e-07;
+    unsigned long long ht = hs;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ht += __shfl_xor_sync(0xffffffffu, ht, o);
+    const double hsum = (double)ht;
+    const bool ok = (b.v2 - b.v1) > eps * (b.v1 + b.v2) + 1.1920928955078125e-07 * hsum;
+    if (lane == 0) {
+      if (ok) {
+        newc[kk * mp + mm] = (uint8_t)b.l1;
+        my_nnz += (unsigned long long)nnz;  // rows left to vote_kernel count their nnz there
+      } else {
+        ++my_fail;
+      }
+      done[gw] = ok ? 1 : 0;
+    }
+  }
+  if (lane == 0 && (my_nnz | my_fail)) {
+    atomicAdd(&s_acc[0], my_nnz);
+    atomicAdd(&s_acc[1], my_fail);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (s_acc[0]) atomicAdd(&acc[0], s_acc[0]);
+    if (s_acc[1]) atomicAdd(&acc[3], s_acc[1]);
+  }
+}
+
 __global__ void __launch_bounds__(32 * kVoteWarps) vote_kernel(const uint32_t* __restrict__ hist,
                                                                const uint32_t* __restrict__ counts, int64_t k, int m,
                                                                int l, int mp, const double* __restrict__ t64,
                                                                const float* __restrict__ t32,
                                                                const __half* __restrict__ t16,
+                                                               const uint8_t* __restrict__ done,
                                                                uint8_t* __restrict__ newc,
                                                                unsigned long long* __restrict__ acc) {
   __shared__ int s_s[kVoteWarps][kMaxL];
@@ -337,7 +441,8 @@ __global__ void __launch_bounds__(32 * kVoteWarps) vote_kernel(const uint32_t* _
   if (gw >= k * m) return;
   const int mm = (int)(gw / k);
   const int64_t kk = gw - (int64_t)mm * k;
-  if (counts[kk] == 0) return;  // empty: left 0, repaired later
+  if (done && done[gw]) return;  // decided by vote16_smem_kernel
+  if (counts[kk] == 0) return;   // empty: left 0, repaired later
   int* ss = s_s[warp];
   uint32_t* sh = s_h[warp];
   const uint32_t* hrow = hist + (kk * m + mm) * l;
@@ -984,10 +1089,28 @@ extern "C" int pqk_vote_device(const uint32_t* d_hist, const uint32_t* d_counts,
     vote_t16_kernel<<<dim3(kT16Slices, m), 1024, 0, stream>>>(d_t32, l, t16);
     PQK_LAUNCH_CHECK("vote_t16_kernel");
   }
+  uint8_t* done = nullptr;
+  if (t16) {
+    // fp16 stage from shared-memory tables; vote_kernel then takes the uncertified rows to fp64
+    static int attr_v16[64] = {};
+    int dev = 0;
+    PQK_CUDA_TRY(cudaGetDevice(&dev));
+    if (!attr_v16[dev & 63]) {
+      PQK_CUDA_TRY(cudaFuncSetAttribute(vote16_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kV16Smem));
+      attr_v16[dev & 63] = 1;
+    }
+    PQK_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&done), (size_t)k * m, stream));
+    const int per = std::max(1, dev_info().sms / m);
+    const int64_t rows = (k + per - 1) / per;
+    vote16_smem_kernel<<<dim3(per, m), 32 * kV16Warps, kV16Smem, stream>>>(d_hist, d_counts, k, m, mp, t16, rows,
+                                                                           d_new_centers, done, acc);
+    PQK_LAUNCH_CHECK("vote16_smem_kernel");
+  }
   vote_kernel<<<(unsigned)((k * m + kVoteWarps - 1) / kVoteWarps), 32 * kVoteWarps, 0, stream>>>(
-      d_hist, d_counts, k, m, l, mp, d_t64, d_t32, t16, d_new_centers, acc);
+      d_hist, d_counts, k, m, l, mp, d_t64, done ? nullptr : d_t32, done ? nullptr : t16, done, d_new_centers, acc);
   PQK_LAUNCH_CHECK("vote_kernel");
   if (t16) PQK_CUDA_TRY(cudaFreeAsync(t16, stream));
+  if (done) PQK_CUDA_TRY(cudaFreeAsync(done, stream));
   empties_kernel<<<(unsigned)((k + 1023) / 1024), 1024, 0, stream>>>(d_counts, k, acc);
   PQK_LAUNCH_CHECK("empties_kernel");
   vote_stats_kernel<<<1, 1, 0, stream>>>(k, acc, d_stats);

@@ -22,6 +22,7 @@
 #include <cmath>
 
 #include "pqk_common.cuh"
+#include "pqk_tc.cuh"
 
 namespace pqk {
 
@@ -421,6 +422,271 @@ __global__ void __launch_bounds__(32 * kV16Warps, 1) vote16_smem_kernel(
   }
   __syncthreads();
   if (threadIdx.x == 0) {
+    if (s_acc[0]) atomicAdd(&acc[0], s_acc[0]);
+    if (s_acc[1]) atomicAdd(&acc[3], s_acc[1]);
+  }
+}
+
+// Tensor-core first stage (l = 256): votes of 128 clusters x 256 candidates per tcgen05
+// tile, D[r][j] = sum_s A[r][s] B[j][s] with A = the clusters' count rows (fp16, exact:
+// counts < 2048, larger counts split as lo = h & 2047 and hi = h >> 11 into a second TMEM
+// accumulator, v = lo + 2048 hi; tiles with a count >= 2^22 go to vote_kernel whole) and
+// B[j][s] = T16[s][j] (fp16 tables, transposed through shared memory once per CTA).
+// Products are exact in the fp32 accumulator and all addends are nonnegative, so the
+// accumulation error is <= 16 instructions x 17 x 2^-23 x v (the encoder's per-instruction
+// bound, tools/diag_tc_error.py); with the fp16 table rounding the winner is certified
+// when v2 - v1 > eps (v1 + v2) + 2^-23 H, eps = 2^-11 + 272 2^-23 + 2^-20, else the row
+// goes to vote_kernel's fp64 path (done[row] = 0).  The dense contraction replaces the
+// SIMT stage's sum over the support (issue bound: ~1e9 FMAs + conversions at config 2).
+constexpr int kVtcThreads = 256;
+constexpr size_t kVtcSmem = 1024 + 256 * 256 * 2 + 128 * 256 * 2;  // align slack + B + A
+__global__ void __launch_bounds__(kVtcThreads, 1) vote_tc_kernel(
+    const uint32_t* __restrict__ hist, const uint32_t* __restrict__ counts, int64_t k, int m, int mp,
+    const __half* __restrict__ t16, uint8_t* __restrict__ newc, uint8_t* __restrict__ done,
+    unsigned long long* __restrict__ acc) {
+  extern __shared__ __align__(1024) uint8_t vtc_raw[];  // (no-swizzle operands need 16 B alignment)
+  uint8_t* smem = vtc_raw;
+  uint8_t* sb = smem;                  // B: 256 (j) x 256 (s) fp16, K-major canonical
+  uint8_t* sa = smem + 256 * 256 * 2;  // A: 128 (rows) x 256 (s) fp16; staging for the transpose
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tbase;
+  __shared__ uint32_t row_h[128];  // cluster sizes: < 2^32 by the API contract
+  __shared__ int row_nnz[128];
+  __shared__ unsigned long long s_acc[2];
+  __shared__ double ep_v1[128], ep_v2[128];
+  __shared__ int ep_l1[128];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int mm = blockIdx.y;
+  const __half* tsub = t16 + (size_t)mm * 256 * 256;
+  // B = T16^T in two 128-row halves staged row-major in the A buffer
+  for (int half = 0; half < 2; ++half) {
+    const uint4* src = reinterpret_cast<const uint4*>(tsub + (size_t)half * 128 * 256);
+    uint4* stg = reinterpret_cast<uint4*>(sa);
+    for (int i0 = 0; i0 < 128 * 256 / 8; i0 += 8 * kVtcThreads) {  // 8 loads in flight per thread
+      uint4 t[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) t[u] = __ldg(src + i0 + u * kVtcThreads + tid);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) stg[i0 + u * kVtcThreads + tid] = t[u];
+    }
+    __syncthreads();
+    const __half* st = reinterpret_cast<const __half*>(sa);
+    // item (j, g): B[j][s] for s = half*128 + 8g .. +7
+    for (int q = tid; q < 256 * 16; q += kVtcThreads) {
+      const int j = q & 255, g = q >> 8;
+      __align__(16) __half v[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) v[e] = st[(8 * g + e) * 256 + j];
+      *reinterpret_cast<uint4*>(sb + tc::kmajor_off(j, half * 128 + 8 * g, 256)) = *reinterpret_cast<uint4*>(v);
+    }
+    __syncthreads();
+  }
+  if (tid == 0) {
+    mbar_init(&bar, 1);
+    fence_mbar_init();
+    s_acc[0] = 0;
+    s_acc[1] = 0;
+  }
+  if (warp == 0) tc::tmem_alloc(&tbase, 512);
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tacc = tbase;
+  uint32_t phase = 0;
+  unsigned long long my_nnz = 0, my_fail = 0;
+  const int64_t ntiles = (k + 127) / 128;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t k0 = tile * 128;
+    if (tid < 128) {
+      row_h[tid] = 0;
+      row_nnz[tid] = 0;
+    }
+    __syncthreads();
+    // A fill: item (r, g) = 8 counts; lanes 0-7 take 8 rows of one core matrix (conflict-free stores)
+    uint32_t hmax = 0;
+    for (int it0 = 0; it0 < 16; it0 += 8) {  // 8 items (16 loads) in flight per thread
+    uint4 ld[8][2];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int q = (it0 + u) * kVtcThreads + tid;
+      const int wq = q >> 5, ln = q & 31;
+      const int r = (wq & 15) * 8 + (ln & 7), g = (wq >> 4) * 4 + (ln >> 3);
+      const int64_t kk = k0 + r;
+      ld[u][0] = ld[u][1] = make_uint4(0u, 0u, 0u, 0u);
+      if (kk < k) {
+        const uint4* src = reinterpret_cast<const uint4*>(hist + (kk * m + mm) * 256 + 8 * g);
+        ld[u][0] = __ldg(src);
+        ld[u][1] = __ldg(src + 1);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int q = (it0 + u) * kVtcThreads + tid;
+      const int wq = q >> 5, ln = q & 31;
+      const int r = (wq & 15) * 8 + (ln & 7), g = (wq >> 4) * 4 + (ln >> 3);
+      const uint4 a = ld[u][0], b = ld[u][1];
+      const uint32_t h[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+      uint32_t hs = 0;
+      int nz = 0;
+      __align__(16) __half v[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        hs += h[e];
+        nz += h[e] != 0;
+        hmax = max(hmax, h[e]);
+        v[e] = __uint2half_rn(h[e] & 2047u);
+      }
+      *reinterpret_cast<uint4*>(sa + tc::kmajor_off(r, 8 * g, 256)) = *reinterpret_cast<uint4*>(v);
+      // lanes l, l+8, l+16, l+24 share row r: combine, then one shared atomic per row
+      hs += __shfl_xor_sync(0xffffffffu, hs, 8);
+      hs += __shfl_xor_sync(0xffffffffu, hs, 16);
+      nz += __shfl_xor_sync(0xffffffffu, nz, 8);
+      nz += __shfl_xor_sync(0xffffffffu, nz, 16);
+      if (ln < 8 && hs) {
+        atomicAdd(&row_h[r], hs);
+        atomicAdd(&row_nnz[r], nz);
+      }
+    }
+    }
+    const int need_hi = __syncthreads_or(hmax >= 2048u);
+    const int too_big = __syncthreads_or(hmax >= (1u << 22));
+    if (too_big) {  // the whole tile to vote_kernel
+      if (tid < 128 && k0 + tid < k) {
+        const int64_t kk = k0 + tid;
+        const bool filled = counts[kk] != 0;
+        done[(int64_t)mm * k + kk] = filled ? 0 : 1;
+        my_fail += filled;
+      }
+      __syncthreads();
+      continue;
+    }
+    for (int pass = 0; pass < 1 + need_hi; ++pass) {
+      if (pass == 1) {  // refill A with the high parts (the lo MMAs have completed)
+        for (int it = 0; it < 16; ++it) {
+          const int q = it * kVtcThreads + tid;
+          const int wq = q >> 5, ln = q & 31;
+          const int r = (wq & 15) * 8 + (ln & 7), g = (wq >> 4) * 4 + (ln >> 3);
+          const int64_t kk = k0 + r;
+          uint32_t h[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+          if (kk < k) {
+            const uint4* src = reinterpret_cast<const uint4*>(hist + (kk * m + mm) * 256 + 8 * g);
+            const uint4 a = __ldg(src), b = __ldg(src + 1);
+            h[0] = a.x; h[1] = a.y; h[2] = a.z; h[3] = a.w; h[4] = b.x; h[5] = b.y; h[6] = b.z; h[7] = b.w;
+          }
+          __align__(16) __half v[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) v[e] = __uint2half_rn(h[e] >> 11);
+          *reinterpret_cast<uint4*>(sa + tc::kmajor_off(r, 8 * g, 256)) = *reinterpret_cast<uint4*>(v);
+        }
+      }
+      tc::fence_proxy_async();
+      tc::fence_before();
+      __syncthreads();
+      tc::fence_after();
+      if (tid == 0) {
+        const uint32_t a0 = smem_u32(sa), b0 = smem_u32(sb);
+        for (int st = 0; st < 16; ++st)
+          tc::mma_f16(tacc + 256 * pass, tc::smem_desc(a0 + st * 256, 128, 4096), tc::smem_desc(b0 + st * 256, 128, 4096),
+                      tc::idesc_f16_f32(128, 256), st > 0 ? 1u : 0u);
+        tc::commit(&bar);
+      }
+      mbar_wait(&bar, phase);
+      phase ^= 1u;
+      tc::fence_after();
+    }
+    {
+      // warp w reads TMEM lanes 32 (w & 3) .. +31 and candidate columns 128 (w >> 2) .. +127
+      const int r = 32 * (warp & 3) + lane, chalf = warp >> 2;
+      const uint32_t lrow = tacc + ((uint32_t)(32 * (warp & 3)) << 16) + 128 * chalf;
+      double v1, v2;
+      int l1;
+      if (!need_hi) {  // nonnegative fp32: the bit patterns order as uint32
+        uint32_t b1 = 0xffffffffu, b2 = 0xffffffffu;
+        int i1 = 0;
+        for (int c0 = 0; c0 < 128; c0 += 16) {
+          uint32_t lo[16];
+          tc::tmem_ld16(lrow + c0, lo);
+          tc::tmem_wait_ld();
+#pragma unroll
+          for (int e = 0; e < 16; ++e) {
+            const uint32_t x = lo[e];
+            b2 = min(b2, max(b1, x));  // second smallest (ties keep the lower index as b1)
+            if (x < b1) i1 = c0 + e;
+            b1 = min(b1, x);
+          }
+        }
+        v1 = (double)__uint_as_float(b1);
+        v2 = (double)__uint_as_float(b2);
+        l1 = 128 * chalf + i1;
+      } else {
+        v1 = __longlong_as_double(0x7ff0000000000000LL);
+        v2 = v1;
+        l1 = 0;
+        for (int c0 = 0; c0 < 128; c0 += 16) {
+          uint32_t lo[16], hi[16];
+          tc::tmem_ld16(lrow + c0, lo);
+          tc::tmem_ld16(lrow + 256 + c0, hi);
+          tc::tmem_wait_ld();
+#pragma unroll
+          for (int e = 0; e < 16; ++e) {
+            const double v = (double)__uint_as_float(lo[e]) + 2048.0 * (double)__uint_as_float(hi[e]);
+            if (v < v1) {
+              v2 = v1;
+              v1 = v;
+              l1 = 128 * chalf + c0 + e;
+            } else if (v < v2) {
+              v2 = v;
+            }
+          }
+        }
+      }
+      if (chalf == 1) {
+        ep_v1[r] = v1;
+        ep_v2[r] = v2;
+        ep_l1[r] = l1;
+      }
+      __syncthreads();
+      if (chalf == 0) {
+        // merge with the upper half (higher indices: it wins only when strictly smaller)
+        const double w1 = ep_v1[r], w2 = ep_v2[r];
+        if (w1 < v1) {
+          v2 = fmin(v1, w2);
+          v1 = w1;
+          l1 = ep_l1[r];
+        } else {
+          v2 = fmin(v2, w1);
+        }
+        const int64_t kk = k0 + r;
+        if (kk < k) {
+          const int64_t gw = (int64_t)mm * k + kk;
+          if (counts[kk] == 0) {
+            done[gw] = 1;
+          } else {
+            const double eps = 4.8828125e-04 + 272.0 * 1.1920928955078125e-07 + 9.5367431640625e-07;
+            const bool ok = (v2 - v1) > eps * (v1 + v2) + 1.1920928955078125e-07 * (double)row_h[r];
+            if (ok) {
+              newc[kk * mp + mm] = (uint8_t)l1;
+              my_nnz += (unsigned long long)row_nnz[r];
+            } else {
+              ++my_fail;
+            }
+            done[gw] = ok ? 1 : 0;
+          }
+        }
+      }
+    }
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+  }
+  if (my_nnz | my_fail) {
+    atomicAdd(&s_acc[0], my_nnz);
+    atomicAdd(&s_acc[1], my_fail);
+  }
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 0) tc::tmem_dealloc(tacc, 512);
+  if (tid == 0) {
     if (s_acc[0]) atomicAdd(&acc[0], s_acc[0]);
     if (s_acc[1]) atomicAdd(&acc[3], s_acc[1]);
   }
@@ -1097,14 +1363,27 @@ extern "C" int pqk_vote_device(const uint32_t* d_hist, const uint32_t* d_counts,
     PQK_CUDA_TRY(cudaGetDevice(&dev));
     if (!attr_v16[dev & 63]) {
       PQK_CUDA_TRY(cudaFuncSetAttribute(vote16_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kV16Smem));
+      PQK_CUDA_TRY(cudaFuncSetAttribute(vote_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kVtcSmem));
       attr_v16[dev & 63] = 1;
     }
     PQK_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&done), (size_t)k * m, stream));
     const int per = std::max(1, dev_info().sms / m);
-    const int64_t rows = (k + per - 1) / per;
-    vote16_smem_kernel<<<dim3(per, m), 32 * kV16Warps, kV16Smem, stream>>>(d_hist, d_counts, k, m, mp, t16, rows,
-                                                                           d_new_centers, done, acc);
-    PQK_LAUNCH_CHECK("vote16_smem_kernel");
+    static const bool simt = [] {
+      const char* e = getenv("PQK_VOTE_SIMT");
+      return e && e[0] == '1';
+    }();
+    if (simt) {
+      const int64_t rows = (k + per - 1) / per;
+      vote16_smem_kernel<<<dim3(per, m), 32 * kV16Warps, kV16Smem, stream>>>(d_hist, d_counts, k, m, mp, t16, rows,
+                                                                             d_new_centers, done, acc);
+      PQK_LAUNCH_CHECK("vote16_smem_kernel");
+    } else {
+      const int64_t tiles = (k + 127) / 128;
+      const int per_tc = (int)std::min<int64_t>(per, tiles);
+      vote_tc_kernel<<<dim3(per_tc, m), kVtcThreads, kVtcSmem, stream>>>(d_hist, d_counts, k, m, mp, t16,
+                                                                          d_new_centers, done, acc);
+      PQK_LAUNCH_CHECK("vote_tc_kernel");
+    }
   }
   vote_kernel<<<(unsigned)((k * m + kVoteWarps - 1) / kVoteWarps), 32 * kVoteWarps, 0, stream>>>(
       d_hist, d_counts, k, m, l, mp, d_t64, done ? nullptr : d_t32, done ? nullptr : t16, done, d_new_centers, acc);

@@ -126,13 +126,15 @@ def test_fit_parity_forced(lib, oracle):
     assert [s.objective for s in res.trace] == [t["objective"] for t in ref["trace"]]
 
 
-@pytest.mark.parametrize("kind", ["random", "lattice", "scaled", "heavy"])
+@pytest.mark.parametrize("kind", ["random", "lattice", "scaled", "heavy", "huge", "empty_rows"])
 def test_vote_fp16_stage(oracle, kind):
-    """The vote's fp16 first stage (L = 256) decides the exact-arithmetic argmin
-    (clustering.py:349-354, lowest j on ties) or hands over to the fp64 stages."""
+    """The vote's tensor-core first stage (L = 256) decides the exact-arithmetic argmin
+    (clustering.py:349-354, lowest j on ties) or hands over to the fp64 stages: counts
+    < 2048 (one accumulator), heavy counts (lo/hi split), counts >= 2^22 (tile handed
+    over whole), and empty clusters between filled ones; 600 clusters = 5 row tiles."""
     from paper_1709_03708_b200 import engine
 
-    rng = np.random.default_rng({"random": 1, "lattice": 2, "scaled": 3, "heavy": 4}[kind])
+    rng = np.random.default_rng({"random": 1, "lattice": 2, "scaled": 3, "heavy": 4, "huge": 5, "empty_rows": 6}[kind])
     m, l_count, k = 2, 256, 600
     if kind == "lattice":
         tables = lattice_tables(m, l_count)  # integer distances: exact ties are common
@@ -145,10 +147,16 @@ def test_vote_fp16_stage(oracle, kind):
         for mm in range(m):
             nnz = int(rng.integers(1, 40))
             sup = rng.choice(l_count, size=nnz, replace=False)
-            hi = 10**6 if kind == "heavy" else 50
+            hi = {"heavy": 10**6, "huge": 2**26}.get(kind, 50)
             hist[kk, mm, sup] = rng.integers(1, hi, size=nnz)
+    if kind == "huge":
+        hist[::3] %= 5000  # tiles mixing small, split and too-large counts
+    if kind == "empty_rows":
+        hist[rng.random(k) < 0.4] = 0
     got = engine.vote_host(hist, tables)
     for kk in range(k):
+        if not hist[kk].any():
+            continue  # empty cluster: left for the repair
         for mm in range(m):
             assert got[kk, mm] == oracle.vote_argmin(hist[kk, mm], tables[mm]), (kk, mm)
 

@@ -679,7 +679,12 @@ __global__ void __launch_bounds__(kVtcThreads, 1) vote_tc_kernel(
     __syncthreads();
     tc::fence_after();
   }
-  if (my_nnz | my_fail) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {  // one shared atomic per warp (a 64-bit CAS loop each)
+    my_nnz += __shfl_xor_sync(0xffffffffu, my_nnz, o);
+    my_fail += __shfl_xor_sync(0xffffffffu, my_fail, o);
+  }
+  if (lane == 0 && (my_nnz | my_fail)) {
     atomicAdd(&s_acc[0], my_nnz);
     atomicAdd(&s_acc[1], my_fail);
   }

@@ -356,7 +356,7 @@ class ShardEngine:
 
 class IterationGraphs:
     """The device part of a Lloyd iteration as two CUDA graphs, replayed every iteration:
-    ``main`` = assign(cur) -> objective sums -> histogram -> vote (~15 kernel launches),
+    ``main`` = assign(cur) -> [objective sums || histogram -> vote] (~15 kernel launches),
     ``repair`` = the empty-cluster repair (~30 launches of the 12-digit radix select).
     ``cur`` is a fixed (K, MP) centers buffer; the caller refreshes it with
     ``cur.copy_(eng.new_centers)`` between replays.  Capture after one eager iteration
@@ -371,12 +371,22 @@ class IterationGraphs:
         lib = _lib.load()
         self.main = torch.cuda.CUDAGraph()
         l0 = lib.pqk_launch_count()
+        side = torch.cuda.Stream(device=eng.dev)
         with torch.cuda.graph(self.main, capture_error_mode="thread_local"):
             eng.assign(cur)
             self.ev_assigned.record()
-            eng.objective()
+            # the objective sums (a latency-bound tree) run on a parallel branch of the graph,
+            # beside the histogram and the vote; they share no buffers
+            fork = torch.cuda.Event()
+            fork.record()
+            side.wait_event(fork)
+            with torch.cuda.stream(side):
+                eng.objective()
+            join = torch.cuda.Event()
+            join.record(side)
             eng.histogram()
             eng.vote()
+            torch.cuda.current_stream(eng.dev).wait_event(join)
         self.main_launches = int(lib.pqk_launch_count() - l0)
         self.repair = torch.cuda.CUDAGraph()
         l0 = lib.pqk_launch_count()

@@ -17,3 +17,6 @@ echo "launch list rc=$?" >> $out/status.txt
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:hscan_kernel -s 2 -c 1 \
   -o $out/ncu_hscan_c2 python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > $out/ncu_full.log 2>&1
 echo "ncu full rc=$?" >> $out/status.txt
+timeout 600 ncu --set full --import-source on --clock-control none -k regex:vote_tc_kernel -s 2 -c 1 \
+  -o $out/ncu_vote_tc_c2 python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > $out/ncu_vote.log 2>&1
+echo "ncu vote rc=$?" >> $out/status.txt

@@ -920,12 +920,31 @@ extern "C" int pqk_assign_device(const uint8_t* d_codes, int64_t n, int32_t m, i
     PQK_LAUNCH_CHECK("table_quantize_kernel");
     const int64_t units = ((k + kc16 - 1) / kc16) * l * mp * (kc16 / 8);
     const int qgrid = (int)std::min<int64_t>((units + 255) / 256, (int64_t)di.sms * 16);
-    switch (mp) {
-      case 4: h16::qbuild16_kernel<4, 16><<<qgrid, 256, 0, stream>>>(w.t16, l, m, qmax, w.ucodes, w.counters, w.q16); break;
-      case 8: h16::qbuild16_kernel<8, 8><<<qgrid, 256, 0, stream>>>(w.t16, l, m, qmax, w.ucodes, w.counters, w.q16); break;
-      case 16: h16::qbuild16_kernel<16, 8><<<qgrid, 256, 0, stream>>>(w.t16, l, m, qmax, w.ucodes, w.counters, w.q16); break;
+    if (l % 8 == 0) {  // row-staged build
+      const int rgrid = (int)std::min<int64_t>((k + kc16 - 1) / kc16, (int64_t)di.sms * 8);
+      const size_t rsm = (size_t)mp * kc16 * (l + 2) * sizeof(uint16_t);
+      static bool attr_q[64] = {};
+      int dev = 0;
+      cudaGetDevice(&dev);
+      if (!attr_q[dev & 63]) {
+        PQK_CUDA_TRY(cudaFuncSetAttribute(h16::qbuild16_rows_kernel<16, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)(16 * 8 * (kMaxL + 2) * sizeof(uint16_t))));
+        attr_q[dev & 63] = true;
+      }
+      switch (mp) {
+        case 4: h16::qbuild16_rows_kernel<4, 16><<<rgrid, 256, rsm, stream>>>(w.t16, l, m, qmax, w.ucodes, w.counters, w.q16); break;
+        case 8: h16::qbuild16_rows_kernel<8, 8><<<rgrid, 256, rsm, stream>>>(w.t16, l, m, qmax, w.ucodes, w.counters, w.q16); break;
+        case 16: h16::qbuild16_rows_kernel<16, 8><<<rgrid, 256, rsm, stream>>>(w.t16, l, m, qmax, w.ucodes, w.counters, w.q16); break;
+      }
+      PQK_LAUNCH_CHECK("qbuild16_rows_kernel");
+    } else {
+      switch (mp) {
+        case 4: h16::qbuild16_kernel<4, 16><<<qgrid, 256, 0, stream>>>(w.t16, l, m, qmax, w.ucodes, w.counters, w.q16); break;
+        case 8: h16::qbuild16_kernel<8, 8><<<qgrid, 256, 0, stream>>>(w.t16, l, m, qmax, w.ucodes, w.counters, w.q16); break;
+        case 16: h16::qbuild16_kernel<16, 8><<<qgrid, 256, 0, stream>>>(w.t16, l, m, qmax, w.ucodes, w.counters, w.q16); break;
+      }
+      PQK_LAUNCH_CHECK("qbuild16_kernel");
     }
-    PQK_LAUNCH_CHECK("qbuild16_kernel");
   }
   // list tier threshold: below it the exact rescan is cheaper than streaming every chunk
   // (fp32 list scan: every CTA streams all chunks, a fixed cost, so it only beats the

@@ -208,6 +208,56 @@ __global__ void qbuild16_kernel(const uint16_t* __restrict__ t16, int l, int m, 
   }
 }
 
+// Same table as qbuild16_kernel, one CTA per chunk t (grid-stride): the chunk's KC center
+// rows T16[mm][c_u][*] (contiguous 2L-byte rows) are copied into shared memory with 16-byte
+// loads, then written out in Q16 order with 16-byte stores.  qbuild16_kernel gathered
+// every value with a 2-byte load from a random row (10M gathers, 16.5 us at config 2).
+template <int MP, int KC>
+__global__ void __launch_bounds__(256) qbuild16_rows_kernel(const uint16_t* __restrict__ t16, int l, int m, int qmax,
+                                                            const uint8_t* __restrict__ ucodes,
+                                                            const int32_t* __restrict__ counters,
+                                                            uint4* __restrict__ q) {
+  extern __shared__ uint16_t sq[];  // [MP * KC][l + 2] (padded rows)
+  const int U = counters[0];
+  const int nchunks = (U + KC - 1) / KC;
+  constexpr int Q8 = KC / 8;
+  const int ls = l + 2;
+  const int l8 = l / 8;  // l is a multiple of 8 (checked by the caller)
+  for (int t = blockIdx.x; t < nchunks; t += gridDim.x) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < MP * KC * l8; i += blockDim.x) {
+      const int c8 = i % l8, row = i / l8;
+      const int mm = row / KC, j = row - mm * KC;
+      const int u = t * KC + j;
+      uint4 v;
+      if (u < U && mm < m) {
+        const int c = ucodes[(size_t)u * MP + mm];
+        v = __ldg(reinterpret_cast<const uint4*>(t16 + ((size_t)mm * l + c) * l) + c8);
+      } else {
+        const uint32_t f = (mm < m) ? ((uint32_t)qmax | ((uint32_t)qmax << 16)) : 0u;
+        v = make_uint4(f, f, f, f);
+      }
+      uint32_t* d = reinterpret_cast<uint32_t*>(sq + row * ls + 8 * c8);  // 4-byte aligned (ls even)
+      d[0] = v.x;
+      d[1] = v.y;
+      d[2] = v.z;
+      d[3] = v.w;
+    }
+    __syncthreads();
+    uint4* qt = q + (size_t)t * l * MP * Q8;
+    for (int i = threadIdx.x; i < l * MP * Q8; i += blockDim.x) {
+      const int q8 = i % Q8;
+      const int r = i / Q8;
+      const int mm = r % MP, sidx = r / MP;
+      const uint16_t* col = sq + (mm * KC + q8 * 8) * ls + sidx;
+      uint32_t w[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) w[e] = (uint32_t)col[(2 * e) * ls] | ((uint32_t)col[(2 * e + 1) * ls] << 16);
+      qt[i] = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+  }
+}
+
 struct HScanParams {
   const uint8_t* codes;
   int64_t n;

@@ -65,6 +65,26 @@ class GpuShardBackend:
         self.n = len(codes_local)
         self.offset = offset
 
+    def enable_fused_exchange(self, world: int, rank: int) -> None:
+        """Put the histogram, the counts and one (sum sqrt sd, sum sd) slot per rank in one
+        int32 buffer, so a single SUM allreduce per iteration exchanges all three: each rank
+        writes its float64 partials into its own slot and zeros elsewhere, and integer sums
+        with zeros reproduce the bit patterns exactly (replaces an all_gather + 2 allreduces)."""
+        nh, nc = self.eng.hist.numel(), self.eng.counts.numel()
+        pad = (nh + nc) & 1  # 8-byte alignment of the float64 slots
+        buf = torch.zeros(nh + nc + pad + 4 * world, dtype=torch.int32, device=self.dev)
+        self.eng.hist = buf[:nh]
+        self.eng.counts = buf[nh:nh + nc]
+        self._xbuf = buf
+        self._xtail = buf[nh + nc + pad:].view(torch.float64).view(world, 2)
+        self._xrank = rank
+
+    def _fill_exchange_slot(self) -> None:
+        if getattr(self, "_xbuf", None) is not None:
+            self._xtail.zero_()
+            if self.n:
+                self._xtail[self._xrank].copy_(self.eng.obj)
+
     def upload_centers(self, centers: np.ndarray):
         return self.engine_mod.upload_codes(centers, self.m, self.dev)
 
@@ -99,22 +119,35 @@ class GpuShardBackend:
                         torch.cuda.Event(enable_timing=True)]
         if self.n == 0:
             self.assign(centers_dev)
-            return self.objective_tensor(), *self.histogram()
+            obj = self.objective_tensor()
+            self._fill_exchange_slot()
+            return obj, *self.histogram()
         g = getattr(self, "_graph_local", None)
         if g is None:
             self._ev[0].record()
             self.eng.assign(centers_dev)
             self._ev[1].record()
             self.eng.objective()
+            self._fill_exchange_slot()
             self.eng.histogram()
             if self.graphs and getattr(self, "_local_eager_done", False):
                 self._cur = centers_dev.clone()
                 self._graph_local = torch.cuda.CUDAGraph()
+                side = torch.cuda.Stream(device=self.dev)
                 with torch.cuda.graph(self._graph_local, capture_error_mode="thread_local"):
                     self.eng.assign(self._cur)
                     self._ev[1].record()
-                    self.eng.objective()
+                    # objective partials on a parallel branch beside the histogram
+                    fork = torch.cuda.Event()
+                    fork.record()
+                    side.wait_event(fork)
+                    with torch.cuda.stream(side):
+                        self.eng.objective()
+                        self._fill_exchange_slot()
+                    join = torch.cuda.Event()
+                    join.record(side)
                     self.eng.histogram()
+                    torch.cuda.current_stream(self.dev).wait_event(join)
                 # the capture did not run the work: this iteration's results come from the
                 # eager launches above
             self._local_eager_done = True
@@ -137,6 +170,20 @@ class GpuShardBackend:
             g.replay()
         self._ev[2].record()
         return self.eng.stats  # on the device: the driver reads it with the objective partials
+
+    def read_host(self, parts_t, st_dev):
+        """Objective partials and vote stats: two async copies into pinned host buffers and
+        one stream sync (a pageable .cpu() of a concatenation cost ~0.1 ms per iteration)."""
+        key = (tuple(parts_t.shape), st_dev.numel())
+        if getattr(self, "_pin_key", None) != key:
+            self._pin_parts = torch.empty(parts_t.shape, dtype=torch.float64).pin_memory()
+            self._pin_st = torch.empty(st_dev.numel(), dtype=torch.int64).pin_memory()
+            self._pin_key = key
+        self._pin_parts.copy_(parts_t, non_blocking=True)
+        self._pin_st.copy_(st_dev.reshape(-1), non_blocking=True)
+        torch.cuda.current_stream(self.dev).synchronize()
+        self.last_stats = self._pin_st.numpy().copy()
+        return self._pin_parts.numpy().copy(), self.last_stats
 
     def step_seconds(self) -> tuple[float, float]:
         """Device time of the last assign and of everything after it up to the vote
@@ -215,6 +262,9 @@ class DistributedLloyd:
         self.group = group
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
+        self.fused = hasattr(backend, "enable_fused_exchange")
+        if self.fused:
+            backend.enable_fused_exchange(self.world, self.rank)
 
     def init_centers(self, seed: int, codes_local: np.ndarray) -> np.ndarray:
         """clustering.py:149-157 over the global index space, rows gathered from owners."""
@@ -249,17 +299,24 @@ class DistributedLloyd:
             self.b.assign(centers_dev)
             obj_t = self.b.objective_tensor()
             hist, counts = self.b.histogram()
-        parts_t = self._gather(obj_t)  # stream-ordered collectives
-        if self.world > 1:
-            dist.all_reduce(hist, op=dist.ReduceOp.SUM, group=self.group)
-            dist.all_reduce(counts, op=dist.ReduceOp.SUM, group=self.group)
+        if self.fused:  # one allreduce: histogram, counts and the per-rank objective slots
+            if self.world > 1:
+                dist.all_reduce(self.b._xbuf, op=dist.ReduceOp.SUM, group=self.group)
+            parts_t = self.b._xtail
+        else:
+            parts_t = self._gather(obj_t)  # stream-ordered collectives
+            if self.world > 1:
+                dist.all_reduce(hist, op=dist.ReduceOp.SUM, group=self.group)
+                dist.all_reduce(counts, op=dist.ReduceOp.SUM, group=self.group)
         if hasattr(self.b, "update_phase"):
             # one device->host read for the objective partials and the vote stats
             st_dev = self.b.update_phase()
-            both = torch.cat([parts_t.reshape(-1).view(torch.int64), st_dev.reshape(-1)]).cpu().numpy()
-            np_parts = both[: parts_t.numel()].view(np.float64).reshape(parts_t.shape)
-            stats = both[parts_t.numel():]
-            parts = np_parts
+            if hasattr(self.b, "read_host"):
+                parts, stats = self.b.read_host(parts_t, st_dev)
+            else:
+                both = torch.cat([parts_t.reshape(-1).view(torch.int64), st_dev.reshape(-1)]).cpu().numpy()
+                parts = both[: parts_t.numel()].view(np.float64).reshape(parts_t.shape)
+                stats = both[parts_t.numel():]
         else:
             stats = self.b.vote()
             parts = parts_t.cpu().numpy()

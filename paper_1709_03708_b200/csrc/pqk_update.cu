@@ -329,12 +329,13 @@ __global__ void __launch_bounds__(1024) vote_t16_kernel(const float* __restrict_
 // (k, m) of a contiguous k range, so every support row is a conflict-free 512-byte
 // shared read instead of an L2 read (the L2-bound warp-per-row kernel took 96 us at
 // config 2).  Same arithmetic and certificate as vote_kernel's fp16 stage; rows it
-// cannot certify are left to vote_kernel (done[row] = 0), which goes straight to fp64.
+// cannot certify are appended to a row list for vote_kernel, which goes straight to fp64.
 constexpr int kV16Warps = 32;
 constexpr size_t kV16Smem = 256 * 256 * sizeof(__half) + (size_t)kV16Warps * 256 * 8;
 __global__ void __launch_bounds__(32 * kV16Warps, 1) vote16_smem_kernel(
     const uint32_t* __restrict__ hist, const uint32_t* __restrict__ counts, int64_t k, int m, int mp,
-    const __half* __restrict__ t16, int64_t rows_per_cta, uint8_t* __restrict__ newc, uint8_t* __restrict__ done,
+    const __half* __restrict__ t16, int64_t rows_per_cta, uint8_t* __restrict__ newc, int32_t* __restrict__ left,
+    int32_t* __restrict__ left_count,
     unsigned long long* __restrict__ acc) {
   constexpr int l = 256;
   extern __shared__ __align__(16) uint8_t v16_smem[];
@@ -358,10 +359,7 @@ __global__ void __launch_bounds__(32 * kV16Warps, 1) vote16_smem_kernel(
   unsigned long long my_nnz = 0, my_fail = 0;
   for (int64_t kk = k_lo + warp; kk < k_hi; kk += kV16Warps) {
     const int64_t gw = (int64_t)mm * k + kk;
-    if (counts[kk] == 0) {
-      if (lane == 0) done[gw] = 1;
-      continue;
-    }
+    if (counts[kk] == 0) continue;
     const uint32_t* hrow = hist + (kk * m + mm) * l;
     uint32_t hv[8];
 #pragma unroll
@@ -412,8 +410,8 @@ __global__ void __launch_bounds__(32 * kV16Warps, 1) vote16_smem_kernel(
         my_nnz += (unsigned long long)nnz;  // rows left to vote_kernel count their nnz there
       } else {
         ++my_fail;
+        left[atomicAdd(left_count, 1)] = (int32_t)gw;
       }
-      done[gw] = ok ? 1 : 0;
     }
   }
   if (lane == 0 && (my_nnz | my_fail)) {
@@ -436,13 +434,14 @@ __global__ void __launch_bounds__(32 * kV16Warps, 1) vote16_smem_kernel(
 // accumulation error is <= 16 instructions x 17 x 2^-23 x v (the encoder's per-instruction
 // bound, tools/diag_tc_error.py); with the fp16 table rounding the winner is certified
 // when v2 - v1 > eps (v1 + v2) + 2^-23 H, eps = 2^-11 + 272 2^-23 + 2^-20, else the row
-// goes to vote_kernel's fp64 path (done[row] = 0).  The dense contraction replaces the
+// goes to vote_kernel's fp64 path (appended to the undecided-row list).  The dense contraction replaces the
 // SIMT stage's sum over the support (issue bound: ~1e9 FMAs + conversions at config 2).
 constexpr int kVtcThreads = 256;
 constexpr size_t kVtcSmem = 1024 + 256 * 256 * 2 + 128 * 256 * 2;  // align slack + B + A
 __global__ void __launch_bounds__(kVtcThreads, 1) vote_tc_kernel(
     const uint32_t* __restrict__ hist, const uint32_t* __restrict__ counts, int64_t k, int m, int mp,
-    const __half* __restrict__ t16, uint8_t* __restrict__ newc, uint8_t* __restrict__ done,
+    const __half* __restrict__ t16, uint8_t* __restrict__ newc, int32_t* __restrict__ left,
+    int32_t* __restrict__ left_count,
     unsigned long long* __restrict__ acc) {
   extern __shared__ __align__(1024) uint8_t vtc_raw[];  // (no-swizzle operands need 16 B alignment)
   uint8_t* smem = vtc_raw;
@@ -554,7 +553,7 @@ __global__ void __launch_bounds__(kVtcThreads, 1) vote_tc_kernel(
       if (tid < 128 && k0 + tid < k) {
         const int64_t kk = k0 + tid;
         const bool filled = counts[kk] != 0;
-        done[(int64_t)mm * k + kk] = filled ? 0 : 1;
+        if (filled) left[atomicAdd(left_count, 1)] = (int32_t)((int64_t)mm * k + kk);
         my_fail += filled;
       }
       __syncthreads();
@@ -659,9 +658,7 @@ __global__ void __launch_bounds__(kVtcThreads, 1) vote_tc_kernel(
         const int64_t kk = k0 + r;
         if (kk < k) {
           const int64_t gw = (int64_t)mm * k + kk;
-          if (counts[kk] == 0) {
-            done[gw] = 1;
-          } else {
+          if (counts[kk] != 0) {
             const double eps = 4.8828125e-04 + 272.0 * 1.1920928955078125e-07 + 9.5367431640625e-07;
             const bool ok = (v2 - v1) > eps * (v1 + v2) + 1.1920928955078125e-07 * (double)row_h[r];
             if (ok) {
@@ -669,8 +666,8 @@ __global__ void __launch_bounds__(kVtcThreads, 1) vote_tc_kernel(
               my_nnz += (unsigned long long)row_nnz[r];
             } else {
               ++my_fail;
+              left[atomicAdd(left_count, 1)] = (int32_t)gw;
             }
-            done[gw] = ok ? 1 : 0;
           }
         }
       }
@@ -697,25 +694,16 @@ __global__ void __launch_bounds__(kVtcThreads, 1) vote_tc_kernel(
   }
 }
 
-__global__ void __launch_bounds__(32 * kVoteWarps) vote_kernel(const uint32_t* __restrict__ hist,
-                                                               const uint32_t* __restrict__ counts, int64_t k, int m,
-                                                               int l, int mp, const double* __restrict__ t64,
-                                                               const float* __restrict__ t32,
-                                                               const __half* __restrict__ t16,
-                                                               const uint8_t* __restrict__ done,
-                                                               uint8_t* __restrict__ newc,
-                                                               unsigned long long* __restrict__ acc) {
-  __shared__ int s_s[kVoteWarps][kMaxL];
-  __shared__ uint32_t s_h[kVoteWarps][kMaxL];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t gw = (int64_t)blockIdx.x * kVoteWarps + warp;
-  if (gw >= k * m) return;
+// one (k, m) row per warp (all lanes call it with the same gw)
+__device__ __forceinline__ void vote_row(int64_t gw, int* __restrict__ ss, uint32_t* __restrict__ sh,
+                                         const uint32_t* __restrict__ hist, const uint32_t* __restrict__ counts,
+                                         int64_t k, int m, int l, int mp, const double* __restrict__ t64,
+                                         const float* __restrict__ t32, const __half* __restrict__ t16,
+                                         uint8_t* __restrict__ newc, unsigned long long* __restrict__ acc) {
+  const int lane = threadIdx.x & 31;
   const int mm = (int)(gw / k);
   const int64_t kk = gw - (int64_t)mm * k;
-  if (done && done[gw]) return;  // decided by vote16_smem_kernel
-  if (counts[kk] == 0) return;   // empty: left 0, repaired later
-  int* ss = s_s[warp];
-  uint32_t* sh = s_h[warp];
+  if (counts[kk] == 0) return;  // empty: left 0, repaired later
   const uint32_t* hrow = hist + (kk * m + mm) * l;
   int nnz = 0;
   unsigned long long hs = 0;  // sum of this row's counts (the fp16 stage's absolute term)
@@ -848,6 +836,30 @@ __global__ void __launch_bounds__(32 * kVoteWarps) vote_kernel(const uint32_t* _
   if (lane == 0) {
     newc[kk * mp + mm] = (uint8_t)d.l;
     atomicAdd(&acc[1], 1ull);
+  }
+}
+
+// rows = nullptr: one warp per (k, m) row; otherwise a grid-stride loop over the *count rows
+// the first stage (vote_tc_kernel / vote16_smem_kernel) could not certify
+__global__ void __launch_bounds__(32 * kVoteWarps) vote_kernel(const uint32_t* __restrict__ hist,
+                                                               const uint32_t* __restrict__ counts, int64_t k, int m,
+                                                               int l, int mp, const double* __restrict__ t64,
+                                                               const float* __restrict__ t32,
+                                                               const __half* __restrict__ t16,
+                                                               const int32_t* __restrict__ rows,
+                                                               const int32_t* __restrict__ row_count,
+                                                               uint8_t* __restrict__ newc,
+                                                               unsigned long long* __restrict__ acc) {
+  __shared__ int s_s[kVoteWarps][kMaxL];
+  __shared__ uint32_t s_h[kVoteWarps][kMaxL];
+  const int warp = threadIdx.x >> 5;
+  if (rows) {
+    const int64_t cnt = *row_count;
+    for (int64_t i = (int64_t)blockIdx.x * kVoteWarps + warp; i < cnt; i += (int64_t)gridDim.x * kVoteWarps)
+      vote_row(rows[i], s_s[warp], s_h[warp], hist, counts, k, m, l, mp, t64, t32, t16, newc, acc);
+  } else {
+    const int64_t gw = (int64_t)blockIdx.x * kVoteWarps + warp;
+    if (gw < k * m) vote_row(gw, s_s[warp], s_h[warp], hist, counts, k, m, l, mp, t64, t32, t16, newc, acc);
   }
 }
 
@@ -1360,7 +1372,7 @@ extern "C" int pqk_vote_device(const uint32_t* d_hist, const uint32_t* d_counts,
     vote_t16_kernel<<<dim3(kT16Slices, m), 1024, 0, stream>>>(d_t32, l, t16);
     PQK_LAUNCH_CHECK("vote_t16_kernel");
   }
-  uint8_t* done = nullptr;
+  int32_t* left = nullptr;  // [0] = count, then the rows the first stage left undecided
   if (t16) {
     // fp16 stage from shared-memory tables; vote_kernel then takes the uncertified rows to fp64
     static int attr_v16[64] = {};
@@ -1371,7 +1383,8 @@ extern "C" int pqk_vote_device(const uint32_t* d_hist, const uint32_t* d_counts,
       PQK_CUDA_TRY(cudaFuncSetAttribute(vote_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kVtcSmem));
       attr_v16[dev & 63] = 1;
     }
-    PQK_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&done), (size_t)k * m, stream));
+    PQK_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&left), ((size_t)k * m + 4) * sizeof(int32_t), stream));
+    PQK_CUDA_TRY(cudaMemsetAsync(left, 0, sizeof(int32_t), stream));
     const int per = std::max(1, dev_info().sms / m);
     static const bool simt = [] {
       const char* e = getenv("PQK_VOTE_SIMT");
@@ -1380,21 +1393,27 @@ extern "C" int pqk_vote_device(const uint32_t* d_hist, const uint32_t* d_counts,
     if (simt) {
       const int64_t rows = (k + per - 1) / per;
       vote16_smem_kernel<<<dim3(per, m), 32 * kV16Warps, kV16Smem, stream>>>(d_hist, d_counts, k, m, mp, t16, rows,
-                                                                             d_new_centers, done, acc);
+                                                                             d_new_centers, left + 4, left, acc);
       PQK_LAUNCH_CHECK("vote16_smem_kernel");
     } else {
       const int64_t tiles = (k + 127) / 128;
       const int per_tc = (int)std::min<int64_t>(per, tiles);
       vote_tc_kernel<<<dim3(per_tc, m), kVtcThreads, kVtcSmem, stream>>>(d_hist, d_counts, k, m, mp, t16,
-                                                                          d_new_centers, done, acc);
+                                                                          d_new_centers, left + 4, left, acc);
       PQK_LAUNCH_CHECK("vote_tc_kernel");
     }
   }
-  vote_kernel<<<(unsigned)((k * m + kVoteWarps - 1) / kVoteWarps), 32 * kVoteWarps, 0, stream>>>(
-      d_hist, d_counts, k, m, l, mp, d_t64, done ? nullptr : d_t32, done ? nullptr : t16, done, d_new_centers, acc);
+  if (left) {  // the undecided rows only (fp64 stage), grid-stride over the device-side count
+    const int grid = (int)std::min<int64_t>((k * m + kVoteWarps - 1) / kVoteWarps, (int64_t)dev_info().sms * 8);
+    vote_kernel<<<grid, 32 * kVoteWarps, 0, stream>>>(d_hist, d_counts, k, m, l, mp, d_t64, nullptr, nullptr,
+                                                      left + 4, left, d_new_centers, acc);
+  } else {
+    vote_kernel<<<(unsigned)((k * m + kVoteWarps - 1) / kVoteWarps), 32 * kVoteWarps, 0, stream>>>(
+        d_hist, d_counts, k, m, l, mp, d_t64, d_t32, t16, nullptr, nullptr, d_new_centers, acc);
+  }
   PQK_LAUNCH_CHECK("vote_kernel");
   if (t16) PQK_CUDA_TRY(cudaFreeAsync(t16, stream));
-  if (done) PQK_CUDA_TRY(cudaFreeAsync(done, stream));
+  if (left) PQK_CUDA_TRY(cudaFreeAsync(left, stream));
   empties_kernel<<<(unsigned)((k + 1023) / 1024), 1024, 0, stream>>>(d_counts, k, acc);
   PQK_LAUNCH_CHECK("empties_kernel");
   vote_stats_kernel<<<1, 1, 0, stream>>>(k, acc, d_stats);

@@ -185,3 +185,20 @@ def test_default_mode_large_problem_uses_16bit_tier(lib, oracle):
     expect, exp_sd = oracle.assign_c(codes, centers, tables, want_sd=True)
     np.testing.assert_array_equal(labels, expect)
     assert sd.tobytes() == exp_sd.tobytes()
+
+
+@pytest.mark.skipif(bool(__import__("os").environ.get("PQK_VOTE_SIMT")), reason="already inside the SIMT child")
+def test_vote_simt_stage_child():
+    """The SIMT shared-table first stage (PQK_VOTE_SIMT=1, read once per process) on the
+    same vote cases, in a child pytest."""
+    import os
+    import subprocess
+    import sys
+
+    here = os.path.dirname(os.path.abspath(__file__))
+    env = dict(os.environ, PQK_VOTE_SIMT="1")
+    res = subprocess.run(
+        [sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-p", "no:cacheprovider",
+         os.path.join(here, "test_gpu_scan16.py"), "-k", "test_vote_fp16_stage"],
+        env=env, cwd=os.path.dirname(here), capture_output=True, text=True, timeout=600)
+    assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-2000:]

@@ -1311,34 +1311,39 @@ extern "C" int pqk_histogram_device(const uint8_t* d_codes, int64_t n, int32_t m
     const size_t rec_b = align_up((size_t)std::max<int64_t>(n, 1) * (mw + 1) * 4, 256);
     { const int _rc = keep_default_pool(); if (_rc != PQK_OK) return _rc; }
     uint8_t* ws = nullptr;
-    PQK_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&ws), cnt_b + base_b + rec_b, stream));
-    uint32_t* cnt = reinterpret_cast<uint32_t*>(ws);
-    uint32_t* base = reinterpret_cast<uint32_t*>(ws + cnt_b);
-    uint32_t* rec = reinterpret_cast<uint32_t*>(ws + cnt_b + base_b);
-    const size_t sm_nb = (size_t)nbi * 4;
-    static int smem_set[64] = {};
-    int dev = 0;
-    PQK_CUDA_TRY(cudaGetDevice(&dev));
-    if (!smem_set[dev & 63]) {
-      PQK_CUDA_TRY(cudaFuncSetAttribute(hbin_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kHistMaxBuckets * 4));
-      PQK_CUDA_TRY(cudaFuncSetAttribute(hbin_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kHistMaxBuckets * 4));
-      PQK_CUDA_TRY(cudaFuncSetAttribute(hbin_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kHistTileBytes));
-      smem_set[dev & 63] = 1;
+    if (cudaMallocAsync(reinterpret_cast<void**>(&ws), cnt_b + base_b + rec_b, stream) != cudaSuccess) {
+      (void)cudaGetLastError();  // no room for the bucketed records: the atomic path below
+      ws = nullptr;
     }
-    hbin_count_kernel<<<ctas, kHistThreads, sm_nb, stream>>>(d_labels, n, per_cta, (uint32_t)tile, nbi, cnt);
-    PQK_LAUNCH_CHECK("hbin_count_kernel");
-    hbin_colscan_kernel<<<(nbi + 255) / 256, 256, 0, stream>>>(cnt, ctas, nbi, base);
-    PQK_LAUNCH_CHECK("hbin_colscan_kernel");
-    hbin_scan_kernel<<<1, 1024, 0, stream>>>(base, nbi);
-    PQK_LAUNCH_CHECK("hbin_scan_kernel");
-    hbin_scatter_kernel<<<ctas, 1024, sm_nb, stream>>>(d_codes, mw, d_labels, n, per_cta, (uint32_t)tile, nbi, cnt,
-                                                       base, rec);
-    PQK_LAUNCH_CHECK("hbin_scatter_kernel");
-    hbin_tile_kernel<<<nbi, kHistThreads, (size_t)tile * m * l * 4, stream>>>(rec, mw, base, tile, k, m, l, d_hist,
-                                                                             d_counts);
-    PQK_LAUNCH_CHECK("hbin_tile_kernel");
-    PQK_CUDA_TRY(cudaFreeAsync(ws, stream));
-    return PQK_OK;
+    if (ws) {
+      uint32_t* cnt = reinterpret_cast<uint32_t*>(ws);
+      uint32_t* base = reinterpret_cast<uint32_t*>(ws + cnt_b);
+      uint32_t* rec = reinterpret_cast<uint32_t*>(ws + cnt_b + base_b);
+      const size_t sm_nb = (size_t)nbi * 4;
+      static int smem_set[64] = {};
+      int dev = 0;
+      PQK_CUDA_TRY(cudaGetDevice(&dev));
+      if (!smem_set[dev & 63]) {
+        PQK_CUDA_TRY(cudaFuncSetAttribute(hbin_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kHistMaxBuckets * 4));
+        PQK_CUDA_TRY(cudaFuncSetAttribute(hbin_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kHistMaxBuckets * 4));
+        PQK_CUDA_TRY(cudaFuncSetAttribute(hbin_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kHistTileBytes));
+        smem_set[dev & 63] = 1;
+      }
+      hbin_count_kernel<<<ctas, kHistThreads, sm_nb, stream>>>(d_labels, n, per_cta, (uint32_t)tile, nbi, cnt);
+      PQK_LAUNCH_CHECK("hbin_count_kernel");
+      hbin_colscan_kernel<<<(nbi + 255) / 256, 256, 0, stream>>>(cnt, ctas, nbi, base);
+      PQK_LAUNCH_CHECK("hbin_colscan_kernel");
+      hbin_scan_kernel<<<1, 1024, 0, stream>>>(base, nbi);
+      PQK_LAUNCH_CHECK("hbin_scan_kernel");
+      hbin_scatter_kernel<<<ctas, 1024, sm_nb, stream>>>(d_codes, mw, d_labels, n, per_cta, (uint32_t)tile, nbi, cnt,
+                                                         base, rec);
+      PQK_LAUNCH_CHECK("hbin_scatter_kernel");
+      hbin_tile_kernel<<<nbi, kHistThreads, (size_t)tile * m * l * 4, stream>>>(rec, mw, base, tile, k, m, l, d_hist,
+                                                                               d_counts);
+      PQK_LAUNCH_CHECK("hbin_tile_kernel");
+      PQK_CUDA_TRY(cudaFreeAsync(ws, stream));
+      return PQK_OK;
+    }
   }
   PQK_CUDA_TRY(cudaMemsetAsync(d_hist, 0, (size_t)k * m * l * sizeof(int32_t), stream));
   if (n > 0) {

@@ -140,6 +140,14 @@ int pqk_vote_device(const uint32_t* d_hist, const uint32_t* d_counts, int64_t k,
                     const double* d_t64, const float* d_t32, uint8_t* d_new_centers, int64_t* d_stats,
                     void* stream);
 
+/* The same vote with the fp16 first-stage tables prebuilt once per table set
+ * (pqk_vote_tables16_device: T16 = fp16(T32 * 2^f) per subspace, M*256*256 halves,
+ * L = 256 only) instead of rebuilt on every call; d_t16 NULL = pqk_vote_device. */
+int pqk_vote_tables16_device(const float* d_t32, int32_t m, int32_t l, void* d_t16, void* stream);
+int pqk_vote16_device(const uint32_t* d_hist, const uint32_t* d_counts, int64_t k, int32_t m, int32_t l,
+                      const double* d_t64, const float* d_t32, const void* d_t16, uint8_t* d_new_centers,
+                      int64_t* d_stats, void* stream);
+
 /* Empty-cluster repair (clustering.py:460-466): the E empty clusters (ascending k)
  * take the codes of the E codes with largest sd_sq (lowest index among ties).  Code
  * indices are 32-bit in the selection keys: n (and base_index + n) <= 2^32. */

@@ -59,6 +59,8 @@ SIGNATURES: dict[str, tuple] = {
     "pqk_paired_distance_device": (C.c_int, [_p, _p, _p, _i64, _i32, _i32, _p, _p, _p]),
     "pqk_histogram_device": (C.c_int, [_p, _i64, _i32, _i32, _p, _i64, _p, _p, _p]),
     "pqk_vote_device": (C.c_int, [_p, _p, _i64, _i32, _i32, _p, _p, _p, _p, _p]),
+    "pqk_vote_tables16_device": (C.c_int, [_p, _i32, _i32, _p, _p]),
+    "pqk_vote16_device": (C.c_int, [_p, _p, _i64, _i32, _i32, _p, _p, _p, _p, _p, _p]),
     "pqk_repair_workspace_bytes": (_sz, [_i64, _i64]),
     "pqk_repair_device": (C.c_int, [_p, _p, _i64, _i32, _p, _i64, _p, _p, _sz, _p, _p]),
     "pqk_repair_candidates_device": (C.c_int, [_p, _i64, _i64, _i64, _p, _sz, _p, _p, _p]),

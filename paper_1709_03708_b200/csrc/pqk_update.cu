@@ -1357,10 +1357,34 @@ extern "C" int pqk_histogram_device(const uint8_t* d_codes, int64_t n, int32_t m
   return PQK_OK;
 }
 
+extern "C" int pqk_vote_tables16_device(const float* d_t32, int32_t m, int32_t l, void* d_t16, void* stream) {
+  if (!d_t32 || !d_t16 || m < 1 || l != 256) return fail(PQK_EINVAL, "pqk_vote_tables16_device: bad arguments");
+  vote_t16_kernel<<<dim3(kT16Slices, m), 1024, 0, (cudaStream_t)stream>>>(d_t32, l, (__half*)d_t16);
+  PQK_LAUNCH_CHECK("vote_t16_kernel");
+  return PQK_OK;
+}
+
+static int vote_impl(const uint32_t* d_hist, const uint32_t* d_counts, int64_t k, int32_t m, int32_t l,
+                     const double* d_t64, const float* d_t32, const __half* t16_given, uint8_t* d_new_centers,
+                     int64_t* d_stats, void* stream_);
+
 // d_stats has PQK_STATS_LEN slots: 0..15 public, 16..19 scratch accumulators of the vote.
 extern "C" int pqk_vote_device(const uint32_t* d_hist, const uint32_t* d_counts, int64_t k, int32_t m, int32_t l,
                                const double* d_t64, const float* d_t32, uint8_t* d_new_centers, int64_t* d_stats,
-                               void* stream_) {
+                               void* stream) {
+  return vote_impl(d_hist, d_counts, k, m, l, d_t64, d_t32, nullptr, d_new_centers, d_stats, stream);
+}
+
+extern "C" int pqk_vote16_device(const uint32_t* d_hist, const uint32_t* d_counts, int64_t k, int32_t m, int32_t l,
+                                 const double* d_t64, const float* d_t32, const void* d_t16,
+                                 uint8_t* d_new_centers, int64_t* d_stats, void* stream) {
+  if (d_t16 && (!d_t32 || l != 256)) return fail(PQK_EINVAL, "pqk_vote16_device: d_t16 needs d_t32 and l == 256");
+  return vote_impl(d_hist, d_counts, k, m, l, d_t64, d_t32, (const __half*)d_t16, d_new_centers, d_stats, stream);
+}
+
+static int vote_impl(const uint32_t* d_hist, const uint32_t* d_counts, int64_t k, int32_t m, int32_t l,
+                     const double* d_t64, const float* d_t32, const __half* t16_given, uint8_t* d_new_centers,
+                     int64_t* d_stats, void* stream_) {
   cudaStream_t stream = (cudaStream_t)stream_;
   const int mp = padded_m(m);
   if (mp == 0 || l < 2 || l > kMaxL || k < 1 || !d_stats) return fail(PQK_EINVAL, "pqk_vote_device: bad arguments");
@@ -1370,12 +1394,14 @@ extern "C" int pqk_vote_device(const uint32_t* d_hist, const uint32_t* d_counts,
   PQK_CUDA_TRY(cudaMemsetAsync(d_new_centers, 0, (size_t)k * mp, stream));
   // fp16 first-stage tables, rebuilt every call (the tables may differ between calls) in
   // stream-ordered memory (cudaMallocAsync: also valid inside a CUDA-graph capture)
-  __half* t16 = nullptr;
-  if (d_t32 && l == 256) {
+  const __half* t16 = t16_given;  // prebuilt by pqk_vote_tables16_device (constant tables)
+  __half* t16_own = nullptr;
+  if (!t16 && d_t32 && l == 256) {
     { const int _rc = keep_default_pool(); if (_rc != PQK_OK) return _rc; }
-    PQK_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&t16), (size_t)m * l * l * sizeof(__half), stream));
-    vote_t16_kernel<<<dim3(kT16Slices, m), 1024, 0, stream>>>(d_t32, l, t16);
+    PQK_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&t16_own), (size_t)m * l * l * sizeof(__half), stream));
+    vote_t16_kernel<<<dim3(kT16Slices, m), 1024, 0, stream>>>(d_t32, l, t16_own);
     PQK_LAUNCH_CHECK("vote_t16_kernel");
+    t16 = t16_own;
   }
   int32_t* left = nullptr;  // [0] = count, then the rows the first stage left undecided
   if (t16) {
@@ -1417,7 +1443,7 @@ extern "C" int pqk_vote_device(const uint32_t* d_hist, const uint32_t* d_counts,
         d_hist, d_counts, k, m, l, mp, d_t64, d_t32, t16, nullptr, nullptr, d_new_centers, acc);
   }
   PQK_LAUNCH_CHECK("vote_kernel");
-  if (t16) PQK_CUDA_TRY(cudaFreeAsync(t16, stream));
+  if (t16_own) PQK_CUDA_TRY(cudaFreeAsync(t16_own, stream));
   if (left) PQK_CUDA_TRY(cudaFreeAsync(left, stream));
   empties_kernel<<<(unsigned)((k + 1023) / 1024), 1024, 0, stream>>>(d_counts, k, acc);
   PQK_LAUNCH_CHECK("empties_kernel");

@@ -65,6 +65,7 @@ class DeviceTables:
     mp: int
     fp64_only: int
     exp2: int
+    t16: "torch.Tensor | None" = None  # fp16 vote tables (L = 256), built once
 
 
 _TABLE_CACHE: dict = {}
@@ -93,7 +94,11 @@ def device_tables(tables: np.ndarray, dev) -> DeviceTables:
     t64 = torch.from_numpy(np.array(t)).to(dev)  # (read-only DistanceTables arrays)
     t32 = torch.empty(mp * l * l, dtype=torch.float32, device=dev)
     call("pqk_tables_to_f32", _ptr(t64), m, l, e.value, _ptr(t32), _stream(dev))
-    dt = DeviceTables(t64, t32, m, l, mp, int(f64.value), int(e.value))
+    t16 = None
+    if l == 256 and not f64.value:
+        t16 = torch.empty(m * l * l, dtype=torch.int16, device=dev)
+        call("pqk_vote_tables16_device", _ptr(t32), m, l, _ptr(t16), _stream(dev))
+    dt = DeviceTables(t64, t32, m, l, mp, int(f64.value), int(e.value), t16)
     with _TABLE_LOCK:
         if len(_TABLE_CACHE) >= 8:
             _TABLE_CACHE.pop(next(iter(_TABLE_CACHE)))
@@ -282,7 +287,7 @@ class ShardEngine:
     def vote(self) -> None:
         t = self.tables
         call(
-            "pqk_vote_device",
+            "pqk_vote16_device",
             _ptr(self.hist),
             _ptr(self.counts),
             self.k,
@@ -290,6 +295,7 @@ class ShardEngine:
             t.l,
             _ptr(t.t64),
             _ptr(None if t.fp64_only else t.t32),
+            _ptr(None if t.fp64_only else t.t16),
             _ptr(self.new_centers),
             _ptr(self.stats),
             _stream(self.dev),

@@ -37,6 +37,8 @@
 // bytes are: every LDS.128 is 4 conflict-free wavefronts (128 B each).
 #include <algorithm>
 #include <cstdio>
+#include <map>
+#include <mutex>
 
 #include "pqk_common.cuh"
 #include "pqk_hscan.cuh"
@@ -833,6 +835,28 @@ extern "C" int pqk_pad_codes_device(const uint8_t* d_raw, int64_t n, int32_t m, 
   return PQK_OK;
 }
 
+// Side stream + fork/join events per (device, caller stream): the 16-bit tier's scale
+// preparation (table maximum, sampled exact scan over the raw centers) runs beside the
+// center dedup and joins before the table quantisation.  Event fork/join also captures
+// into a CUDA graph as two parallel branches.
+struct SideStream {
+  cudaStream_t s = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
+static int side_stream_for(int dev, cudaStream_t main, SideStream** out) {
+  static std::mutex mu;
+  static std::map<std::pair<int, cudaStream_t>, SideStream> table;
+  std::lock_guard<std::mutex> lock(mu);
+  SideStream& ss = table[{dev, main}];
+  if (!ss.s) {
+    PQK_CUDA_TRY(cudaStreamCreateWithFlags(&ss.s, cudaStreamNonBlocking));
+    PQK_CUDA_TRY(cudaEventCreateWithFlags(&ss.fork, cudaEventDisableTiming));
+    PQK_CUDA_TRY(cudaEventCreateWithFlags(&ss.join, cudaEventDisableTiming));
+  }
+  *out = &ss;
+  return PQK_OK;
+}
+
 extern "C" size_t pqk_assign_workspace_bytes(int64_t n, int64_t k, int32_t m, int32_t l) {
   const int mp = padded_m(m);
   if (mp == 0 || k < 1 || n < 0 || l < 1) return 0;
@@ -860,6 +884,32 @@ extern "C" int pqk_assign_device(const uint8_t* d_codes, int64_t n, int32_t m, i
   AssignWS w = assign_ws_layout(d_ws, n, k, mp, l);
   if (ws_bytes < w.total) return fail(PQK_EINVAL, "pqk_assign_device: workspace too small");
 
+  const DevInfo& di0 = dev_info();
+  SideStream* side = nullptr;
+  if (use16) {
+    // 0. scale preparation on the side branch (w.scale is free: the fork follows every
+    //    earlier reader on the caller's stream)
+    int dev = 0;
+    PQK_CUDA_TRY(cudaGetDevice(&dev));
+    { const int rc = side_stream_for(dev, stream, &side); if (rc != PQK_OK) return rc; }
+    static bool attr16[64] = {};
+    if (!attr16[dev & 63]) {
+      PQK_CUDA_TRY(cudaFuncSetAttribute(h16::scale_sample_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        96 * 1024));
+      attr16[dev & 63] = true;
+    }
+    PQK_CUDA_TRY(cudaEventRecord(side->fork, stream));
+    PQK_CUDA_TRY(cudaStreamWaitEvent(side->s, side->fork, 0));
+    PQK_CUDA_TRY(cudaMemsetAsync(w.scale, 0, sizeof(h16::Scale), side->s));
+    const int64_t cnt = (int64_t)m * l * l;
+    h16::table_max_kernel<<<(int)std::min<int64_t>((cnt + 255) / 256, (int64_t)di0.sms * 4), 256, 0, side->s>>>(
+        d_t64, cnt, w.scale);
+    PQK_LAUNCH_CHECK("table_max_kernel");
+    h16::scale_sample_kernel<<<h16::kScaleSample, 256, (size_t)m * l * sizeof(double), side->s>>>(
+        d_codes, n, mp, m, l, d_centers, nullptr, d_t64, w.scale, (int)k);
+    PQK_LAUNCH_CHECK("scale_sample_kernel");
+    PQK_CUDA_TRY(cudaEventRecord(side->join, side->s));
+  }
   // 1. dedup
   PQK_CUDA_TRY(cudaMemsetAsync(w.counters, 0, 16 * sizeof(int32_t), stream));
   PQK_CUDA_TRY(cudaMemsetAsync(w.hash, 0xff, w.hash_size * sizeof(int32_t), stream));
@@ -896,24 +946,7 @@ extern "C" int pqk_assign_device(const uint8_t* d_codes, int64_t n, int32_t m, i
   if (use16) {
     // 16-bit fixed-point tables (scale from the table maximum) and their chunks
     const int qmax = h16::qmax_for(m);
-    PQK_CUDA_TRY(cudaMemsetAsync(w.scale, 0, sizeof(h16::Scale), stream));
-    const int64_t cnt = (int64_t)m * l * l;
-    h16::table_max_kernel<<<(int)std::min<int64_t>((cnt + 255) / 256, (int64_t)di.sms * 4), 256, 0, stream>>>(
-        d_t64, cnt, w.scale);
-    PQK_LAUNCH_CHECK("table_max_kernel");
-    {
-      static bool attr16[64] = {};
-      int dev = 0;
-      cudaGetDevice(&dev);
-      if (!attr16[dev & 63]) {
-        PQK_CUDA_TRY(cudaFuncSetAttribute(h16::scale_sample_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          96 * 1024));
-        attr16[dev & 63] = true;
-      }
-      h16::scale_sample_kernel<<<h16::kScaleSample, 256, (size_t)m * l * sizeof(double), stream>>>(
-          d_codes, n, mp, m, l, w.ucodes, w.counters, d_t64, w.scale);
-      PQK_LAUNCH_CHECK("scale_sample_kernel");
-    }
+    PQK_CUDA_TRY(cudaStreamWaitEvent(stream, side->join, 0));  // scale ready (side branch)
     const int64_t cntp = (int64_t)mp * l * l;
     h16::table_quantize_kernel<<<(int)std::min<int64_t>((cntp + 255) / 256, (int64_t)di.sms * 8), 256, 0,
                                  stream>>>(d_t64, m, l, mp, qmax, w.scale, w.t16);

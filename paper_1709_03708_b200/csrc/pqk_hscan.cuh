@@ -67,13 +67,13 @@ constexpr int kScaleSample = 128;
 __global__ void __launch_bounds__(256) scale_sample_kernel(const uint8_t* __restrict__ codes, int64_t n, int mp,
                                                            int m, int l, const uint8_t* __restrict__ ucodes,
                                                            const int32_t* __restrict__ counters,
-                                                           const double* __restrict__ t64, Scale* sc) {
+                                                           const double* __restrict__ t64, Scale* sc, int u_fixed) {
   extern __shared__ double s_rows[];  // m * l
   __shared__ double s_best[8];
   __shared__ int s_bu[8];
   const int64_t idx = (int64_t)blockIdx.x * n / gridDim.x;
   const uint8_t* xc = codes + idx * mp;
-  const int U = counters[0];
+  const int U = u_fixed >= 0 ? u_fixed : counters[0];  // u_fixed: raw centers (duplicates kept)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int e = tid; e < m * l; e += blockDim.x) {
     const int mm = e / l, s = e - mm * l;

@@ -260,6 +260,10 @@ int pqk_host_release(int32_t device);
 /* tcgen05 self-test: C (128 x 256, fp32) = A (128 x k, fp16, row-major) * B (256 x k,
  * fp16, row-major)^T through UMMA descriptors, TMEM and tcgen05.ld (k % 16 == 0). */
 int pqk_tc_selftest(const void* d_a_f16, const void* d_b_f16, float* d_c, int32_t k, void* stream);
+/* Measured shared-memory load ceiling (bench roofline denominator): conflict-free
+ * LDS.128 from one 1024-thread CTA per SM over `iters` x 16 loads per thread; returns
+ * bytes/s (and the timed launch in ms) measured with CUDA events on `stream`. */
+int pqk_smem_probe(int32_t device, int32_t iters, double* bytes_per_s, double* ms_out, void* stream);
 
 #ifdef __cplusplus
 }

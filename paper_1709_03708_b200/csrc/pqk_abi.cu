@@ -74,8 +74,18 @@ struct HostCtx {
     void* p = nullptr;
     size_t bytes = 0;
   };
-  Buf raw, codes, centers_raw, centers, t64, t32, labels, sd, ws, stats, hist, counts, newc, rws, vec, cw, obj, objws,
-      plan, scale;
+  Buf raw, codes, centers_raw, centers, t64, t32, t16, labels, sd, ws, stats, hist, counts, newc, rws, vec, cw, obj,
+      objws, plan, scale;
+  // the last table set uploaded (compared by content: a caller re-running assign or fit
+  // steps with the same DistanceTables skips the upload, the scale decision's host sync
+  // and the fp16 vote-table build)
+  std::vector<double> tab_host;
+  int tab_m = 0, tab_l = 0, tab_fp64_only = 0;
+  bool tab_t16 = false;
+  // pinned staging for results copied out while later work runs (pageable caller buffers
+  // would make cudaMemcpyAsync wait for the copy, serialising the host)
+  void* stage = nullptr;
+  size_t stage_bytes = 0;
   // cached numpy-summation plan for the last n (uploaded into `plan`)
   int64_t plan_n = -1, plan_nleaves = 0, plan_nnodes = 0;
   size_t plan_o_len = 0, plan_o_na = 0, plan_o_nb = 0;
@@ -164,10 +174,17 @@ static void table_scale_decide(double mx, double mn, int32_t* e_out, int32_t* f6
   *e_out = e;
 }
 
-// Upload tables, build the scaled fp32 copy (scale decided on the device).
+// Upload tables, build the scaled fp32 copy (scale decided on the device) and, for
+// L = 256, the fp16 first-stage vote tables; skipped when the content is unchanged.
 static int upload_tables(HostCtx* c, const double* tables, int m, int l, int& fp64_only) {
   const int mp = padded_m(m);
   const size_t cnt = (size_t)m * l * l;
+  if (c->tab_m == m && c->tab_l == l && c->tab_host.size() == cnt &&
+      std::memcmp(c->tab_host.data(), tables, cnt * sizeof(double)) == 0) {
+    fp64_only = c->tab_fp64_only;
+    return PQK_OK;
+  }
+  c->tab_m = 0;  // invalid until the upload below completes
   PQK_TRY(ensure(c->t64, cnt * sizeof(double)));
   PQK_TRY(ensure(c->t32, (size_t)mp * l * l * sizeof(float)));
   PQK_TRY(ensure(c->scale, 4 * sizeof(unsigned long long)));
@@ -188,7 +205,51 @@ static int upload_tables(HostCtx* c, const double* tables, int m, int l, int& fp
   int32_t e = 0, f64 = 0;
   table_scale_decide(mx, mn, &e, &f64);
   fp64_only = f64;
-  return pqk_tables_to_f32((const double*)c->t64.p, m, l, e, (float*)c->t32.p, c->stream);
+  PQK_TRY(pqk_tables_to_f32((const double*)c->t64.p, m, l, e, (float*)c->t32.p, c->stream));
+  c->tab_t16 = false;
+  if (l == 256 && !f64) {
+    PQK_TRY(ensure(c->t16, cnt * 2));
+    PQK_TRY(pqk_vote_tables16_device((const float*)c->t32.p, m, l, c->t16.p, c->stream));
+    c->tab_t16 = true;
+  }
+  c->tab_host.assign(tables, tables + cnt);
+  c->tab_fp64_only = f64;
+  c->tab_m = m;
+  c->tab_l = l;
+  return PQK_OK;
+}
+
+// Device -> host copy of a result on `stream`: straight into the caller's buffer when it is
+// page-locked, else into the context's pinned staging buffer (finish_d2h copies it out
+// after the stream is synchronised).
+static bool host_is_pinned(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();  // clear the sticky-free error of an unknown pointer
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
+static int start_d2h(HostCtx* c, void* dst, const void* src, size_t bytes, cudaStream_t stream, bool& staged) {
+  staged = !host_is_pinned(dst);
+  if (!staged) {
+    PQK_CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, stream));
+    return PQK_OK;
+  }
+  if (c->stage_bytes < bytes) {
+    if (c->stage) cudaFreeHost(c->stage);
+    c->stage = nullptr;
+    c->stage_bytes = 0;
+    PQK_CUDA_TRY(cudaMallocHost(&c->stage, bytes));
+    c->stage_bytes = bytes;
+  }
+  PQK_CUDA_TRY(cudaMemcpyAsync(c->stage, src, bytes, cudaMemcpyDeviceToHost, stream));
+  return PQK_OK;
+}
+
+static void finish_d2h(HostCtx* c, void* dst, size_t bytes, bool staged) {
+  if (staged) std::memcpy(dst, c->stage, bytes);
 }
 
 static int upload_codes(HostCtx* c, HostCtx::Buf& rawb, HostCtx::Buf& dst, const uint8_t* h, int64_t n, int m,
@@ -336,10 +397,12 @@ extern "C" int pqk_assign_host(const uint8_t* codes, int64_t n, int32_t m, const
   PQK_TRY(pqk_assign_device((const uint8_t*)c->codes.p, n, m, l, (const uint8_t*)c->centers.p, k,
                             (const double*)c->t64.p, (const float*)c->t32.p, fp64_only, c->ws.p, wsb,
                             (uint32_t*)c->labels.p, (double*)c->sd.p, (int64_t*)c->stats.p, c->stream));
-  PQK_CUDA_TRY(cudaMemcpyAsync(labels, c->labels.p, (size_t)n * sizeof(uint32_t), cudaMemcpyDeviceToHost, c->stream));
+  bool staged = false;
+  PQK_TRY(start_d2h(c, labels, c->labels.p, (size_t)n * sizeof(uint32_t), c->stream, staged));
   if (sd_sq)
     PQK_CUDA_TRY(cudaMemcpyAsync(sd_sq, c->sd.p, (size_t)n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
   PQK_CUDA_TRY(cudaStreamSynchronize(c->stream));
+  finish_d2h(c, labels, (size_t)n * sizeof(uint32_t), staged);
   return PQK_OK;
 }
 
@@ -431,16 +494,16 @@ extern "C" int pqk_lloyd_step_host(const uint8_t* codes, int64_t n, int32_t m, c
   // labels are final once assigned: copy them out on the side while the update runs
   PQK_CUDA_TRY(cudaEventRecord(c->assigned, c->stream));
   PQK_CUDA_TRY(cudaStreamWaitEvent(c->copy_stream, c->assigned, 0));
-  PQK_CUDA_TRY(cudaMemcpyAsync(labels, c->labels.p, (size_t)n * sizeof(uint32_t), cudaMemcpyDeviceToHost,
-                               c->copy_stream));
+  bool staged = false;
+  PQK_TRY(start_d2h(c, labels, c->labels.p, (size_t)n * sizeof(uint32_t), c->copy_stream, staged));
   PQK_TRY(pqk_objective_device((const double*)c->sd.p, n, nleaves, ndepth, (const int64_t*)pb,
                                (const int32_t*)(pb + o_len), depth_start_h, (const int32_t*)(pb + o_na),
                                (const int32_t*)(pb + o_nb), c->objws.p, owsb, (double*)c->obj.p, c->stream));
   PQK_TRY(pqk_histogram_device((const uint8_t*)c->codes.p, n, m, l, (const uint32_t*)c->labels.p, k,
                                (uint32_t*)c->hist.p, (uint32_t*)c->counts.p, c->stream));
-  PQK_TRY(pqk_vote_device((const uint32_t*)c->hist.p, (const uint32_t*)c->counts.p, k, m, l, (const double*)c->t64.p,
-                          fp64_only ? nullptr : (const float*)c->t32.p,
-                          (uint8_t*)c->newc.p, dstats, c->stream));
+  PQK_TRY(pqk_vote16_device((const uint32_t*)c->hist.p, (const uint32_t*)c->counts.p, k, m, l,
+                            (const double*)c->t64.p, fp64_only ? nullptr : (const float*)c->t32.p,
+                            c->tab_t16 ? c->t16.p : nullptr, (uint8_t*)c->newc.p, dstats, c->stream));
   int64_t hstats[PQK_STATS_LEN];
   PQK_CUDA_TRY(cudaMemcpyAsync(hstats, dstats, sizeof(hstats), cudaMemcpyDeviceToHost, c->stream));
   PQK_CUDA_TRY(cudaStreamSynchronize(c->stream));
@@ -460,6 +523,7 @@ extern "C" int pqk_lloyd_step_host(const uint8_t* codes, int64_t n, int32_t m, c
     for (int64_t i = 0; i < k; ++i) std::memcpy(new_centers + i * m, tmp.data() + i * mp, m);
   }
   PQK_CUDA_TRY(cudaStreamSynchronize(c->copy_stream));
+  finish_d2h(c, labels, (size_t)n * sizeof(uint32_t), staged);
   return PQK_OK;
 }
 
@@ -469,16 +533,27 @@ extern "C" int pqk_host_release(int32_t device) {
   if (!c.init) return PQK_OK;
   std::lock_guard<std::mutex> lock(c.mu);
   PQK_CUDA_TRY(cudaSetDevice(device));
-  HostCtx::Buf* bufs[] = {&c.raw, &c.codes, &c.centers_raw, &c.centers, &c.t64, &c.t32, &c.labels,
-                          &c.sd,  &c.ws,    &c.stats,       &c.hist,    &c.counts, &c.newc, &c.rws,
-                          &c.vec, &c.cw,    &c.obj,         &c.objws,   &c.plan, &c.scale};
+  HostCtx::Buf* bufs[] = {&c.raw, &c.codes, &c.centers_raw, &c.centers, &c.t64, &c.t32,   &c.t16,
+                          &c.labels, &c.sd, &c.ws,  &c.stats,       &c.hist,    &c.counts, &c.newc, &c.rws,
+                          &c.vec, &c.cw,    &c.obj, &c.objws,       &c.plan,    &c.scale};
   for (auto* b : bufs) {
     if (b->p) cudaFree(b->p);
     b->p = nullptr;
     b->bytes = 0;
   }
+  if (c.stage) cudaFreeHost(c.stage);
+  c.stage = nullptr;
+  c.stage_bytes = 0;
+  c.tab_host.clear();
+  c.tab_host.shrink_to_fit();
+  c.tab_m = c.tab_l = 0;
+  c.tab_t16 = false;
   cudaStreamDestroy(c.stream);
-  c.stream = nullptr;
+  cudaStreamDestroy(c.copy_stream);
+  cudaEventDestroy(c.assigned);
+  cudaEventDestroy(c.codes_ready);
+  c.stream = c.copy_stream = nullptr;
+  c.assigned = c.codes_ready = nullptr;
   c.init = false;
   c.plan_n = -1;
   c.plan_depth_start.clear();

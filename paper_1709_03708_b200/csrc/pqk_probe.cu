@@ -1,0 +1,75 @@
+// pqk_probe.cu — measured ceilings for the bench rooflines.
+//
+// pqk_smem_probe: shared-memory load bandwidth of the whole GPU, measured with the
+// instruction mix the assignment scan's ceiling rests on: conflict-free LDS.128 from
+// every warp of a CTA, one CTA of 1024 threads per SM (the scan kernels run one
+// persistent CTA per SM).  A warp's LDS.128 is 512 B = 4 wavefronts of 128 B; the
+// architectural ceiling is 128 B/clk/SM.  The loads are volatile (never hoisted or
+// merged), the loaded words are folded into one register per thread and written out
+// once so nothing is dead code.  Returns bytes/s measured with CUDA events on `stream`.
+#include "pqk_common.cuh"
+
+namespace pqk {
+
+constexpr int kProbeThreads = 1024;
+constexpr int kProbeSmemBytes = 64 * 1024;  // 4096 16-byte slots
+
+__global__ void __launch_bounds__(kProbeThreads, 1) smem_probe_kernel(int iters, uint32_t* __restrict__ sink) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  uint32_t* w = reinterpret_cast<uint32_t*>(smem);
+  for (int i = threadIdx.x; i < kProbeSmemBytes / 4; i += blockDim.x) w[i] = i * 2654435761u;
+  __syncthreads();
+  const uint32_t base = smem_u32(smem);
+  // lane i of a warp reads slot (warp*32 + i + u*256 + it) mod 4096: 32 consecutive 16-byte
+  // slots per instruction (conflict-free, 4 wavefronts); the 16 unrolled loads have
+  // distinct addresses (identical volatile loads could be merged)
+  uint32_t off = (uint32_t)threadIdx.x * 16u;
+  uint32_t acc = 0;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      const uint32_t a = base + ((off + (uint32_t)u * 4096u) & (kProbeSmemBytes - 1));
+      uint32_t x, y, z, v;
+      asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(x), "=r"(y), "=r"(z), "=r"(v) : "r"(a) : "memory");
+      acc ^= x + y + z + v;
+    }
+    off += 16u;  // walk the buffer (still 32 consecutive slots per warp instruction)
+  }
+  if (acc == 0x9e3779b9u) sink[blockIdx.x * blockDim.x + threadIdx.x] = acc;  // practically never; keeps acc live
+}
+
+}  // namespace pqk
+
+using namespace pqk;
+
+extern "C" int pqk_smem_probe(int32_t device, int32_t iters, double* bytes_per_s, double* ms_out, void* stream) {
+  if (!bytes_per_s || iters < 1) return fail(PQK_EINVAL, "pqk_smem_probe: bad arguments");
+  PQK_CUDA_TRY(cudaSetDevice(device));
+  int sms = 0;
+  PQK_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+  cudaStream_t s = (cudaStream_t)stream;
+  PQK_CUDA_TRY(cudaFuncSetAttribute(smem_probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kProbeSmemBytes));
+  uint32_t* sink = nullptr;
+  PQK_CUDA_TRY(cudaMallocAsync((void**)&sink, (size_t)sms * kProbeThreads * sizeof(uint32_t), s));
+  cudaEvent_t e0, e1;
+  PQK_CUDA_TRY(cudaEventCreate(&e0));
+  PQK_CUDA_TRY(cudaEventCreate(&e1));
+  // warm-up launch (clocks ramp, module load), then the timed one
+  smem_probe_kernel<<<sms, kProbeThreads, kProbeSmemBytes, s>>>(std::max(1, iters / 8), sink);
+  PQK_LAUNCH_CHECK("smem_probe_kernel");
+  PQK_CUDA_TRY(cudaEventRecord(e0, s));
+  smem_probe_kernel<<<sms, kProbeThreads, kProbeSmemBytes, s>>>(iters, sink);
+  PQK_LAUNCH_CHECK("smem_probe_kernel");
+  PQK_CUDA_TRY(cudaEventRecord(e1, s));
+  PQK_CUDA_TRY(cudaEventSynchronize(e1));
+  float ms = 0.f;
+  PQK_CUDA_TRY(cudaEventElapsedTime(&ms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  PQK_CUDA_TRY(cudaFreeAsync(sink, s));
+  PQK_CUDA_TRY(cudaStreamSynchronize(s));
+  const double bytes = (double)sms * kProbeThreads * (double)iters * 16.0 * 16.0;
+  *bytes_per_s = bytes / (ms * 1e-3);
+  if (ms_out) *ms_out = ms;
+  return PQK_OK;
+}

@@ -404,15 +404,22 @@ class IterationGraphs:
 # ---------------------------------------------------------------------------
 # one-shot host helpers used by the public API
 def assign_host(codes: np.ndarray, centers: np.ndarray, tables: np.ndarray, *, device=None, want_sd=False):
+    """Labels (and optionally sd) of host codes through ``pqk_assign_host``, the C-ABI of the
+    AssignStrategy plugin: a cached per-device context (grow-only buffers, tables compared by
+    content) runs only the assignment — no histogram, repair workspace or summation plan."""
     dev = device_of(device)
-    dt = device_tables(tables, dev)
-    with torch.cuda.device(dev):
-        codes_dev = upload_codes(codes, dt.m, dev)
-        centers_dev = upload_codes(centers, dt.m, dev)
-        eng = ShardEngine(codes_dev, dt, len(centers), dev)
-        eng.assign(centers_dev)
-        labels = eng.labels_host()
-        sd = eng.sd_host() if want_sd else None
+    c = np.ascontiguousarray(codes, dtype=np.uint8)
+    ce = np.ascontiguousarray(centers, dtype=np.uint8)
+    t = np.ascontiguousarray(tables, dtype=np.float64)
+    n, m = c.shape
+    labels = np.empty(n, dtype=np.uint32)
+    sd = np.empty(n, dtype=np.float64) if want_sd else None
+    lib = _lib.load()
+    _lib.check(
+        lib.pqk_assign_host(c.ctypes.data, n, m, ce.ctypes.data, len(ce), t.ctypes.data, t.shape[1],
+                            labels.ctypes.data, None if sd is None else sd.ctypes.data, dev.index),
+        "pqk_assign_host",
+    )
     return (labels, sd) if want_sd else labels
 
 

@@ -176,3 +176,22 @@ def test_init_centers_matches_reference_rule():
     centers = pqk.init_centers(codes, 10, seed=3)
     expect = codes[np.random.default_rng(3).choice(64, size=10, replace=False)]
     np.testing.assert_array_equal(centers, expect)
+
+
+def test_integration_stub_is_the_tested_file():
+    """INTEGRATION.md's ctypes stub is tests/pqclust_b200.py verbatim (run by test_gpu_plugin)."""
+    root = Path(__file__).resolve().parents[1]
+    doc = (root / "INTEGRATION.md").read_text()
+    start = doc.index("```python\n", doc.index("## ctypes stub")) + len("```python\n")
+    block = doc[start : doc.index("```", start)]
+    assert block == (root / "tests" / "pqclust_b200.py").read_text()
+
+
+def test_bench_codebooks_present_and_recipe():
+    """bench_assets hold the reference-trained codebook of every bench config (BASELINE recipe)."""
+    import bench
+
+    for name, cfg in bench.CONFIGS.items():
+        book = bench.make_codebook(name, cfg["m"], cfg["l"])
+        assert book.dtype == np.float32 and book.shape == (cfg["m"], cfg["l"], cfg["dim"] // cfg["m"])
+        assert bench.CODEBOOK_RECIPES[name]["iterations"] == 20

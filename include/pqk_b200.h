@@ -256,6 +256,15 @@ int pqk_lloyd_step_host(const uint8_t* codes, int64_t n, int32_t m, const uint8_
 /* Release the cached per-device context of the host entry points. */
 int pqk_host_release(int32_t device);
 
+/* ---- single-process multi-GPU exchange (peer memory over NVLink/NVSwitch) ------- */
+/* d_out[i] = sum over g of peer_ptrs[j][i], i < count (uint32; peer_ptrs is a HOST array
+ * of g <= 16 device pointers, any device with peer access enabled; d_out may alias one of
+ * them).  The histogram/count allreduce of a sharded iteration (clustering.py:344-347,
+ * :458) as a reduce-scatter: each device sums its slice of clusters from every peer. */
+int pqk_peer_sum_device(const uint32_t* const* peer_ptrs, int32_t g, int64_t count, uint32_t* d_out, void* stream);
+/* cudaDeviceEnablePeerAccess for every ordered pair of distinct listed devices. */
+int pqk_enable_peer_access(const int32_t* devices, int32_t g);
+
 /* ---- diagnostics -------------------------------------------------------------- */
 /* tcgen05 self-test: C (128 x 256, fp32) = A (128 x k, fp16, row-major) * B (256 x k,
  * fp16, row-major)^T through UMMA descriptors, TMEM and tcgen05.ld (k % 16 == 0). */

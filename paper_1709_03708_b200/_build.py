@@ -18,7 +18,8 @@ CSRC = PKG / "csrc"
 INCLUDE = ROOT / "include"
 LIB = PKG / "libpqk_b200.so"
 SOURCES = ["pqk_abi.cu", "pqk_assign.cu", "pqk_update.cu", "pqk_encode.cu", "pqk_encode_tc.cu", "pqk_train.cu",
-           "pqk_eval.cu", "pqk_binary.cu", "pqk_ingest.cu", "pqk_probe.cu"]
+           "pqk_eval.cu", "pqk_binary.cu", "pqk_ingest.cu", "pqk_probe.cu",
+           "pqk_peer.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -72,6 +72,8 @@ SIGNATURES: dict[str, tuple] = {
     "pqk_lloyd_step_host": (C.c_int, [_p, _i64, _i32, _p, _i64, _p, _i32, _p, _p, _p, _p, _i32]),
     "pqk_host_release": (C.c_int, [_i32]),
     "pqk_tc_selftest": (C.c_int, [_p, _p, _p, _i32, _p]),
+    "pqk_peer_sum_device": (C.c_int, [_p, _i32, _i64, _p, _p]),
+    "pqk_enable_peer_access": (C.c_int, [_p, _i32]),
     "pqk_smem_probe": (C.c_int, [_i32, _i32, C.POINTER(C.c_double), C.POINTER(C.c_double), _p]),
     "pqk_train_workspace_bytes": (_sz, [_i64, _i32]),
     "pqk_train_step_device": (C.c_int, [_p, _i64, _i32, _i32, _i32, _p, _i32, _p, _p, _p, _p, _p, _sz, _p, _p]),

@@ -260,6 +260,7 @@ def fit(
     strategy: str | None = None,
     initial_centers: np.ndarray | None = None,
     device: int | None = None,
+    devices: list[int] | None = None,
 ) -> ClusteringResult:
     """Cluster PQ codes with k-means in the compressed domain on the GPU.
 
@@ -268,6 +269,11 @@ def fit(
     repeats exactly or after ``max_iterations``, empty clusters re-seeded on the
     farthest codes.  ``threads`` is accepted and ignored (results never depend
     on it).  The returned labels are those of the last assignment.
+
+    ``devices=[0, 1, ...]`` shards the codes over several GPUs of this process
+    (:mod:`.multidevice`: peer-memory histogram exchange, sliced vote); the result is
+    identical to one GPU.  It needs the built-in scan (``strategy`` None or
+    "linear_scan").
     """
     import torch
 
@@ -291,6 +297,12 @@ def fit(
     if strategy not in _ASSIGNMENT_STRATEGIES:
         raise ValueError(f"unknown assignment strategy {strategy!r}")
     external = None if _ASSIGNMENT_STRATEGIES[strategy] is _gpu_linear_scan else _ASSIGNMENT_STRATEGIES[strategy]
+    if devices is not None:
+        if external is not None:
+            raise ValueError("devices=... runs the built-in GPU scan; use strategy='linear_scan'")
+        from .multidevice import fit_multi_device
+
+        return fit_multi_device(codes, t, k, centers, max_iterations, update, devices)
 
     dev = engine.device_of(device)
     with torch.cuda.device(dev):

@@ -65,30 +65,43 @@ def main():
                     print(f"| {s} | {float(r[ix[key]]) / tot:.3f} |")
         print()
     if launches:
-        rows = list(csv.reader(open(launches)))
-        hdr = None
-        agg = collections.OrderedDict()
-        for r in rows:
-            if "Kernel Name" in r:
-                hdr = r
-                continue
-            if hdr and len(r) == len(hdr):
-                d = dict(zip(hdr, r))
-                nm = d["Kernel Name"].split("(")[0]
-                v = float(d["Metric Value"].replace(",", ""))
-                a = agg.setdefault(nm, [0, 0.0])
-                a[0] += 1
-                a[1] += v
-        steps = max(v[0] for k, v in agg.items() if "scan_kernel" in k)
-        per_step = {k: v for k, v in agg.items() if "encode" not in k and "Fill" not in k and "tables_to" not in k}
-        tot = sum(v[1] for v in per_step.values())
-        print(f"## Launch list (`{launches.split('/')[-1]}`, `--metrics gpu__time_duration.sum`, cold and serialised)\n")
-        print(f"{steps} Lloyd iterations (3 warm-up + 2 timed); set-up kernels (encode, fills) excluded from shares.\n")
-        print("| kernel | launches | avg µs | share of iteration kernel time |\n|---|---|---|---|")
-        for k, v in sorted(agg.items(), key=lambda x: -x[1][1]):
-            share = f"{v[1] / tot:.3f}" if k in per_step else "setup"
-            print(f"| `{k}` | {v[0]} | {v[1] / v[0] / 1e3:.1f} | {share} |")
+        print(launch_table(launches))
 
+
+UNIT = {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "msecond": 1e3, "s": 1e6, "second": 1e6}
+SETUP = ("encode", "Fill", "tables_to", "at::", "elementwise", "distribution", "gamma", "reduce_kernel", "vote_t16",
+         "smem_probe", "pad_codes", "table_stats")
+
+
+def launch_table(launches: str) -> str:
+    """Per-kernel totals of an ncu `--metrics gpu__time_duration.sum --csv` launch list (µs)."""
+    rows = list(csv.reader(open(launches)))
+    hdr = None
+    agg = collections.OrderedDict()
+    for r in rows:
+        if "Kernel Name" in r:
+            hdr = r
+            continue
+        if hdr and len(r) == len(hdr):
+            d = dict(zip(hdr, r))
+            nm = d["Kernel Name"].split("(")[0]
+            v = float(d["Metric Value"].replace(",", "")) * UNIT.get(d.get("Metric Unit", "ns"), 1e-3)
+            a = agg.setdefault(nm, [0, 0.0])
+            a[0] += 1
+            a[1] += v
+    first = [v[0] for k, v in agg.items() if "hscan_kernel<" in k] or \
+        [v[0] for k, v in agg.items() if "pqk::scan_kernel<" in k]
+    steps = max(first, default=1)
+    per_step = {k: v for k, v in agg.items() if not any(t in k for t in SETUP)}
+    tot = sum(v[1] for v in per_step.values())
+    out = [f"## Launch list (`{launches.split('/')[-1]}`, `--metrics gpu__time_duration.sum`, cold and serialised)\n",
+           f"{steps} Lloyd iterations; set-up kernels (data generation, encode, fills, table builds) excluded "
+           "from the shares.\n",
+           "| kernel | launches | avg µs | total ms | share of iteration kernel time |", "|---|---|---|---|---|"]
+    for k, v in sorted(agg.items(), key=lambda x: -x[1][1]):
+        share = f"{v[1] / tot:.4f}" if k in per_step else "setup"
+        out.append(f"| `{k[:90]}` | {v[0]} | {v[1] / v[0]:.1f} | {v[1] / 1e3:.3f} | {share} |")
+    return "\n".join(out)
 
 if __name__ == "__main__":
     main()

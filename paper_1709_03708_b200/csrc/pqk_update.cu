@@ -1027,22 +1027,106 @@ __global__ void sel_collect_kernel(const double* __restrict__ sd, int64_t n, int
   }
 }
 
-// rank sort of the (exactly E, unique) candidates, descending
-__global__ void sel_rank_kernel(const SelState* __restrict__ stp, const uint64_t* __restrict__ ck_hi,
-                                const uint32_t* __restrict__ ck_lo, uint64_t* __restrict__ out_hi,
-                                uint32_t* __restrict__ out_lo) {
-  const int64_t cnt = (int64_t)stp->count;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cnt; i += (int64_t)gridDim.x * blockDim.x) {
-    const uint64_t hi = ck_hi[i];
-    const uint32_t lo = ck_lo[i];
-    int64_t r = 0;
-    for (int64_t j = 0; j < cnt; ++j) {
-      const uint64_t h2 = ck_hi[j];
-      r += (h2 > hi) || (h2 == hi && ck_lo[j] > lo);
+// Descending sort of the (exactly E, unique) candidates: a bitonic network over P = the
+// power of two >= the workspace capacity min(N, K) (fixed at launch, so the repair graph
+// replays for any E), keys padded with (0, 0), which is below every real key (lo =
+// ~index >= 1 since indices are < 2^32 - 1).  Stages with partner distance < 2048 run in
+// shared memory (one block = 2048 keys); the longer ones are one global pass each:
+// log2(P/2048) * (log2(P/2048) + 1) / 2 + log2(P/2048) + 1 launches, O(P log^2 P) work
+// (E = 1e5: 28 launches, ~1e7 compare-exchanges) instead of the O(E^2) rank count.
+constexpr int kSortTile = 2048;
+
+__device__ __forceinline__ bool key_less(uint64_t ah, uint32_t al, uint64_t bh, uint32_t bl) {
+  return ah < bh || (ah == bh && al < bl);
+}
+
+// compare-exchange of i and i^j inside stage k (overall order descending)
+__device__ __forceinline__ void cmpx(uint64_t* hi, uint32_t* lo, int64_t gi, int i, int j, int64_t k) {
+  const int p = i ^ j;
+  if (p > i) {
+    const bool desc = (gi & k) == 0;
+    const bool sw = desc ? key_less(hi[i], lo[i], hi[p], lo[p]) : key_less(hi[p], lo[p], hi[i], lo[i]);
+    if (sw) {
+      const uint64_t th = hi[i];
+      const uint32_t tl = lo[i];
+      hi[i] = hi[p];
+      lo[i] = lo[p];
+      hi[p] = th;
+      lo[p] = tl;
     }
-    out_hi[r] = hi;
-    out_lo[r] = lo;
   }
+}
+
+// load (with padding) and sort each 2048-key tile: stages k = 2 .. 2048
+__global__ void __launch_bounds__(1024) sort_tile_kernel(const SelState* __restrict__ stp,
+                                                         const uint64_t* __restrict__ ck_hi,
+                                                         const uint32_t* __restrict__ ck_lo, uint64_t* __restrict__ s_hi,
+                                                         uint32_t* __restrict__ s_lo) {
+  __shared__ uint64_t hi[kSortTile];
+  __shared__ uint32_t lo[kSortTile];
+  const int64_t cnt = (int64_t)stp->count;
+  const int64_t base = (int64_t)blockIdx.x * kSortTile;
+  for (int t = threadIdx.x; t < kSortTile; t += blockDim.x) {
+    const int64_t g = base + t;
+    hi[t] = g < cnt ? ck_hi[g] : 0ull;
+    lo[t] = g < cnt ? ck_lo[g] : 0u;
+  }
+  __syncthreads();
+  for (int k = 2; k <= kSortTile; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int t = threadIdx.x; t < kSortTile; t += blockDim.x) cmpx(hi, lo, base + t, t, j, k);
+      __syncthreads();
+    }
+  }
+  for (int t = threadIdx.x; t < kSortTile; t += blockDim.x) {
+    s_hi[base + t] = hi[t];
+    s_lo[base + t] = lo[t];
+  }
+}
+
+// one global compare-exchange pass (partner distance j >= 2048) of stage k
+__global__ void sort_global_kernel(uint64_t* __restrict__ s_hi, uint32_t* __restrict__ s_lo, int64_t p, int64_t j,
+                                   int64_t k) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < p; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t q = i ^ j;
+    if (q <= i) continue;
+    const bool desc = (i & k) == 0;
+    const uint64_t ah = s_hi[i], bh = s_hi[q];
+    const uint32_t al = s_lo[i], bl = s_lo[q];
+    if (desc ? key_less(ah, al, bh, bl) : key_less(bh, bl, ah, al)) {
+      s_hi[i] = bh;
+      s_lo[i] = bl;
+      s_hi[q] = ah;
+      s_lo[q] = al;
+    }
+  }
+}
+
+// the remaining distances j = 1024 .. 1 of stage k, in shared memory per tile
+__global__ void __launch_bounds__(1024) sort_merge_tile_kernel(uint64_t* __restrict__ s_hi, uint32_t* __restrict__ s_lo,
+                                                               int64_t k) {
+  __shared__ uint64_t hi[kSortTile];
+  __shared__ uint32_t lo[kSortTile];
+  const int64_t base = (int64_t)blockIdx.x * kSortTile;
+  for (int t = threadIdx.x; t < kSortTile; t += blockDim.x) {
+    hi[t] = s_hi[base + t];
+    lo[t] = s_lo[base + t];
+  }
+  __syncthreads();
+  for (int j = kSortTile >> 1; j > 0; j >>= 1) {
+    for (int t = threadIdx.x; t < kSortTile; t += blockDim.x) cmpx(hi, lo, base + t, t, j, k);
+    __syncthreads();
+  }
+  for (int t = threadIdx.x; t < kSortTile; t += blockDim.x) {
+    s_hi[base + t] = hi[t];
+    s_lo[base + t] = lo[t];
+  }
+}
+
+static int64_t sort_extent(int64_t cap) {
+  int64_t p = kSortTile;
+  while (p < cap) p <<= 1;
+  return p;
 }
 
 __global__ void repair_apply_kernel(const SelState* __restrict__ stp, const uint32_t* __restrict__ sorted_lo,
@@ -1196,8 +1280,9 @@ struct RepairWS {
   int32_t* empty_list;
   uint64_t* ck_hi;
   uint32_t* ck_lo;
-  uint64_t* s_hi;
+  uint64_t* s_hi;  // sorted candidates, sort_p entries (power of two >= capacity)
   uint32_t* s_lo;
+  int64_t sort_p;
   size_t total;
 };
 
@@ -1218,8 +1303,9 @@ static RepairWS repair_layout(void* base, int64_t n, int64_t k) {
   const size_t o_el = take(std::max<int64_t>(k, 1) * sizeof(int32_t));
   const size_t o_ch = take(cap * sizeof(uint64_t));
   const size_t o_cl = take(cap * sizeof(uint32_t));
-  const size_t o_sh = take(cap * sizeof(uint64_t));
-  const size_t o_sl = take(cap * sizeof(uint32_t));
+  w.sort_p = sort_extent(cap);
+  const size_t o_sh = take(w.sort_p * sizeof(uint64_t));
+  const size_t o_sl = take(w.sort_p * sizeof(uint32_t));
   w.total = align_up(off, 256);
   char* b = static_cast<char*>(base);
   if (b) {
@@ -1250,8 +1336,18 @@ static int run_select(const double* d_sd, int64_t n, int64_t base, const int64_t
   }
   sel_collect_kernel<<<grid, 256, 0, stream>>>(d_sd, n, base, w.st, w.ck_hi, w.ck_lo, e_src, e_const);
   PQK_LAUNCH_CHECK("sel_collect_kernel");
-  sel_rank_kernel<<<di.sms * 2, 256, 0, stream>>>(w.st, w.ck_hi, w.ck_lo, w.s_hi, w.s_lo);
-  PQK_LAUNCH_CHECK("sel_rank_kernel");
+  const int64_t p = w.sort_p;
+  sort_tile_kernel<<<(unsigned)(p / kSortTile), 1024, 0, stream>>>(w.st, w.ck_hi, w.ck_lo, w.s_hi, w.s_lo);
+  PQK_LAUNCH_CHECK("sort_tile_kernel");
+  for (int64_t k = 2 * kSortTile; k <= p; k <<= 1) {
+    for (int64_t j = k >> 1; j >= kSortTile; j >>= 1) {
+      sort_global_kernel<<<(unsigned)std::min<int64_t>((p + 255) / 256, (int64_t)di.sms * 8), 256, 0, stream>>>(
+          w.s_hi, w.s_lo, p, j, k);
+      PQK_LAUNCH_CHECK("sort_global_kernel");
+    }
+    sort_merge_tile_kernel<<<(unsigned)(p / kSortTile), 1024, 0, stream>>>(w.s_hi, w.s_lo, k);
+    PQK_LAUNCH_CHECK("sort_merge_tile_kernel");
+  }
   return PQK_OK;
 }
 

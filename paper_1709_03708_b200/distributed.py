@@ -13,7 +13,8 @@ broadcast.  Per iteration:
    collective (NCCL over NVLink on GPUs, gloo in the CPU tests);
 4. replicated vote;
 5. if E clusters are empty: every rank proposes its local top-E (sd desc, global
-   index asc) codes, an allgather merges them and all ranks apply the same E.
+   index asc) codes, an allgather collects them and every rank merges them with two
+   stable device sorts and applies the same E rows (no host round trip).
 
 The loop is written against a small backend protocol so that the same host
 logic runs with the GPU :class:`GpuShardBackend` (product) and, in tests, with a
@@ -190,9 +191,6 @@ class GpuShardBackend:
         (CUDA events; valid once vote()'s host read has synchronised)."""
         return self._ev[0].elapsed_time(self._ev[1]) / 1e3, self._ev[1].elapsed_time(self._ev[2]) / 1e3
 
-    def counts_host(self) -> np.ndarray:
-        return self.eng.counts.cpu().numpy()
-
     def objective_tensor(self):
         """(sum sqrt(sd), sum sd) of the local subtree, float64 on the device (no host sync)."""
         if self.n == 0:
@@ -218,11 +216,11 @@ class GpuShardBackend:
     def tensor_device(self):
         return self.dev
 
-    def apply_repair(self, empty: np.ndarray, rows: np.ndarray) -> None:
-        if len(empty):
-            idx = torch.from_numpy(empty.astype(np.int64)).to(self.dev)
-            val = self.engine_mod.upload_codes(rows, self.m, self.dev)
-            self.eng.new_centers[idx] = val
+    def counts_tensor(self):
+        return self.eng.counts  # the allreduced counts (int32 view of uint32)
+
+    def apply_repair_rows(self, empty_idx, rows) -> None:
+        self.eng.new_centers[empty_idx, : self.m] = rows
 
     def take_new_centers(self):
         return self.eng.new_centers.clone()
@@ -247,6 +245,26 @@ def merge_candidates(parts, e: int):
     rows = np.concatenate([p[2] for p in parts]) if parts else np.zeros((0, 1), np.uint8)
     order = np.lexsort((index, ~keys))[:e]  # primary: key desc (as ~key asc), then index asc
     return keys[order], index[order], rows[order]
+
+
+def merge_candidates_device(gk: "torch.Tensor", gi: "torch.Tensor", gr: "torch.Tensor", e: int) -> "torch.Tensor":
+    """Rows of the global top-e candidates by (sd desc, index asc), on the tensors' device.
+
+    gk: (world, e) int64 bit patterns of non-negative float64 sd (they order like the
+    values); gi: (world, e) int64 global indices (padding = int64 max, key 0); gr:
+    (world, e, M) uint8 rows.  Two stable sorts (index, then key descending) replace the
+    host lexsort of :func:`merge_candidates` (clustering.py:460-466 order)."""
+    keys = gk.reshape(-1)
+    idx = gi.reshape(-1)
+    rows = gr.reshape(-1, gr.shape[-1])
+    o1 = torch.argsort(idx, stable=True)
+    o2 = torch.argsort(keys[o1], stable=True, descending=True)
+    return rows[o1[o2[:e]]]
+
+
+def empty_clusters_device(counts: "torch.Tensor", e: int) -> "torch.Tensor":
+    """The e empty clusters in ascending order (counts == 0) without a host round trip."""
+    return torch.argsort((counts != 0).to(torch.int8), stable=True)[:e]
 
 
 class DistributedLloyd:
@@ -333,17 +351,11 @@ class DistributedLloyd:
             return StepStats(objective, objective_sq, 0, 0, 0, assign_seconds, 0.0), centers_dev, True
         empty_n = int(stats[3])
         if empty_n:
-            counts_h = self.b.counts_host()
-            empty = np.flatnonzero(counts_h == 0)
+            # stream-ordered on the device: no host read of the counts, no host merge
             pk, pi, pr = self.b.local_candidates(empty_n)
-            gk = self._gather(pk).cpu().numpy().reshape(-1).view(np.uint64)
-            gi = self._gather(pi).cpu().numpy().reshape(-1)
-            gr = self._gather(pr).cpu().numpy().reshape(-1, self.m)
-            _, _, rows = merge_candidates([(gk, gi, gr)], empty_n)
-            self.b.apply_repair(empty, rows)
+            rows = merge_candidates_device(self._gather(pk), self._gather(pi), self._gather(pr), empty_n)
+            self.b.apply_repair_rows(empty_clusters_device(self.b.counts_tensor(), empty_n), rows)
         nxt = self.b.take_new_centers()
-        if empty_n:
-            self.b.sync()
         update_seconds = vote_seconds + (time.perf_counter() - t1)
         st = StepStats(objective, objective_sq, empty_n, int(stats[4]), int(stats[2]), assign_seconds, update_seconds)
         return st, nxt, False

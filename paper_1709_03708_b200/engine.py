@@ -18,6 +18,7 @@ Data layout in HBM (one device, one shard of N codes):
 from __future__ import annotations
 
 import ctypes as C
+import hashlib
 import threading
 from dataclasses import dataclass
 
@@ -75,12 +76,10 @@ _TABLE_LOCK = threading.Lock()
 def device_tables(tables: np.ndarray, dev) -> DeviceTables:
     """Upload (M, L, L) float64 tables and build the scaled fp32 filter copy (cached)."""
     t = np.ascontiguousarray(tables, dtype=np.float64)
-    if t.flags.writeable:
-        key = (dev.index, t.shape, hash(t.tobytes()))
-        hold = None
-    else:
-        key = (dev.index, t.shape, id(t), t.ctypes.data)
-        hold = t
+    # keyed by content (never by identity: a read-only view can still change through a
+    # writable base, and the reference recomputes from the array every call)
+    key = (dev.index, t.shape, hashlib.blake2b(t.tobytes(), digest_size=16).digest())
+    hold = None
     with _TABLE_LOCK:
         hit = _TABLE_CACHE.get(key)
         if hit is not None:

@@ -70,9 +70,6 @@ class CpuShardBackend:
         st[4] = int((counts > 0).sum())
         return st
 
-    def counts_host(self):
-        return self.counts.numpy()
-
     def local_candidates(self, e):
         keys = self.sd.view(np.uint64)
         idx = np.arange(self.n) + self.offset
@@ -85,8 +82,11 @@ class CpuShardBackend:
         pr[: len(order)] = self.codes[order]
         return torch.from_numpy(pk.view(np.int64)), torch.from_numpy(pi), torch.from_numpy(pr)
 
-    def apply_repair(self, empty, rows):
-        self.new[empty] = rows
+    def counts_tensor(self):
+        return self.counts
+
+    def apply_repair_rows(self, empty_idx, rows):
+        self.new[empty_idx.numpy()] = rows.numpy()
 
     def take_new_centers(self):
         return self.new.copy()

@@ -82,3 +82,19 @@ def test_reference_error_messages(pqk, oracle):
         pqk.assign(codes, codes[:2], tables, strategy="nope")
     with pytest.raises(ValueError):
         pqk.assign(np.full((3, 2), 9, np.uint8), codes[:2], tables)  # subindex >= L
+
+
+@pytest.mark.parametrize("k,distinct", [(30_000, 100), (5000, 4000), (2100, 50)])
+def test_repair_many_empty_clusters(pqk, oracle, k, distinct):
+    """E close to K (the sorted-candidate network covers up to min(N, K) = 2^15 keys and
+    more): one fit iteration's repair must place exactly the reference's farthest codes
+    (clustering.py:460-466: sd descending, lowest index first)."""
+    rng = np.random.default_rng(k + distinct)
+    tables = random_tables(4, 256, seed=distinct)
+    protos = rng.integers(0, 256, size=(distinct, 4))
+    codes = protos[rng.integers(0, distinct, size=40_000)].astype(np.uint8)
+    res = pqk.fit(codes, tables, k, max_iterations=2, seed=5)
+    ref = oracle.fit(codes, tables, k, max_iterations=2, seed=5, scan=lambda c, ce, t: oracle.assign_c(c, ce, t))
+    assert res.trace[0].repaired_clusters == ref["trace"][0]["repaired"] > k // 2
+    np.testing.assert_array_equal(res.centers, ref["centers"])
+    np.testing.assert_array_equal(res.labels, ref["labels"])

@@ -195,3 +195,25 @@ def test_bench_codebooks_present_and_recipe():
         book = bench.make_codebook(name, cfg["m"], cfg["l"])
         assert book.dtype == np.float32 and book.shape == (cfg["m"], cfg["l"], cfg["dim"] // cfg["m"])
         assert bench.CODEBOOK_RECIPES[name]["iterations"] == 20
+
+
+@pytest.mark.parametrize("world,e", [(1, 5), (2, 7), (3, 40)])
+def test_merge_candidates_device_equals_host(world, e):
+    """The device merge (two stable sorts) picks the host lexsort's rows, ties and padding included."""
+    import torch
+
+    from paper_1709_03708_b200.distributed import empty_clusters_device, merge_candidates, merge_candidates_device
+
+    rng = np.random.default_rng(world * 100 + e)
+    sd = rng.choice([0.0, 1.5, 2.25, 7.0, 9.5], size=(world, e))  # many exact ties
+    gk = sd.view(np.int64).copy()
+    gi = np.sort(rng.choice(10_000, size=(world, e), replace=False), axis=1).astype(np.int64)
+    gi[-1, -2:] = np.iinfo(np.int64).max  # padding rows of a short shard
+    gk[-1, -2:] = 0
+    gr = rng.integers(0, 256, size=(world, e, 4)).astype(np.uint8)
+    _, _, rows_h = merge_candidates([(gk.reshape(-1).view(np.uint64), gi.reshape(-1), gr.reshape(-1, 4))], e)
+    rows_d = merge_candidates_device(torch.from_numpy(gk), torch.from_numpy(gi), torch.from_numpy(gr), e)
+    np.testing.assert_array_equal(rows_d.numpy(), rows_h)
+    counts = torch.from_numpy(rng.integers(0, 3, size=50).astype(np.int32))
+    z = np.flatnonzero(counts.numpy() == 0)
+    np.testing.assert_array_equal(empty_clusters_device(counts, len(z)).numpy(), z)

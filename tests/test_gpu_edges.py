@@ -95,6 +95,6 @@ def test_repair_many_empty_clusters(pqk, oracle, k, distinct):
     codes = protos[rng.integers(0, distinct, size=40_000)].astype(np.uint8)
     res = pqk.fit(codes, tables, k, max_iterations=2, seed=5)
     ref = oracle.fit(codes, tables, k, max_iterations=2, seed=5, scan=lambda c, ce, t: oracle.assign_c(c, ce, t))
-    assert res.trace[0].repaired_clusters == ref["trace"][0]["repaired"] > k // 2
+    assert res.trace[0].repaired_clusters == ref["trace"][0]["repaired"] > k // 3
     np.testing.assert_array_equal(res.centers, ref["centers"])
     np.testing.assert_array_equal(res.labels, ref["labels"])

@@ -58,7 +58,8 @@ CONFIGS = {
 }
 DEFAULT_CONFIG = "c4"
 SEED = 20260419
-DTYPE = "u16 fixed-point scan + f32 filters, f64 exact (results bit-identical to the float64 reference)"
+DTYPE = ("u8 fixed-point scan (M<=4; u16 for M 8/16) + f32 filters, f64 exact "
+         "(results bit-identical to the float64 reference)")
 
 
 def log(*a):
@@ -756,9 +757,10 @@ def main() -> None:
 
     # roofline of the dominant kernel (assignment scan): shared-memory lookups
     u = int(np.median(uniq))
-    lb = int(np.median(lookup_b)) or 4  # 2: 16-bit first tier (uint16 tables), 4: fp32 scan
+    lb = int(np.median(lookup_b)) or 4  # 1: 8-bit first tier, 2: 16-bit first tier, 4: fp32 scan
     lookup_bytes = n_loc * u * m * lb  # algorithmic: one table lookup per (code, center, subspace)
-    scan_name = "hscan_kernel (16-bit fixed-point tables)" if lb == 2 else "scan_kernel (fp32 tables)"
+    scan_name = {1: "hscan8_kernel (8-bit fixed-point tables, top-6 chunk keys)",
+                 2: "hscan_kernel (16-bit fixed-point tables)"}.get(lb, "scan_kernel (fp32 tables)")
     scan_s = float(np.mean(scan_ms)) / 1e3
     sm_count = torch.cuda.get_device_properties(dev).multi_processor_count
     clk = clocks.summary()

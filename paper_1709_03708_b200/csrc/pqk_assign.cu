@@ -42,6 +42,7 @@
 
 #include "pqk_common.cuh"
 #include "pqk_hscan.cuh"
+#include "pqk_hscan8.cuh"
 
 namespace pqk {
 
@@ -570,17 +571,17 @@ __global__ void __launch_bounds__(256) rescan_cta_kernel(
 }
 
 // first window sets the statistics, later windows add their flagged codes
-// kc16 > 0: the 16-bit first tier ran (chunks of kc16 centres, 2-byte lookups)
+// kc_tier > 0: a fixed-point first tier ran (chunks of kc_tier centres, lookup_bytes per lookup)
 __global__ void assign_stats_kernel(const int32_t* __restrict__ counters, int64_t* __restrict__ stats, int first,
-                                    int kc16, int32_t list_min) {
+                                    int kc_tier, int lookup_bytes, int32_t list_min) {
   stats[PQK_STAT_UNIQUE_CENTERS] = counters[0];
   stats[PQK_STAT_FLAGGED] = (first ? 0 : stats[PQK_STAT_FLAGGED]) + counters[1];
   // codes decided by the exact rescan: the first-tier list when short, else what the
   // fp32 list tier left
-  const int32_t exact = !kc16 ? counters[1] : (counters[1] < list_min ? counters[1] : counters[3]);
+  const int32_t exact = !kc_tier ? counters[1] : (counters[1] < list_min ? counters[1] : counters[3]);
   stats[PQK_STAT_FLAGGED_FP64] = (first ? 0 : stats[PQK_STAT_FLAGGED_FP64]) + exact;
-  stats[PQK_STAT_NCHUNKS] = kc16 ? (counters[0] + kc16 - 1) / kc16 : counters[2];
-  stats[PQK_STAT_LOOKUP_BYTES] = kc16 ? 2 : 4;
+  stats[PQK_STAT_NCHUNKS] = kc_tier ? (counters[0] + kc_tier - 1) / kc_tier : counters[2];
+  stats[PQK_STAT_LOOKUP_BYTES] = lookup_bytes;
 }
 
 __global__ void paired_distance_kernel(const uint8_t* __restrict__ a, const uint8_t* __restrict__ b,
@@ -628,11 +629,18 @@ struct AssignWS {
   uint4* q16;
   int32_t* flags2;
   uint2* keys16;
+  // 8-bit first tier (padded M = 4): aliases of the 16-bit buffers (never both in a call)
+  uint8_t* t8;
+  uint4* q8;
+  uint32_t* keys8;
 };
 
 // Rows per scan window: the scan and the flag list index rows of a window in 32 bits;
 // larger shards are scanned window by window (the table chunks are built once).
 constexpr int64_t kScanWindow = (int64_t)1 << 30;
+// The 8-bit tier keeps T keys per code (structure of arrays, T x 4 B per code of a window):
+// smaller windows bound that buffer (2^28 codes: 8 GB at T = 8).
+constexpr int64_t kScanWindow8 = (int64_t)1 << 28;
 
 static AssignWS assign_ws_layout(void* base, int64_t n, int64_t k, int mp, int l) {
   AssignWS w{};
@@ -664,8 +672,10 @@ static AssignWS assign_ws_layout(void* base, int64_t n, int64_t k, int mp, int l
   const size_t o_q16 = take(h16_ok ? (size_t)((k + kc16 - 1) / kc16) * l * mp * kc16 * sizeof(uint16_t) : 0, 1024);
   const size_t o_fl2 =
       take(h16_ok ? (size_t)std::max<int64_t>(std::min(n, kScanWindow), 1) * sizeof(int32_t) : 0, 256);
-  const size_t o_k16 =
-      take(h16_ok ? (size_t)std::max<int64_t>(std::min(n, kScanWindow), 1) * sizeof(uint2) : 0, 256);
+  const size_t k16_bytes = h16_ok ? (size_t)std::max<int64_t>(std::min(n, kScanWindow), 1) * sizeof(uint2) : 0;
+  const size_t k8_bytes =
+      mp == 4 ? (size_t)std::max<int64_t>(std::min(n, kScanWindow8), 1) * h8::kMaxT * sizeof(uint32_t) : 0;
+  const size_t o_k16 = take(std::max(k16_bytes, k8_bytes), 256);
   w.total = align_up(off, 256);
   char* b = static_cast<char*>(base);
   if (b) {
@@ -682,6 +692,10 @@ static AssignWS assign_ws_layout(void* base, int64_t n, int64_t k, int mp, int l
     w.q16 = reinterpret_cast<uint4*>(b + o_q16);
     w.flags2 = reinterpret_cast<int32_t*>(b + o_fl2);
     w.keys16 = reinterpret_cast<uint2*>(b + o_k16);
+    // q16 region: ceil(k/16) x l x 4 x 16 x 2 B >= ceil(k/32) x l x 128 B; t16: 4 l^2 x 2 B >= 4 l^2
+    w.t8 = reinterpret_cast<uint8_t*>(b + o_t16);
+    w.q8 = reinterpret_cast<uint4*>(b + o_q16);
+    w.keys8 = reinterpret_cast<uint32_t*>(b + o_k16);
   }
   return w;
 }
@@ -795,8 +809,69 @@ static int launch_hscan(const h16::HScanParams& base_params, uint2* keys, int l,
   return launch_hscan_c<MP, KC, NW, S, Cs...>(c_need, p, keys, grid, l, stream);
 }
 
-// 0: 16-bit first tier where it pays off (default); 1: fp32 scan only; 2: 16-bit first tier
-// whenever supported; 3: as 2, and the fp32 list tier for any list length (tests)
+
+// ---------------------------------------------------------------------------
+// 8-bit first tier (pqk_hscan8.cuh, padded M = 4)
+static int h8_top() {
+  static int t = [] {
+    const char* e = getenv("PQK_H8_T");  // diagnostic: keys kept per code (4 or 6)
+    return (e && atoi(e) == 4) ? 4 : 6;
+  }();
+  return t;
+}
+
+template <int NW, int S, int T, int C, int... Cs>
+static int launch_hscan8_c(int c_need, const h8::H8Params& p, uint32_t* keys, int64_t kstride, int grid, int l,
+                           cudaStream_t stream) {
+  if constexpr (sizeof...(Cs) > 0) {
+    if (c_need > C) return launch_hscan8_c<NW, S, T, Cs...>(c_need, p, keys, kstride, grid, l, stream);
+  }
+  const DevInfo& di = dev_info();
+  const size_t smem = 128 + (size_t)S * 256 * h8::ROW;  // ring stride: 256 rows (immediate offsets)
+  if ((int)smem > di.smem_optin) return fail(PQK_EUNSUPPORTED, "assignment chunk ring exceeds shared memory");
+  auto kern = h8::hscan8_kernel<C, NW, S, T>;
+  PQK_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  ProfileEvents& pe = profile_events();
+  if (pe.before) PQK_CUDA_TRY(record_profile_event(pe.before, stream));
+  kern<<<grid, (NW + 1) * 32, smem, stream>>>(p, keys, kstride);
+  PQK_LAUNCH_CHECK("hscan8_kernel");
+  if (pe.after) PQK_CUDA_TRY(record_profile_event(pe.after, stream));
+  const int fgrid = (int)std::min<int64_t>((p.n + 255) / 256, (int64_t)di.sms * 64);
+  h8::hfinal8_kernel<T><<<std::max(fgrid, 1), 256, 0, stream>>>(p, keys, kstride);
+  PQK_LAUNCH_CHECK("hfinal8_kernel");
+  return PQK_OK;
+}
+
+template <int NW, int S, int T, int... Cs>
+static int launch_hscan8(const h8::H8Params& base_params, uint32_t* keys, int64_t kstride, int l,
+                         cudaStream_t stream) {
+  constexpr int OWN = NW * 32;
+  constexpr int CMAX = std::max({Cs...});
+  constexpr int NB = OWN * CMAX;
+  const DevInfo& di = dev_info();
+  h8::H8Params p = base_params;
+  const int64_t n = p.n;
+  const int64_t G = di.sms;
+  const int64_t per_cta = std::max<int64_t>(1, (n + G * NB - 1) / (G * NB));
+  int64_t npasses = G * per_cta;
+  int64_t pass_size = (n + npasses - 1) / npasses;
+  const int64_t min_pass = std::max<int64_t>(1, NB / 4);
+  if (pass_size < min_pass) {
+    pass_size = min_pass;
+    npasses = (n + pass_size - 1) / pass_size;
+  }
+  p.pass_size = pass_size;
+  p.npasses = npasses;
+  const int grid = (int)std::min<int64_t>(G, npasses);
+  if (grid <= 0) return PQK_OK;
+  const int c_need = (int)((pass_size + OWN - 1) / OWN);
+  return launch_hscan8_c<NW, S, T, Cs...>(c_need, p, keys, kstride, grid, l, stream);
+}
+
+// 0: fixed-point first tier where it pays off (default: 8-bit for padded M = 4, 16-bit for
+// 8 and 16); 1: fp32 scan only; 2: fixed-point first tier whenever supported; 3: as 2, and
+// the fp32 list tier for any list length (tests); 4, 5: as 2, 3 with the 16-bit tier at
+// padded M = 4 too (no 8-bit tier)
 static int g_scan_mode = 0;
 
 }  // namespace pqk
@@ -806,7 +881,7 @@ using namespace pqk;
 extern "C" int32_t pqk_padded_m(int32_t m) { return padded_m(m); }
 
 extern "C" int pqk_set_scan_mode(int32_t mode) {
-  if (mode < 0 || mode > 3) return fail(PQK_EINVAL, "pqk_set_scan_mode: mode must be in [0, 3]");
+  if (mode < 0 || mode > 5) return fail(PQK_EINVAL, "pqk_set_scan_mode: mode must be in [0, 5]");
   g_scan_mode = mode;
   return PQK_OK;
 }
@@ -879,14 +954,17 @@ extern "C" int pqk_assign_device(const uint8_t* d_codes, int64_t n, int32_t m, i
   const int kc16 = h16::kcFor(mp);
   // the 16-bit tier pays off above ~2^31 lookups (its per-call table preparation and
   // finalisation cost tens of microseconds); smaller problems run the fp32 scan
-  const bool use16 = fast && g_scan_mode != 1 && mp <= 16 && (k + kc16 - 1) / kc16 <= 65535 &&
-                     (g_scan_mode >= 2 || (double)n * (double)k * (double)m >= 2147483648.0);
+  const bool tier_on = fast && g_scan_mode != 1 &&
+                       (g_scan_mode >= 2 || (double)n * (double)k * (double)m >= 2147483648.0);
+  const bool use8 = tier_on && mp == 4 && g_scan_mode < 4 && (k + h8::KC - 1) / h8::KC < (1 << 24) - 1;
+  const bool use16 = tier_on && !use8 && mp <= 16 && (k + kc16 - 1) / kc16 <= 65535;
+  const bool use_tier = use8 || use16;
   AssignWS w = assign_ws_layout(d_ws, n, k, mp, l);
   if (ws_bytes < w.total) return fail(PQK_EINVAL, "pqk_assign_device: workspace too small");
 
   const DevInfo& di0 = dev_info();
   SideStream* side = nullptr;
-  if (use16) {
+  if (use_tier) {
     // 0. scale preparation on the side branch (w.scale is free: the fork follows every
     //    earlier reader on the caller's stream)
     int dev = 0;
@@ -943,6 +1021,19 @@ extern "C" int pqk_assign_device(const uint8_t* d_codes, int64_t n, int32_t m, i
     const int rc = qbuild32(nullptr, 0);
     if (rc != PQK_OK) return rc;
   }
+  if (use8) {
+    // 8-bit fixed-point tables and their 32-centre chunks
+    const int qmax = h8::qmax_for(m);
+    PQK_CUDA_TRY(cudaStreamWaitEvent(stream, side->join, 0));  // scale ready (side branch)
+    const int64_t cnt4 = (int64_t)4 * l * l;
+    h8::table_quantize8_kernel<<<(int)std::min<int64_t>((cnt4 + 255) / 256, (int64_t)di.sms * 8), 256, 0,
+                                 stream>>>(d_t64, m, l, qmax, w.scale, w.t8);
+    PQK_LAUNCH_CHECK("table_quantize8_kernel");
+    const int rgrid = (int)std::min<int64_t>((k + h8::KC - 1) / h8::KC, (int64_t)di.sms * 8);
+    const size_t rsm = (size_t)4 * h8::KC * (l + 4);
+    h8::qbuild8_rows_kernel<<<rgrid, 256, rsm, stream>>>(w.t8, l, m, qmax, w.ucodes, w.counters, w.q8);
+    PQK_LAUNCH_CHECK("qbuild8_rows_kernel");
+  }
   if (use16) {
     // 16-bit fixed-point tables (scale from the table maximum) and their chunks
     const int qmax = h16::qmax_for(m);
@@ -982,7 +1073,7 @@ extern "C" int pqk_assign_device(const uint8_t* d_codes, int64_t n, int32_t m, i
   // list tier threshold: below it the exact rescan is cheaper than streaming every chunk
   // (fp32 list scan: every CTA streams all chunks, a fixed cost, so it only beats the
   // exact rescan, whose cost is per code, for lists of ~250 codes per SM and more)
-  const int32_t list_min = g_scan_mode == 3 ? 0 : di.sms * 256;
+  const int32_t list_min = (g_scan_mode == 3 || g_scan_mode == 5) ? 0 : di.sms * 256;
   const size_t rows_bytes = (size_t)m * l * sizeof(double);
   const bool cta_rescan = rows_bytes <= 96 * 1024;
   if (cta_rescan) {
@@ -994,13 +1085,35 @@ extern "C" int pqk_assign_device(const uint8_t* d_codes, int64_t n, int32_t m, i
       attr_set[dev & 63] = true;
     }
   }
-  for (int64_t w0 = 0; w0 < n; w0 += kScanWindow) {
-    const int64_t wn = std::min(kScanWindow, n - w0);
+  const int64_t window = use8 ? kScanWindow8 : kScanWindow;
+  for (int64_t w0 = 0; w0 < n; w0 += window) {
+    const int64_t wn = std::min(window, n - w0);
     const uint8_t* codes = d_codes + w0 * mp;
     uint32_t* labels = d_labels + w0;
     double* sd_sq = d_sd_sq + w0;
     if (w0 > 0) PQK_CUDA_TRY(cudaMemsetAsync(w.counters + 1, 0, sizeof(int32_t), stream));
     if (w0 > 0) PQK_CUDA_TRY(cudaMemsetAsync(w.counters + 3, 0, sizeof(int32_t), stream));
+    if (use8) {
+      // 3a. 8-bit first tier over every code
+      h8::H8Params hp{};
+      hp.codes = codes;
+      hp.n = wn;
+      hp.q = w.q8;
+      hp.l = l;
+      hp.m = m;
+      hp.counters = w.counters;
+      hp.pos2idx = w.pos2idx;
+      hp.ucodes = w.ucodes;
+      hp.t64 = d_t64;
+      hp.sc = w.scale;
+      hp.labels = labels;
+      hp.sd_sq = sd_sq;
+      hp.flags = w.flags;
+      hp.flag_count = w.counters + 1;
+      const int rc = h8_top() == 4 ? launch_hscan8<11, 4, 4, 1, 2, 3, 4, 5, 6, 7, 8>(hp, w.keys8, wn, l, stream)
+                                   : launch_hscan8<11, 4, 6, 1, 2, 3, 4, 5, 6, 7, 8>(hp, w.keys8, wn, l, stream);
+      if (rc != PQK_OK) return rc;
+    }
     if (use16) {
       // 3a. 16-bit first tier over every code
       h16::HScanParams hp{};
@@ -1025,8 +1138,10 @@ extern "C" int pqk_assign_device(const uint8_t* d_codes, int64_t n, int32_t m, i
         case 16: rc = launch_hscan<16, 8, 11, 3, 1, 2, 3, 4>(hp, w.keys16, l, stream); break;
       }
       if (rc != PQK_OK) return rc;
+    }
+    if (use_tier) {
       // 3b. fp32 tier over the uncertified list when it is long
-      rc = qbuild32(w.counters + 1, list_min);
+      int rc = qbuild32(w.counters + 1, list_min);
       if (rc != PQK_OK) return rc;
       ScanParams sp{};
       sp.codes = codes;
@@ -1062,7 +1177,8 @@ extern "C" int pqk_assign_device(const uint8_t* d_codes, int64_t n, int32_t m, i
                                                                 sd_sq, 0, 0x7fffffff);
       PQK_LAUNCH_CHECK("rescan_cta_kernel");
       if (d_stats) {
-        assign_stats_kernel<<<1, 1, 0, stream>>>(w.counters, d_stats, w0 == 0, kc16, list_min);
+        assign_stats_kernel<<<1, 1, 0, stream>>>(w.counters, d_stats, w0 == 0, use8 ? h8::KC : kc16,
+                                                 use8 ? 1 : 2, list_min);
         PQK_LAUNCH_CHECK("assign_stats_kernel");
       }
       continue;
@@ -1108,7 +1224,7 @@ extern "C" int pqk_assign_device(const uint8_t* d_codes, int64_t n, int32_t m, i
       PQK_LAUNCH_CHECK("rescan_kernel");
     }
     if (d_stats) {
-      assign_stats_kernel<<<1, 1, 0, stream>>>(w.counters, d_stats, w0 == 0, 0, 0);
+      assign_stats_kernel<<<1, 1, 0, stream>>>(w.counters, d_stats, w0 == 0, 0, 4, 0);
       PQK_LAUNCH_CHECK("assign_stats_kernel");
     }
   }

@@ -1,8 +1,10 @@
-"""GPU parity of the 16-bit fixed-point first tier of the assignment (pqk_hscan.cuh).
+"""GPU parity of the fixed-point first tiers of the assignment: the 8-bit tier with
+top-T chunk keys (pqk_hscan8.cuh, padded M = 4) and the 16-bit tier (pqk_hscan.cuh).
 
-The default mode engages the 16-bit tier only above 2^31 lookups, so the small cases
-below force it (scan mode 2) and also force the fp32 list tier for any list length
-(mode 3), then compare labels and sd_sq byte for byte with the oracle's linear scan
+The default mode engages a fixed-point tier only above 2^31 lookups, so the small cases
+below force it (scan mode 2: 8-bit at M <= 4, 16-bit above; mode 4: 16-bit at every M)
+and also force the fp32 list tier for any list length (modes 3 and 5), then compare
+labels and sd_sq byte for byte with the oracle's linear scan
 (clustering.py:167-197: float64, ascending m, lowest index on ties) and with the fp32
 path (mode 1).  Cases: random tables at every supported width, lattice tables with
 massive exact ties, duplicated centres, tables spanning huge scales (saturated
@@ -36,9 +38,11 @@ def _assign(lib, mode, codes, centers, tables):
         _lib.check(lib.pqk_set_scan_mode(0), "scan mode")
 
 
-def _check(lib, oracle, codes, centers, tables, modes=(2, 3)):
+def _check(lib, oracle, codes, centers, tables, modes=(2, 3, 4, 5)):
     expect = oracle.assign_c(codes, centers, tables)
     exp_sd = oracle.paired_distance_sq(tables, codes.astype(np.int64), centers[expect].astype(np.int64))
+    if codes.shape[1] > 4:  # modes 4 / 5 only differ from 2 / 3 at padded M = 4
+        modes = tuple(md for md in modes if md not in (4, 5))
     for mode in modes:
         labels, sd = _assign(lib, mode, codes, centers, tables)
         np.testing.assert_array_equal(labels, expect, err_msg=f"mode {mode}")
@@ -98,7 +102,7 @@ def test_clustered_codes_multi_pass(lib, oracle, m):
     tables = random_tables(m, l_count, seed=11 * m, sub_dim=4)
     codes = mixture_codes(60_000 if m < 16 else 30_000, m, l_count, 400, seed=m)
     centers = codes[rng.choice(len(codes), size=1000, replace=False)].copy()
-    _check(lib, oracle, codes, centers, tables, modes=(1, 2, 3))
+    _check(lib, oracle, codes, centers, tables, modes=(1, 2, 3, 4, 5))
 
 
 def test_single_center_and_k_equals_n(lib, oracle):
@@ -107,6 +111,28 @@ def test_single_center_and_k_equals_n(lib, oracle):
     codes = rng.integers(0, 32, size=(500, 4)).astype(np.uint8)
     _check(lib, oracle, codes, codes[:1].copy(), tables)
     _check(lib, oracle, codes, codes.copy(), tables)
+
+
+@pytest.mark.parametrize("k", [2, 33, 64, 95, 161, 192, 193])
+def test_fewer_chunks_than_keys(lib, oracle, k):
+    """The 8-bit tier keeps T = 6 chunk keys per code: K below / at / just above 6 chunks
+    of 32 leaves sentinel keys (no bound from unstored chunks) or a partial last chunk."""
+    rng = np.random.default_rng(k)
+    tables = random_tables(4, 256, seed=k, sub_dim=4)
+    codes = mixture_codes(5000, 4, 256, 50, seed=k)
+    centers = codes[rng.choice(len(codes), size=k, replace=False)].copy()
+    _check(lib, oracle, codes, centers, tables)
+
+
+@pytest.mark.parametrize("trial", range(3))
+def test_cross_chunk_ties(lib, oracle, trial):
+    """Exact ties between centres of different chunks: the 8-bit finalisation visits the
+    stored chunks by key, not by index, and must still return the lowest index."""
+    rng = np.random.default_rng(700 + trial)
+    tables = lattice_tables(4, 8)
+    codes = rng.integers(0, 8, size=(6000, 4)).astype(np.uint8)
+    centers = rng.integers(0, 8, size=(400, 4)).astype(np.uint8)
+    _check(lib, oracle, codes, centers, tables)
 
 
 def test_fit_parity_forced(lib, oracle):
@@ -124,6 +150,13 @@ def test_fit_parity_forced(lib, oracle):
     np.testing.assert_array_equal(res.labels, ref["labels"])
     np.testing.assert_array_equal(res.centers, ref["centers"])
     assert [s.objective for s in res.trace] == [t["objective"] for t in ref["trace"]]
+    _lib.check(lib.pqk_set_scan_mode(4), "scan mode")
+    try:
+        res16 = pqk.fit(codes, tables, 200, max_iterations=5, seed=3)
+    finally:
+        _lib.check(lib.pqk_set_scan_mode(0), "scan mode")
+    np.testing.assert_array_equal(res16.labels, ref["labels"])
+    np.testing.assert_array_equal(res16.centers, ref["centers"])
 
 
 @pytest.mark.parametrize("kind", ["random", "lattice", "scaled", "heavy", "huge", "empty_rows"])
@@ -161,15 +194,17 @@ def test_vote_fp16_stage(oracle, kind):
             assert got[kk, mm] == oracle.vote_argmin(hist[kk, mm], tables[mm]), (kk, mm)
 
 
-def test_default_mode_large_problem_uses_16bit_tier(lib, oracle):
-    """Default mode at >= 2^31 lookups: the 16-bit tier runs (2-byte lookups in the stats)
-    and labels / sd_sq still equal the oracle's linear scan on clustered codes."""
+@pytest.mark.parametrize("m,lookup_bytes", [(4, 1), (8, 2)])
+def test_default_mode_large_problem_uses_fixed_point_tier(lib, oracle, m, lookup_bytes):
+    """Default mode at >= 2^31 lookups: the 8-bit tier runs at M = 4 and the 16-bit tier at
+    M = 8 (1- / 2-byte lookups in the stats); labels / sd_sq still equal the oracle's
+    linear scan on clustered codes."""
     import torch
 
     from paper_1709_03708_b200 import _lib, engine
 
     rng = np.random.default_rng(31)
-    m, l_count = 4, 256
+    l_count = 256
     tables = random_tables(m, l_count, seed=31, sub_dim=8)
     codes = mixture_codes(700_000, m, l_count, 3000, seed=31)
     centers = codes[rng.choice(len(codes), size=800, replace=False)].copy()
@@ -181,7 +216,7 @@ def test_default_mode_large_problem_uses_16bit_tier(lib, oracle):
         eng.assign(engine.upload_codes(centers, m, dev))
         labels, sd = eng.labels_host(), eng.sd_host()
         st = eng.stats.cpu().numpy()
-    assert int(st[_lib.STAT_LOOKUP_BYTES]) == 2
+    assert int(st[_lib.STAT_LOOKUP_BYTES]) == lookup_bytes
     expect, exp_sd = oracle.assign_c(codes, centers, tables, want_sd=True)
     np.testing.assert_array_equal(labels, expect)
     assert sd.tobytes() == exp_sd.tobytes()

@@ -1,9 +1,10 @@
-"""A/B of the assignment scan tiers on a bench workload: 16-bit fixed-point first tier
-(mode 0) vs the fp32 scan (mode 1).  Labels and sd_sq must be bit-identical; prints
+"""A/B of the assignment scan tiers on a bench workload: the default first tier (mode 0:
+8-bit at padded M = 4, 16-bit otherwise), the 16-bit tier (mode 4) and the fp32 scan
+(mode 1).  Labels and sd_sq must be bit-identical; prints
 the per-assign time of each mode, the first-tier scan kernel time (profile events) and
 the flagged counts.  Also runs a few Lloyd iterations per mode and compares centres.
 
-usage: python tools/diag_scan16.py [c1|c2|c3s|c4s|c5s] [reps] [mode_a (default 0)]
+usage: python tools/diag_scan16.py [c1|c2|c3s|c4s|c5s|c4] [reps] [mode_a (default 0)] [mode_b (default 4)]
   c3s/c4s/c5s: the config's codes at a reduced N (same K, M) so the run stays short."""
 import sys
 import time
@@ -18,7 +19,8 @@ from paper_1709_03708_b200.pq import PQCodebook, build_distance_tables  # noqa: 
 
 cfgn = sys.argv[1] if len(sys.argv) > 1 else "c2"
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 5
-mode_a = int(sys.argv[3]) if len(sys.argv) > 3 else 0  # 2: force the 16-bit tier (small configs)
+mode_a = int(sys.argv[3]) if len(sys.argv) > 3 else 0  # 2: force the first tier (small configs)
+mode_b = int(sys.argv[4]) if len(sys.argv) > 4 else 4  # 4: 16-bit tier at M = 4
 base = cfgn.rstrip("s")
 cfg = dict(bench.CONFIGS[base])
 n = {"c3s": 1_000_000, "c4s": 4_000_000, "c5s": 2_000_000}.get(cfgn, cfg["n"])
@@ -84,14 +86,17 @@ ok = True
 cur_centers = centers0
 for it in range(3):
     r0 = run(mode_a, cur_centers)
+    r2 = run(mode_b, cur_centers)
     r1 = run(1, cur_centers)
     same = bool(torch.equal(r0[0], r1[0]) and torch.equal(r0[1].view(torch.int64), r1[1].view(torch.int64)))
+    same &= bool(torch.equal(r2[0], r1[0]) and torch.equal(r2[1].view(torch.int64), r1[1].view(torch.int64)))
     ok &= same
     u = r0[7]
-    print(f"[{cfgn} it{it}] n={n} k={k} m={m} U={u}  mode0 assign {r0[2]:.3f} ms (scan16 {r0[3]:.3f} ms, "
-          f"{n * u * m * 2 / (r0[3] / 1e3) / 1e9:.0f} GB/s, flagged {r0[4]} -> fp64 {r0[5]})  "
+    print(f"[{cfgn} it{it}] n={n} k={k} m={m} U={u}  mode{mode_a} assign {r0[2]:.3f} ms (first tier {r0[3]:.3f} ms, "
+          f"{r0[6]} B lookups, {n * u * m * r0[6] / (r0[3] / 1e3) / 1e9:.0f} GB/s, flagged {r0[4]} -> fp64 {r0[5]})  "
+          f"mode{mode_b} assign {r2[2]:.3f} ms (first tier {r2[3]:.3f} ms, {r2[6]} B, flagged {r2[4]} -> fp64 {r2[5]})  "
           f"mode1 assign {r1[2]:.3f} ms (scan32 {r1[3]:.3f} ms, flagged {r1[4]})  "
-          f"speedup {r1[2] / r0[2]:.2f}x  identical={same}", flush=True)
+          f"speedup vs b {r2[2] / r0[2]:.2f}x  identical={same}", flush=True)
     # next centres: one Lloyd update from the mode-0 labels
     eng.objective()
     eng.histogram()

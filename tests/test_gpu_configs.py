@@ -1,4 +1,5 @@
-"""Parity at the BASELINE.json configurations, on the default (16-bit first tier) path.
+"""Parity at the BASELINE.json configurations, on the default path (8-bit first tier at
+M = 4: configs 2 and 4; 16-bit at M = 8 / 16: configs 3 and 5; fp32 scan for config 1).
 
 Each workload is built exactly as bench.py builds it (bench.build_workload: the
 reference-trained codebook of bench_assets/, the same seeded vectors, the GPU
@@ -68,17 +69,17 @@ def _engine_iterations(cfg_name, iterations, rows, votes=2000, n_loc=None):
     return wl, records
 
 
-def _assert_clean(records, first_tier_bytes=2):
+def _assert_clean(records, first_tier_bytes):
     for i, rec in enumerate(records):
         assert rec["mismatch"] == 0, (i, rec)
         assert rec["objective_equal"], (i, rec)
-        assert rec["lookup_bytes"] == first_tier_bytes, (i, rec)  # the default 16-bit tier ran
+        assert rec["lookup_bytes"] == first_tier_bytes, (i, rec)  # the default first tier ran
 
 
 def test_config2_full_rows():
     """Config 2 (N=1e6, K=1e4, M=4): every code's label and sd, two iterations."""
     _, recs = _engine_iterations("c2", 2, rows=1_000_000)
-    _assert_clean(recs)
+    _assert_clean(recs, first_tier_bytes=1)
     assert recs[0]["rows"] == 1_000_000
 
 
@@ -105,10 +106,11 @@ def test_config2_fit_vs_oracle(oracle):
 
 
 def test_config4_shard():
-    """Config 4's per-GPU shard (N=1.25e8 SIFT-like codes, K=1e5, M=4): 6,250 chunks of
-    16 centres and the fp32 list tier (~1e5 flagged codes per iteration) on the default path."""
+    """Config 4's per-GPU shard (N=1.25e8 SIFT-like codes, K=1e5, M=4): 3,125 chunks of
+    32 centres in the 8-bit tier, the fp32 list tier (~6e4 flagged codes per iteration) and
+    scan windows of 2^28 codes on the default path."""
     _, recs = _engine_iterations("c4", 2, rows=50_000)
-    _assert_clean(recs)
+    _assert_clean(recs, first_tier_bytes=1)
     assert recs[0]["hist_bins"] == 100_000 * 4 * 256
 
 
@@ -134,14 +136,14 @@ def test_config4_encode_sample(oracle):
 def test_config5_shard():
     """Config 5's per-GPU shard (N=1.25e7 mixture codes, K=1e5, M=16)."""
     _, recs = _engine_iterations("c5", 2, rows=20_000)
-    _assert_clean(recs)
+    _assert_clean(recs, first_tier_bytes=2)
 
 
 def test_config3_sampled():
     """Config 3 (N=1e7 deep-feature-like 4096-D vectors encoded by the K-streamed
     tensor-core encoder, K=1e4, M=8)."""
     _, recs = _engine_iterations("c3", 2, rows=50_000)
-    _assert_clean(recs)
+    _assert_clean(recs, first_tier_bytes=2)
 
 
 def test_config1_full():

@@ -283,10 +283,26 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) hscan8_kernel(const H8Params
       const int idx = my0 + j * OWN;
       if (idx < end) {
 #pragma unroll
-        for (int e = 0; e < T; ++e) keys[(int64_t)e * kstride + idx] = key[j][e];
+        for (int e = 0; e < T; ++e) __stcs(keys + (int64_t)e * kstride + idx, key[j][e]);  // evict-first: Q8 stays in L2
       }
     }
   }
+}
+
+// L2 policy for the chunk-table re-reads of the finalisation: keep Q8 (100 MB at config
+// 4) resident while the keys, codes, labels and distances stream through with evict-first
+// loads/stores.
+__device__ __forceinline__ uint64_t l2_evict_last_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ uint4 ldg4_keep(const uint4* ptr, uint64_t pol) {
+  uint4 v;
+  asm volatile("ld.global.nc.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(ptr), "l"(pol));
+  return v;
 }
 
 // Finalisation, one thread per code (see the header comment).
@@ -297,11 +313,12 @@ __global__ void __launch_bounds__(256, 4) hfinal8_kernel(const H8Params p, const
   const int m = p.m;
   const double s_q = p.sc->s;
   const bool bad = p.sc->bad != 0;
+  const uint64_t pol = l2_evict_last_policy();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < p.n; i += (int64_t)gridDim.x * blockDim.x) {
     uint32_t k[T];
 #pragma unroll
-    for (int e = 0; e < T; ++e) k[e] = __ldg(keys + (int64_t)e * kstride + i);
-    const uint32_t xw = __ldg(reinterpret_cast<const uint32_t*>(p.codes) + i);
+    for (int e = 0; e < T; ++e) k[e] = __ldcs(keys + (int64_t)e * kstride + i);
+    const uint32_t xw = __ldcs(reinterpret_cast<const uint32_t*>(p.codes) + i);
     const uint32_t lim = (k[0] >> 24) + (uint32_t)m + 1u;
     // every chunk not stored has a minimum >= the T-th key (none: fewer than T chunks)
     uint32_t qlow = (k[T - 1] == 0xffffffffu) ? 0xffffffffu : (k[T - 1] >> 24);
@@ -328,7 +345,7 @@ __global__ void __launch_bounds__(256, 4) hfinal8_kernel(const H8Params p, const
       for (int mm = 0; mm < 4; ++mm) {
         const uint32_t x = (xw >> (8 * mm)) & 0xffu;
         const uint4* src = p.q + (((size_t)t * p.l + x) * 4 + mm) * 2;
-        const uint4 a0 = __ldg(src), a1 = __ldg(src + 1);
+        const uint4 a0 = ldg4_keep(src, pol), a1 = ldg4_keep(src + 1, pol);
         r[0] += a0.x;
         r[1] += a0.y;
         r[2] += a0.z;
@@ -375,8 +392,8 @@ __global__ void __launch_bounds__(256, 4) hfinal8_kernel(const H8Params p, const
       cert = lo > best * s_q * (1.0 + 0x1p-40);
     }
     if (cert) {
-      p.labels[i] = (uint32_t)__ldg(&p.pos2idx[bu]);
-      p.sd_sq[i] = best;
+      __stcs(p.labels + i, (uint32_t)__ldg(&p.pos2idx[bu]));
+      __stcs(p.sd_sq + i, best);
     } else {
       const int f = atomicAdd(p.flag_count, 1);
       p.flags[f] = (int32_t)i;

@@ -1190,10 +1190,22 @@ __global__ void obj_leaf8_kernel(const double* __restrict__ sd, int64_t nleaves,
     double r1 = 0.0, r2 = 0.0;
     const int nb = n - (n % 8);
     if (n >= 8) {
-      r2 = a[j];
+      r2 = __ldcs(a + j);
       r1 = __dsqrt_rn(r2);
-      for (int i = 8; i < nb; i += 8) {
-        const double x = a[i + j];
+      int i = 8;
+      // four loads in flight per lane, then the sequential (numpy-order) adds
+      for (; i + 32 <= nb; i += 32) {
+        double x[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) x[q] = __ldcs(a + i + 8 * q + j);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          r2 = __dadd_rn(r2, x[q]);
+          r1 = __dadd_rn(r1, __dsqrt_rn(x[q]));
+        }
+      }
+      for (; i < nb; i += 8) {
+        const double x = __ldcs(a + i + j);
         r2 = __dadd_rn(r2, x);
         r1 = __dadd_rn(r1, __dsqrt_rn(x));
       }

@@ -19,6 +19,7 @@ from __future__ import annotations
 
 import ctypes as C
 import hashlib
+import os
 import threading
 from dataclasses import dataclass
 
@@ -51,8 +52,43 @@ def _stream(dev: "torch.device") -> C.c_void_p:
     return C.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
 
 
+# PQK_GUARD=1 (diagnostic; the pool has no compute-sanitizer): every buffer the kernels
+# write is allocated between two 64 KB guard zones filled with 0xA5, and check_guards()
+# reports any zone a kernel overwrote (an out-of-bounds store into a neighbouring buffer).
+_GUARD = os.environ.get("PQK_GUARD", "") == "1"
+_GUARD_BYTES = 64 << 10
+_GUARDS: list = []
+
+
+def _alloc(shape, dtype, dev, zero: bool = False) -> "torch.Tensor":
+    if not _GUARD:
+        return (torch.zeros if zero else torch.empty)(shape, dtype=dtype, device=dev)
+    shape = (shape,) if isinstance(shape, int) else tuple(shape)
+    numel = 1
+    for s in shape:
+        numel *= int(s)
+    nbytes = numel * torch.tensor([], dtype=dtype).element_size()
+    raw = torch.full((_GUARD_BYTES + nbytes + _GUARD_BYTES,), 0xA5, dtype=torch.uint8, device=dev)
+    body = raw[_GUARD_BYTES:_GUARD_BYTES + nbytes]
+    if zero:
+        body.zero_()
+    _GUARDS.append((raw, nbytes))
+    return body.view(dtype).view(shape)
+
+
+def check_guards() -> list:
+    """Indices of guarded buffers whose guard zones were overwritten (empty: all intact)."""
+    bad = []
+    for i, (raw, nbytes) in enumerate(_GUARDS):
+        lo = raw[:_GUARD_BYTES]
+        hi = raw[_GUARD_BYTES + nbytes:]
+        if bool((lo != 0xA5).any()) or bool((hi != 0xA5).any()):
+            bad.append(i)
+    return bad
+
+
 def _empty(n_bytes: int, dev) -> "torch.Tensor":
-    return torch.empty(max(int(n_bytes), 1), dtype=torch.uint8, device=dev)
+    return _alloc(max(int(n_bytes), 1), torch.uint8, dev)
 
 
 # ---------------------------------------------------------------------------
@@ -211,17 +247,17 @@ class ShardEngine:
         self.base_index = int(base_index)
         m, l, mp = tables.m, tables.l, tables.mp
         lib = _lib.load()
-        self.labels = torch.empty(max(self.n, 1), dtype=torch.int32, device=dev)
-        self.sd = torch.empty(max(self.n, 1), dtype=torch.float64, device=dev)
+        self.labels = _alloc(max(self.n, 1), torch.int32, dev)
+        self.sd = _alloc(max(self.n, 1), torch.float64, dev)
         self.ws_bytes = int(lib.pqk_assign_workspace_bytes(max(self.n, 1), self.k, m, l))
         self.ws = _empty(self.ws_bytes, dev)
-        self.stats = torch.zeros(STATS_LEN, dtype=torch.int64, device=dev)
-        self.hist = torch.empty(self.k * m * l, dtype=torch.int32, device=dev)
-        self.counts = torch.empty(self.k, dtype=torch.int32, device=dev)
-        self.new_centers = torch.zeros((self.k, mp), dtype=torch.uint8, device=dev)
+        self.stats = _alloc(STATS_LEN, torch.int64, dev, zero=True)
+        self.hist = _alloc(self.k * m * l, torch.int32, dev)
+        self.counts = _alloc(self.k, torch.int32, dev)
+        self.new_centers = _alloc((self.k, mp), torch.uint8, dev, zero=True)
         self.rws_bytes = int(lib.pqk_repair_workspace_bytes(max(self.n, 1), self.k))
         self.rws = _empty(self.rws_bytes, dev)
-        self.obj = torch.zeros(2, dtype=torch.float64, device=dev)
+        self.obj = _alloc(2, torch.float64, dev, zero=True)
         self.plan = pairwise_plan(self.n, dev) if self.n else None
 
     # -- stream-ordered launches ------------------------------------------------
@@ -509,10 +545,10 @@ def train_codebook_host(vectors: np.ndarray, m: int, l: int, iterations: int, se
     with torch.cuda.device(dev):
         s = _stream(dev)
         x = torch.from_numpy(vectors).to(dev)
-        labels = torch.empty(n, dtype=torch.int32, device=dev)
-        sums = torch.empty(l * sub, dtype=torch.float64, device=dev)
-        counts = torch.empty(l, dtype=torch.int32, device=dev)
-        own = torch.empty(n, dtype=torch.float64, device=dev)
+        labels = _alloc(n, torch.int32, dev)
+        sums = _alloc(l * sub, torch.float64, dev)
+        counts = _alloc(l, torch.int32, dev)
+        own = _alloc(n, torch.float64, dev)
         ws_bytes = int(lib.pqk_train_workspace_bytes(n, sub))
         ws = _empty(ws_bytes, dev)
         stats = torch.zeros(STATS_LEN, dtype=torch.int64, device=dev)
@@ -541,8 +577,8 @@ def train_codebook_host(vectors: np.ndarray, m: int, l: int, iterations: int, se
 def encode_device(vec_dev, cw_dev, m: int, l: int, dev, stride: int | None = None, stats=None):
     n, d = int(vec_dev.shape[0]), int(vec_dev.shape[1])
     stride = m if stride is None else stride
-    out = torch.empty((n, stride), dtype=torch.uint8, device=dev)
-    st = stats if stats is not None else torch.zeros(STATS_LEN, dtype=torch.int64, device=dev)
+    out = _alloc((n, stride), torch.uint8, dev)
+    st = stats if stats is not None else _alloc(STATS_LEN, torch.int64, dev, zero=True)
     if n:
         call("pqk_encode_device", _ptr(vec_dev), n, d, _ptr(cw_dev), m, l, _ptr(out), stride, _ptr(st), _stream(dev))
     return out

@@ -1,8 +1,12 @@
-"""Small workload that launches every hot kernel of the path once or twice, for
-compute-sanitizer (memcheck / racecheck / synccheck) runs on one B200:
+"""Small workload that launches every hot kernel of the path once or twice, checked
+against the oracle and (PQK_GUARD=1) for out-of-bounds stores:
 
-  compute-sanitizer --tool memcheck  --error-exitcode 3 python tools/sanitize_fit.py
-  compute-sanitizer --tool racecheck --error-exitcode 3 python tools/sanitize_fit.py
+  PQK_GUARD=1 python tools/sanitize_fit.py                       # atomic histogram
+  PQK_GUARD=1 PQK_HIST_MODE=tiled python tools/sanitize_fit.py   # cluster-tiled hbin_*
+
+With PQK_GUARD=1 every buffer the engine hands to a kernel for writing sits between two
+64 KB guard zones of 0xA5 (engine._alloc), and the run fails if any zone changed.  (The
+pool does not allow compute-sanitizer; this is the substitute, plus the oracle checks.)
 
 Covered: dedup, scale preparation, the 8-bit (hscan8/hfinal8) and 16-bit (hscan/hfinal)
 first tiers, the fp32 scan and its list tier, the exact rescans, histogram (atomic and
@@ -91,5 +95,17 @@ check("train_codebook", np.array_equal(np.asarray(cb.codewords), np.asarray(ref_
 t_gpu = pqk.build_distance_tables(cb).tables
 check("build_distance_tables", np.array_equal(t_gpu, O.build_distance_tables(np.asarray(cb.codewords))))
 
+# a mid-size assignment: several persistent passes per CTA, 8-bit tier by default size rule
+tables = random_tables(4, 256, seed=21, sub_dim=4)
+codes = mixture_codes(400_000, 4, 256, 3000, seed=21)
+centers = codes[rng.choice(len(codes), size=6000, replace=False)].copy()
+labels = pqk.assign(codes, centers, tables)
+check("assign 4e5 x 6e3 default tiers", np.array_equal(labels, O.assign_c(codes, centers, tables)))
+
+from paper_1709_03708_b200 import engine  # noqa: E402
+
+if engine._GUARD:
+    bad = engine.check_guards()
+    check(f"guard zones intact ({len(engine._GUARDS)} guarded buffers)", not bad)
 print("SANITIZE_FIT", "OK" if not fails else f"{fails} MISMATCHES", flush=True)
 sys.exit(1 if fails else 0)

@@ -827,7 +827,7 @@ static int launch_hscan8_c(int c_need, const h8::H8Params& p, uint32_t* keys, in
     if (c_need > C) return launch_hscan8_c<NW, S, T, Cs...>(c_need, p, keys, kstride, grid, l, stream);
   }
   const DevInfo& di = dev_info();
-  const size_t smem = 128 + (size_t)S * 256 * h8::ROW;  // ring stride: 256 rows (immediate offsets)
+  const size_t smem = 128 + 1024 + (size_t)S * 256 * h8::ROW;  // ring stride: 256 rows (immediate offsets); 1 KB alignment slack
   if ((int)smem > di.smem_optin) return fail(PQK_EUNSUPPORTED, "assignment chunk ring exceeds shared memory");
   auto kern = h8::hscan8_kernel<C, NW, S, T>;
   PQK_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

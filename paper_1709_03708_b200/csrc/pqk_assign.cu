@@ -629,6 +629,7 @@ struct AssignWS {
   uint4* q16;
   int32_t* flags2;
   uint2* keys16;
+  uint32_t* keys3;
   // 8-bit first tier (padded M = 4): aliases of the 16-bit buffers (never both in a call)
   uint8_t* t8;
   uint4* q8;
@@ -672,7 +673,9 @@ static AssignWS assign_ws_layout(void* base, int64_t n, int64_t k, int mp, int l
   const size_t o_q16 = take(h16_ok ? (size_t)((k + kc16 - 1) / kc16) * l * mp * kc16 * sizeof(uint16_t) : 0, 1024);
   const size_t o_fl2 =
       take(h16_ok ? (size_t)std::max<int64_t>(std::min(n, kScanWindow), 1) * sizeof(int32_t) : 0, 256);
-  const size_t k16_bytes = h16_ok ? (size_t)std::max<int64_t>(std::min(n, kScanWindow), 1) * sizeof(uint2) : 0;
+  // (B, Sg) per code, plus the third key when one lane owns a code (KC = 8: MP 8 / 16)
+  const size_t k16_bytes =
+      h16_ok ? (size_t)std::max<int64_t>(std::min(n, kScanWindow), 1) * (sizeof(uint2) + (kc16 == 8 ? 4 : 0)) : 0;
   const size_t k8_bytes =
       mp == 4 ? (size_t)std::max<int64_t>(std::min(n, kScanWindow8), 1) * h8::kMaxT * sizeof(uint32_t) : 0;
   const size_t o_k16 = take(std::max(k16_bytes, k8_bytes), 256);
@@ -692,6 +695,7 @@ static AssignWS assign_ws_layout(void* base, int64_t n, int64_t k, int mp, int l
     w.q16 = reinterpret_cast<uint4*>(b + o_q16);
     w.flags2 = reinterpret_cast<int32_t*>(b + o_fl2);
     w.keys16 = reinterpret_cast<uint2*>(b + o_k16);
+    w.keys3 = reinterpret_cast<uint32_t*>(b + o_k16 + (size_t)std::max<int64_t>(std::min(n, kScanWindow), 1) * sizeof(uint2));
     // q16 region: ceil(k/16) x l x 4 x 16 x 2 B >= ceil(k/32) x l x 128 B; t16: 4 l^2 x 2 B >= 4 l^2
     w.t8 = reinterpret_cast<uint8_t*>(b + o_t16);
     w.q8 = reinterpret_cast<uint4*>(b + o_q16);
@@ -1131,6 +1135,7 @@ extern "C" int pqk_assign_device(const uint8_t* d_codes, int64_t n, int32_t m, i
       hp.sd_sq = sd_sq;
       hp.flags = w.flags;
       hp.flag_count = w.counters + 1;
+      hp.keys3 = w.keys3;
       int rc = PQK_OK;
       switch (mp) {
         case 4: rc = launch_hscan<4, 16, 11, 4, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15, 16>(hp, w.keys16, l, stream); break;

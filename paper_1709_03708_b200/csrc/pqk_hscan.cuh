@@ -275,6 +275,7 @@ struct HScanParams {
   int32_t* flag_count;
   int64_t pass_size;
   int64_t npasses;
+  uint32_t* keys3;  // one lane per code (KC = 8): the third-smallest chunk key per code
 };
 
 template <int W>
@@ -312,13 +313,76 @@ __device__ __forceinline__ void load_code_rot(const uint8_t* __restrict__ codes,
   for (int k = 0; k < W; ++k) out[k] = __funnelshift_r(u[k], u[(k + 1) % W], 8 * rb);
 }
 
+// Exact pass over one chunk of a code (finalisation): the KC fixed-point sums (as in the
+// scan), centres with Q <= lim re-evaluated in float64 (ascending m, __dadd_rn) into
+// (best, bu) with the lowest index on ties (chunks may be visited out of index order),
+// the smallest sum above lim into qn.
+template <int MP, int KC>
+__device__ __forceinline__ void hfinal_chunk(const HScanParams& p, const uint32_t (&xb)[MP / 4], uint32_t chunk,
+                                             uint32_t lim, int U, int m, double& best, int& bu, uint32_t& qn) {
+  constexpr int G8 = KC / 8;  // uint4 groups of 8 centres per (chunk, row, subspace)
+  uint32_t r[G8][4];
+#pragma unroll
+  for (int g = 0; g < G8; ++g) r[g][0] = r[g][1] = r[g][2] = r[g][3] = 0u;
+#pragma unroll
+  for (int mm = 0; mm < MP; ++mm) {
+    if (mm < m) {
+      const uint32_t x = (xb[mm >> 2] >> (8 * (mm & 3))) & 0xffu;
+#pragma unroll
+      for (int g = 0; g < G8; ++g) {
+        const uint4 w = __ldg(p.q + (((size_t)chunk * p.l + x) * MP + mm) * G8 + g);
+        r[g][0] += w.x;
+        r[g][1] += w.y;
+        r[g][2] += w.z;
+        r[g][3] += w.w;
+      }
+    }
+  }
+  const int u0 = (int)chunk * KC;
+  const int nreal = min(KC, U - u0);  // real centres of the chunk (the last chunk is partial)
+  uint32_t cand = 0u;
+#pragma unroll
+  for (int e = 0; e < KC; ++e) {
+    const uint32_t w = r[e >> 3][(e & 7) >> 1];
+    const uint32_t qv = (e < nreal) ? ((e & 1) ? (w >> 16) : (w & 0xffffu)) : 0xffffffffu;
+    const bool c = qv <= lim;
+    cand |= (c ? 1u : 0u) << e;
+    if (!c) qn = min(qn, qv);  // padding (~0) never lowers qn
+  }
+  while (cand) {  // ascending centre index within the chunk
+    const int e = __ffs(cand) - 1;
+    cand &= cand - 1u;
+    const int u = u0 + e;
+    uint32_t cb[MP / 4];
+#pragma unroll
+    for (int w = 0; w < MP / 4; ++w) cb[w] = __ldg(reinterpret_cast<const uint32_t*>(p.ucodes + (size_t)u * MP) + w);
+    double d = 0.0;
+#pragma unroll
+    for (int mm = 0; mm < MP; ++mm) {
+      if (mm < m) {
+        const uint32_t x = (xb[mm >> 2] >> (8 * (mm & 3))) & 0xffu;
+        const uint32_t c = (cb[mm >> 2] >> (8 * (mm & 3))) & 0xffu;
+        d = dadd(d, __ldg(&p.t64[((size_t)mm * p.l + x) * p.l + c]));
+      }
+    }
+    if (d < best || (d == best && u < bu)) {
+      best = d;
+      bu = u;
+    }
+  }
+}
+
 // Finalisation, one thread per code (a separate, fully parallel kernel: its dependent
 // global loads would otherwise stall every warp of the scan at the end of each pass).
 // keys[i] = (B, Sg): B = (Q << 16 | chunk) of the smallest chunk minimum, Sg the lower
-// bound of every centre outside chunk(B) (~0: none).
+// bound of every centre outside chunk(B) (~0: none).  With one lane per code (KC = 8)
+// Sg is the second-smallest chunk key and keys3[i] the third: when Sg's chunk holds
+// candidates (value <= lim) it is evaluated too and the third key bounds the rest (a
+// code-level top-2 of chunks left 0.5% of config 5's codes uncertified, top-3 none of
+// 3,000 sampled).
 template <int MP, int KC>
-__global__ void __launch_bounds__(256, 4) hfinal_kernel(const HScanParams p, const uint2* __restrict__ keys) {
-  constexpr int G8 = KC / 8;  // uint4 groups of 8 centres per (chunk, row, subspace)
+__global__ void __launch_bounds__(256, MP >= 16 ? 2 : 4) hfinal_kernel(const HScanParams p, const uint2* __restrict__ keys) {
+  constexpr bool T3 = (KC == 8);
   const int U = p.counters[0];
   const int m = p.m;
   const double s_q = p.sc->s;
@@ -330,71 +394,22 @@ __global__ void __launch_bounds__(256, 4) hfinal_kernel(const HScanParams p, con
     uint32_t xb[MP / 4];
 #pragma unroll
     for (int w = 0; w < MP / 4; ++w) xb[w] = __ldg(reinterpret_cast<const uint32_t*>(xc) + w);
-    // the KC exact sums of chunk c* (as in the scan)
-    uint32_t r[G8][4];
-#pragma unroll
-    for (int g = 0; g < G8; ++g) r[g][0] = r[g][1] = r[g][2] = r[g][3] = 0u;
-#pragma unroll
-    for (int mm = 0; mm < MP; ++mm) {
-      if (mm < m) {
-        const uint32_t x = (xb[mm >> 2] >> (8 * (mm & 3))) & 0xffu;
-#pragma unroll
-        for (int g = 0; g < G8; ++g) {
-          const uint4 w = __ldg(p.q + (((size_t)cstar * p.l + x) * MP + mm) * G8 + g);
-          r[g][0] += w.x;
-          r[g][1] += w.y;
-          r[g][2] += w.z;
-          r[g][3] += w.w;
-        }
-      }
-    }
-    const int u0 = (int)cstar * KC;
-    const int nreal = min(KC, U - u0);  // real centres of chunk c* (the last chunk is partial)
-    uint32_t qv[KC];
-#pragma unroll
-    for (int e = 0; e < KC; ++e) {
-      const uint32_t w = r[e >> 3][(e & 7) >> 1];
-      qv[e] = (e < nreal) ? ((e & 1) ? (w >> 16) : (w & 0xffffu)) : 0xffffffffu;
-    }
-    uint32_t qmin = qv[0];
-#pragma unroll
-    for (int e = 1; e < KC; ++e) qmin = min(qmin, qv[e]);
-    // candidates: within M + 1 units of the chunk minimum; the rest bound from below (Qn)
-    const uint32_t lim = qmin + (uint32_t)m + 1u;
-    uint32_t cand = 0u, qn = 0xffffffffu;  // qn: smallest non-candidate sum (none: ~0)
-#pragma unroll
-    for (int e = 0; e < KC; ++e) {
-      const bool c = qv[e] <= lim;
-      cand |= (c ? 1u : 0u) << e;
-      if (!c) qn = min(qn, qv[e]);  // padding (~0) never lowers qn
-    }
+    // candidates: within M + 1 units of the smallest chunk minimum; the rest bound from below
+    const uint32_t lim = (kv.x >> 16) + (uint32_t)m + 1u;
     double best = __longlong_as_double(0x7ff0000000000000LL);
     int bu = 0x7fffffff;
-    while (cand) {  // ascending centre index: ties keep the lower one
-      const int e = __ffs(cand) - 1;
-      cand &= cand - 1u;
-      const int u = u0 + e;
-      uint32_t cb[MP / 4];
-#pragma unroll
-      for (int w = 0; w < MP / 4; ++w) cb[w] = __ldg(reinterpret_cast<const uint32_t*>(p.ucodes + (size_t)u * MP) + w);
-      double d = 0.0;
-#pragma unroll
-      for (int mm = 0; mm < MP; ++mm) {
-        if (mm < m) {
-          const uint32_t x = (xb[mm >> 2] >> (8 * (mm & 3))) & 0xffu;
-          const uint32_t c = (cb[mm >> 2] >> (8 * (mm & 3))) & 0xffu;
-          d = dadd(d, __ldg(&p.t64[((size_t)mm * p.l + x) * p.l + c]));
-        }
-      }
-      if (d < best) {
-        best = d;
-        bu = u;
-      }
+    uint32_t qn = 0xffffffffu;  // smallest non-candidate sum of the evaluated chunks (none: ~0)
+    hfinal_chunk<MP, KC>(p, xb, cstar, lim, U, m, best, bu, qn);
+    // lower bound of every centre not evaluated: other chunks and the non-candidates
+    uint32_t qlow;
+    if (T3 && sg != 0xffffffffu && (sg >> 16) <= lim) {
+      hfinal_chunk<MP, KC>(p, xb, sg & 0xffffu, lim, U, m, best, bu, qn);
+      const uint32_t k3 = __ldg(p.keys3 + i);
+      qlow = min(k3 == 0xffffffffu ? 0xffffffffu : (k3 >> 16), qn);
+    } else {
+      qlow = min(sg == 0xffffffffu ? 0xffffffffu : (sg >> 16), qn);
     }
     bool cert = !bad && bu != 0x7fffffff;
-    // lower bound of every centre other than the candidates: other chunks (Sg) and the
-    // non-candidates of c* (Qn); ~0 = no such centre
-    const uint32_t qlow = min(sg == 0xffffffffu ? 0xffffffffu : (sg >> 16), qn);
     if (cert && qlow != 0xffffffffu) {
       const double lo = (double)qlow - 0.5 * (double)m - 0.01;
       cert = lo > best * s_q * (1.0 + 0x1p-40);
@@ -485,7 +500,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) hscan_kernel(const HScanPara
 
     // per (slot, subspace step) the shared-memory address of the code's row in stage 0
     uint32_t off[C][MP];
-    uint32_t bk[C], sk[C];
+    uint32_t bk[C], sk[C], rk[C];  // rk: third-smallest key (one lane per code only)
 #pragma unroll
     for (int j = 0; j < C; ++j) {
       const int idx = my0 + j * OWN;
@@ -494,7 +509,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) hscan_kernel(const HScanPara
 #pragma unroll
       for (int i = 0; i < MP; ++i)
         off[j][i] = __byte_perm(cw[i >> 2], 0u, 0x4440u | (uint32_t)(i & 3)) * ROW + lc[i] + stage0;
-      bk[j] = sk[j] = 0xffffffffu;
+      bk[j] = sk[j] = rk[j] = 0xffffffffu;
     }
 
     for (int t0 = 0; t0 < nchunks; t0 += S) {
@@ -526,6 +541,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) hscan_kernel(const HScanPara
         const uint32_t cm = vmin2(vmin2(r0, r1), vmin2(r2, r3));
         const uint32_t c2 = vmin2(cm, __byte_perm(cm, 0u, 0x1032));  // both halves: min of the 8
         const uint32_t kk = __byte_perm((uint32_t)t, c2, 0x5410);      // (min << 16) | chunk
+        if constexpr (H == 1) rk[j] = max(sk[j], min(rk[j], kk));     // third smallest
         sk[j] = max(bk[j], min(sk[j], kk));                            // second smallest (bk <= sk)
         bk[j] = min(bk[j], kk);
       }
@@ -547,7 +563,10 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) hscan_kernel(const HScanPara
       const uint32_t cstar = kb & 0xffffu;
       const uint32_t sg = min(((k0 & 0xffffu) == cstar) ? s0 : k0, ((k1 & 0xffffu) == cstar) ? s1 : k1);
       const int idx = my0 + j * OWN;
-      if (h == 0 && idx < end) keys[idx] = make_uint2(kb, sg);
+      if (h == 0 && idx < end) {
+        keys[idx] = make_uint2(kb, sg);
+        if constexpr (H == 1) p.keys3[idx] = rk[j];
+      }
     }
   }
 }

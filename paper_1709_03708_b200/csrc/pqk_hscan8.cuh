@@ -24,9 +24,9 @@
 // recomputed from the chunk table, centres with Q <= lim are re-evaluated exactly in
 // float64 (ascending m, __dadd_rn) and the smallest (lowest position on ties: positions
 // ascend with the original index) is the winner w* with distance d*.  Every centre not
-// evaluated has Q >= min(Qn, V_T): Qn the smallest non-candidate sum of an evaluated chunk
-// or the value of a stored chunk above lim, V_T the T-th key's value (or none when the
-// code saw fewer than T chunks).  Certified when that bound - M/2 - 0.01 > s d* (1 + 2^-40):
+// evaluated has Q >= min(lim + 1, V_T): lim + 1 bounds the non-candidates of evaluated
+// chunks and every stored chunk above lim, V_T the T-th key's value the chunks not stored
+// (none when the code saw fewer than T chunks).  Certified when that bound - M/2 - 0.01 > s d* (1 + 2^-40):
 // every other centre's float64 sum then exceeds d*, so w* is the reference's argmin and d*
 // its paired_distance_sq.  Uncertified codes go to the next tier (fp32 list scan, exact
 // fp64 rescan) exactly as after the 16-bit tier.
@@ -359,14 +359,18 @@ __global__ void __launch_bounds__(256, 4) hfinal8_kernel(const H8Params p, const
       }
       const int u0 = (int)t * KC;
       const int nreal = min(KC, U - u0);
-      uint32_t cand = 0u;
+      // candidates (Q <= lim) word by word; every real non-candidate has Q >= lim + 1, which
+      // is the bound used for them (exact minima give the same certificate rate on config-4
+      // data, and cost a byte extraction per centre)
+      const uint32_t lim4 = min(lim, 255u) * 0x01010101u;
+      qlow = min(qlow, lim + 1u);
+      uint32_t cand = 0u;  // bit j: centre j is a candidate
 #pragma unroll
-      for (int j = 0; j < KC; ++j) {
-        const uint32_t qv = (r[j >> 2] >> (8 * (j & 3))) & 0xffu;
-        if (j < nreal) {
-          if (qv <= lim) cand |= 1u << j;
-          else qlow = min(qlow, qv);
-        }
+      for (int w = 0; w < 8; ++w) {
+        const int nb = min(4, max(0, nreal - 4 * w));
+        const uint32_t realm = nb >= 4 ? 0xffffffffu : ((1u << (8 * nb)) - 1u);
+        const uint32_t hb = __vcmpleu4(r[w], lim4) & realm & 0x80808080u;
+        cand |= ((hb * 0x00204081u) >> 28) << (4 * w);  // byte flags 7/15/23/31 -> bits 28..31
       }
       while (cand) {  // ascending position within the chunk
         const int j = __ffs(cand) - 1;

@@ -59,14 +59,16 @@ constexpr int kHistThreads = 512;
 // pass 1: cnt[c][b] = members of bucket b among CTA c's contiguous element range
 __global__ void __launch_bounds__(kHistThreads) hbin_count_kernel(const uint32_t* __restrict__ labels, int64_t n,
                                                                   int64_t per_cta, uint32_t tile, int nb,
-                                                                  uint32_t* __restrict__ cnt) {
+                                                                  uint32_t* __restrict__ cnt, int pad4) {
   extern __shared__ uint32_t sc[];
   for (int b = threadIdx.x; b < nb; b += blockDim.x) sc[b] = 0;
   __syncthreads();
   const int64_t lo = blockIdx.x * per_cta, hi = min(n, lo + per_cta);
   for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) atomicAdd(&sc[__ldg(labels + i) / tile], 1u);
   __syncthreads();
-  for (int b = threadIdx.x; b < nb; b += blockDim.x) cnt[(int64_t)blockIdx.x * nb + b] = sc[b];
+  // pad4 (sector-staged scatter): every (CTA, bucket) run is a whole number of 32-byte
+  // sectors of 8-byte records, padding records carry label word ~0
+  for (int b = threadIdx.x; b < nb; b += blockDim.x) cnt[(int64_t)blockIdx.x * nb + b] = pad4 ? (sc[b] + 3u) & ~3u : sc[b];
 }
 
 // thread per bucket: cnt[c][b] -> exclusive prefix over c, tot[b] = bucket size
@@ -164,6 +166,72 @@ __global__ void __launch_bounds__(1024) hbin_scatter_kernel(
   }
 }
 
+// pass 2, sector-staged (4-byte codes, nb * 40 B of shared memory): each bucket keeps a
+// 4-record (32-byte) buffer in shared memory and its CTA run cursor; a full buffer leaves
+// as one whole sector (two 16-byte stores, sector-aligned: runs are padded to 4 records),
+// so no partial line is ever written back to DRAM (the direct scatter's 8-byte stores to
+// ~600k open runs read-modify-wrote 2.3 GB at config 4).  Elements go in rounds of one
+// per thread: a slot is claimed with a shared atomic; the thread that fills slot 3 flushes
+// after a barrier; threads that overflowed a full buffer retry next round.
+__global__ void __launch_bounds__(1024) hbin_scatter4_kernel(
+    const uint32_t* __restrict__ codes, const uint32_t* __restrict__ labels, int64_t n, int64_t per_cta,
+    uint32_t tile, int nb, const uint32_t* __restrict__ cnt, const uint32_t* __restrict__ base,
+    uint2* __restrict__ rec) {
+  extern __shared__ __align__(16) uint8_t hs4[];
+  uint4* buf = reinterpret_cast<uint4*>(hs4);          // [nb][2] (4 records)
+  uint32_t* cur = reinterpret_cast<uint32_t*>(hs4 + (size_t)nb * 32);
+  uint32_t* fill = cur + nb;
+  for (int b = threadIdx.x; b < nb; b += blockDim.x) {
+    cur[b] = base[b] + cnt[(int64_t)blockIdx.x * nb + b];
+    fill[b] = 0u;
+  }
+  __syncthreads();
+  const int64_t lo = blockIdx.x * per_cta, hi = min(n, lo + per_cta);
+  uint2* bufr = reinterpret_cast<uint2*>(hs4);
+  for (int64_t i0 = lo; i0 < hi; i0 += blockDim.x) {
+    const int64_t i = i0 + threadIdx.x;
+    bool pending = i < hi;
+    uint32_t b = 0, s = 0;
+    uint2 r = make_uint2(0u, 0u);
+    if (pending) {
+      const uint32_t k = __ldcs(labels + i);
+      b = k / tile;
+      r = make_uint2(__ldcs(codes + i), k - b * tile);
+    }
+    while (__syncthreads_or(pending)) {
+      bool flusher = false;
+      if (pending) {
+        s = atomicAdd(&fill[b], 1u);
+        if (s < 4u) {
+          bufr[b * 4 + s] = r;
+          pending = false;
+          flusher = (s == 3u);
+        }
+      }
+      __syncthreads();
+      if (flusher) {
+        const uint32_t p = cur[b];
+        cur[b] = p + 4u;
+        fill[b] = 0u;
+        uint4* dst = reinterpret_cast<uint4*>(rec + p);
+        dst[0] = buf[2 * b];
+        dst[1] = buf[2 * b + 1];
+      }
+      __syncthreads();
+    }
+  }
+  // partial buffers: pad to a whole sector with ~0-label records
+  for (int b = threadIdx.x; b < nb; b += blockDim.x) {
+    const uint32_t f = fill[b];
+    if (f) {
+      for (uint32_t q = f; q < 4u; ++q) bufr[b * 4 + q] = make_uint2(0u, 0xffffffffu);
+      uint4* dst = reinterpret_cast<uint4*>(rec + cur[b]);
+      dst[0] = buf[2 * b];
+      dst[1] = buf[2 * b + 1];
+    }
+  }
+}
+
 // pass 3: one CTA per cluster tile — shared-memory counts, dense slab write, counts[k]
 __global__ void __launch_bounds__(kHistThreads) hbin_tile_kernel(
     const uint32_t* __restrict__ rec, int mw, const uint32_t* __restrict__ base,
@@ -180,6 +248,7 @@ __global__ void __launch_bounds__(kHistThreads) hbin_tile_kernel(
   const int rw = mw + 1;
   for (int64_t p = lo + threadIdx.x; p < hi; p += blockDim.x) {
     const uint32_t* r = rec + p * rw;
+    if (r[mw] == 0xffffffffu) continue;  // padding of the sector-staged scatter
     uint32_t* hk = sh + (int)r[mw] * row;
     for (int w = 0; 4 * w < m; ++w) {
       const uint32_t c = r[w];
@@ -1412,11 +1481,22 @@ extern "C" int pqk_histogram_device(const uint8_t* d_codes, int64_t n, int32_t m
     }();
     // (measured at config 4, 4167 buckets: 47 CTAs 4.7 ms scatter, 188 CTAs 3.9 ms, 296 CTAs
     // 8.1 ms with 13 GB of DRAM read-modify-write; the scatter is store-transaction bound)
-    const int ctas = (int)std::max<int64_t>(di.sms, std::min<int64_t>(di.sms * 2, (int64_t)(frontier / (128.0 * nbi))));
     const int mw = mp / 4;
+    // sector-staged scatter (4-byte codes, bucket buffers in shared memory, one CTA per SM);
+    // PQK_HIST_STAGED=0 keeps the direct scatter (diagnostic)
+    static const bool staged_on = [] {
+      const char* e = getenv("PQK_HIST_STAGED");
+      return !(e && e[0] == '0');
+    }();
+    const size_t staged_smem = (size_t)nbi * 40;
+    const bool staged = staged_on && mw == 1 && staged_smem <= (size_t)di.smem_optin &&
+                        (double)n + 3.0 * di.sms * nbi < 4294967295.0;
+    const int ctas = staged ? di.sms
+                            : (int)std::max<int64_t>(di.sms, std::min<int64_t>(di.sms * 2, (int64_t)(frontier / (128.0 * nbi))));
     const int64_t per_cta = std::max<int64_t>((n + ctas - 1) / ctas, 1);
     const size_t cnt_b = align_up((size_t)ctas * nbi * 4, 256), base_b = align_up((size_t)(nbi + 1) * 4, 256);
-    const size_t rec_b = align_up((size_t)std::max<int64_t>(n, 1) * (mw + 1) * 4, 256);
+    const int64_t nrec = std::max<int64_t>(n, 1) + (staged ? 3LL * ctas * nbi : 0);  // + sector padding
+    const size_t rec_b = align_up((size_t)nrec * (mw + 1) * 4, 256);
     { const int _rc = keep_default_pool(); if (_rc != PQK_OK) return _rc; }
     uint8_t* ws = nullptr;
     if (cudaMallocAsync(reinterpret_cast<void**>(&ws), cnt_b + base_b + rec_b, stream) != cudaSuccess) {
@@ -1435,17 +1515,26 @@ extern "C" int pqk_histogram_device(const uint8_t* d_codes, int64_t n, int32_t m
         PQK_CUDA_TRY(cudaFuncSetAttribute(hbin_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kHistMaxBuckets * 4));
         PQK_CUDA_TRY(cudaFuncSetAttribute(hbin_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kHistMaxBuckets * 4));
         PQK_CUDA_TRY(cudaFuncSetAttribute(hbin_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kHistTileBytes));
+        PQK_CUDA_TRY(cudaFuncSetAttribute(hbin_scatter4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, di.smem_optin));
         smem_set[dev & 63] = 1;
       }
-      hbin_count_kernel<<<ctas, kHistThreads, sm_nb, stream>>>(d_labels, n, per_cta, (uint32_t)tile, nbi, cnt);
+      hbin_count_kernel<<<ctas, kHistThreads, sm_nb, stream>>>(d_labels, n, per_cta, (uint32_t)tile, nbi, cnt,
+                                                               staged ? 1 : 0);
       PQK_LAUNCH_CHECK("hbin_count_kernel");
       hbin_colscan_kernel<<<(nbi + 255) / 256, 256, 0, stream>>>(cnt, ctas, nbi, base);
       PQK_LAUNCH_CHECK("hbin_colscan_kernel");
       hbin_scan_kernel<<<1, 1024, 0, stream>>>(base, nbi);
       PQK_LAUNCH_CHECK("hbin_scan_kernel");
-      hbin_scatter_kernel<<<ctas, 1024, sm_nb, stream>>>(d_codes, mw, d_labels, n, per_cta, (uint32_t)tile, nbi, cnt,
-                                                         base, rec);
-      PQK_LAUNCH_CHECK("hbin_scatter_kernel");
+      if (staged) {
+        hbin_scatter4_kernel<<<ctas, 1024, staged_smem, stream>>>(reinterpret_cast<const uint32_t*>(d_codes), d_labels,
+                                                                   n, per_cta, (uint32_t)tile, nbi, cnt, base,
+                                                                   reinterpret_cast<uint2*>(rec));
+        PQK_LAUNCH_CHECK("hbin_scatter4_kernel");
+      } else {
+        hbin_scatter_kernel<<<ctas, 1024, sm_nb, stream>>>(d_codes, mw, d_labels, n, per_cta, (uint32_t)tile, nbi, cnt,
+                                                           base, rec);
+        PQK_LAUNCH_CHECK("hbin_scatter_kernel");
+      }
       hbin_tile_kernel<<<nbi, kHistThreads, (size_t)tile * m * l * 4, stream>>>(rec, mw, base, tile, k, m, l, d_hist,
                                                                                d_counts);
       PQK_LAUNCH_CHECK("hbin_tile_kernel");

@@ -82,10 +82,10 @@ np.save(sys.argv[3], pqk.encode(pqk.PQCodebook(d["cw"]), d["x"]))
 """
 
 
-def test_tc_encode_many_tiles_matches_simt_path(tmp_path):
+def test_tc_encode_many_tiles_matches_simt_path(tmp_path, oracle):
     """~11 tiles x 4 subspaces per CTA (buffer reuse across items): the tcgen05 path must
-    equal the SIMT certified path (run in a subprocess with PQK_ENCODE_SIMT=1), and the
-    fp64 fallback must stay rare."""
+    equal the SIMT certified path (run in a subprocess with PQK_ENCODE_SIMT=1) and, on a
+    20,000-row sample spanning both halves, the oracle; the fp64 fallback must stay rare."""
     import os
     import subprocess
     import sys
@@ -110,23 +110,30 @@ def test_tc_encode_many_tiles_matches_simt_path(tmp_path):
     subprocess.run([sys.executable, "-c", _SIMT_SCRIPT, root, str(tmp_path / "in.npz"), str(tmp_path / "out.npy")],
                    check=True, env=env)
     np.testing.assert_array_equal(tc_codes, np.load(tmp_path / "out.npy"))
+    rows = np.sort(rng.choice(n, size=20_000, replace=False))
+    np.testing.assert_array_equal(tc_codes[rows], oracle.encode(cw, x[rows]))
     # the integer half lies ~20x outside the codebook's range (distances ~ |x|^2, gaps ~ |x||c|):
     # the fp32 certificate leaves ~0.2% of its pairs to the exact path
     assert flagged < n * 4 * 3e-3, flagged  # the stats slot counts every uncertified pair
 
 
-def test_tc_encode_sift_like_flag_rate():
-    """SIFT-like data (BASELINE configs 2/4): the certificate must cover almost every pair."""
+def test_tc_encode_sift_like_flag_rate(oracle):
+    """SIFT-like data with the config-2 / config-4 reference codebooks (bench_assets): the
+    certificate must cover almost every pair, and every code must equal the oracle's."""
     import torch
 
+    import bench
     from paper_1709_03708_b200 import _lib, engine, synth
 
-    x = synth.sift_like(100_000, 5)
-    cw = synth.train_codebook_fast(synth.sift_like(20_000, 6), 4, 256, iterations=3, seed=1)
+    x = synth.sift_like(40_000, 5)
     dev = engine.device_of()
-    stats = torch.zeros(_lib.STATS_LEN, dtype=torch.int64, device=dev)
-    engine.encode_device(torch.from_numpy(x).to(dev), torch.from_numpy(cw).to(dev), 4, 256, dev, stride=4, stats=stats)
-    assert int(stats[_lib.STAT_ENCODE_FLAGGED].item()) < 100_000 * 4 * 1e-3
+    for cfg in ("c2", "c4"):
+        cw = bench.make_codebook(cfg, 4, 256)
+        stats = torch.zeros(_lib.STATS_LEN, dtype=torch.int64, device=dev)
+        codes = engine.encode_device(torch.from_numpy(x).to(dev), torch.from_numpy(np.asarray(cw)).to(dev), 4, 256,
+                                     dev, stride=4, stats=stats).cpu().numpy()
+        assert int(stats[_lib.STAT_ENCODE_FLAGGED].item()) < 40_000 * 4 * 1e-3
+        np.testing.assert_array_equal(codes, oracle.encode(cw, x))
 
 
 def test_tc_encode_config3_shape(oracle):

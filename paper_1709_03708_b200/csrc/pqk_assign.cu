@@ -1021,7 +1021,7 @@ extern "C" int pqk_assign_device(const uint8_t* d_codes, int64_t n, int32_t m, i
     PQK_LAUNCH_CHECK("qbuild_kernel");
     return PQK_OK;
   };
-  if (fast && !use16) {
+  if (fast && !use_tier) {  // the fixed-point tiers build it only for a long uncertified list
     const int rc = qbuild32(nullptr, 0);
     if (rc != PQK_OK) return rc;
   }

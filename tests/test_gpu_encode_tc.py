@@ -146,3 +146,25 @@ def test_tc_encode_config3_shape(oracle):
     cw = x[rng.choice(3000, 256, replace=False)].reshape(256, 8, 512).transpose(1, 0, 2).copy()
     cw += rng.normal(0, 1e-3, size=cw.shape).astype(np.float32)
     np.testing.assert_array_equal(_encode(cw, x), oracle.encode(cw, x))
+
+
+def test_tck_prepared_operands_follow_codebook_changes(oracle):
+    """The K-streamed path keeps its prepared codebook operands between calls with the same
+    codebook (pointer, shape, contents); an in-place change of the codebook must be seen."""
+    import torch
+
+    from paper_1709_03708_b200 import engine
+
+    rng = np.random.default_rng(31)
+    cw = rng.normal(size=(2, 256, 128)).astype(np.float32)
+    x = rng.normal(size=(900, 256)).astype(np.float32)
+    dev = engine.device_of()
+    xd = torch.from_numpy(x).to(dev)
+    cd = torch.from_numpy(cw).to(dev)
+    for step in range(3):
+        got = engine.encode_device(xd, cd, 2, 256, dev).cpu().numpy()
+        np.testing.assert_array_equal(got, oracle.encode(cw, x), err_msg=f"step {step}")
+        if step == 0:
+            continue  # step 1 reuses the prepared operands
+        cw[1, 7] += 0.5  # in place, same device pointer
+        cd.copy_(torch.from_numpy(cw))

@@ -7,6 +7,8 @@
 // architectural ceiling is 128 B/clk/SM.  The loads are volatile (never hoisted or
 // merged), the loaded words are folded into one register per thread and written out
 // once so nothing is dead code.  Returns bytes/s measured with CUDA events on `stream`.
+#include <algorithm>
+
 #include "pqk_common.cuh"
 
 namespace pqk {
@@ -57,13 +59,18 @@ extern "C" int pqk_smem_probe(int32_t device, int32_t iters, double* bytes_per_s
   // warm-up launch (clocks ramp, module load), then the timed one
   smem_probe_kernel<<<sms, kProbeThreads, kProbeSmemBytes, s>>>(std::max(1, iters / 8), sink);
   PQK_LAUNCH_CHECK("smem_probe_kernel");
-  PQK_CUDA_TRY(cudaEventRecord(e0, s));
-  smem_probe_kernel<<<sms, kProbeThreads, kProbeSmemBytes, s>>>(iters, sink);
-  PQK_LAUNCH_CHECK("smem_probe_kernel");
-  PQK_CUDA_TRY(cudaEventRecord(e1, s));
-  PQK_CUDA_TRY(cudaEventSynchronize(e1));
+  // best of three timed launches (the peak is an upper bound: take the fastest)
   float ms = 0.f;
-  PQK_CUDA_TRY(cudaEventElapsedTime(&ms, e0, e1));
+  for (int rep = 0; rep < 3; ++rep) {
+    PQK_CUDA_TRY(cudaEventRecord(e0, s));
+    smem_probe_kernel<<<sms, kProbeThreads, kProbeSmemBytes, s>>>(iters, sink);
+    PQK_LAUNCH_CHECK("smem_probe_kernel");
+    PQK_CUDA_TRY(cudaEventRecord(e1, s));
+    PQK_CUDA_TRY(cudaEventSynchronize(e1));
+    float t = 0.f;
+    PQK_CUDA_TRY(cudaEventElapsedTime(&t, e0, e1));
+    ms = rep == 0 ? t : std::min(ms, t);
+  }
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   PQK_CUDA_TRY(cudaFreeAsync(sink, s));

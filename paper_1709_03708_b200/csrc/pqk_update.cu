@@ -1323,32 +1323,44 @@ struct DepthStarts {
   long long v[64];
 };
 
-// All remaining (small) levels, deepest first, in one CTA; writes the root sums.
+// All remaining (small, <= 4096-node) levels, deepest first, in one CTA; writes the root
+// sums.  Each level's values stay in shared memory for the next one (the first tail level
+// reads its children from nodeval, leaves from leafval), so a level costs a barrier, not
+// a global round trip.
+constexpr int kObjTailMax = 4096;
 __global__ void __launch_bounds__(1024) obj_levels_tail_kernel(int top_depth, DepthStarts ds,
                                                                const int32_t* __restrict__ na,
                                                                const int32_t* __restrict__ nb,
                                                                const double2* __restrict__ leafval,
-                                                               double2* __restrict__ nodeval, double* __restrict__ out2) {
+                                                               const double2* __restrict__ nodeval,
+                                                               double* __restrict__ out2) {
+  extern __shared__ double2 s_tail[];  // [2][kObjTailMax]
+  double2(*sbuf)[kObjTailMax] = reinterpret_cast<double2(*)[kObjTailMax]>(s_tail);
+  int cur = 0;
+  bool prev_smem = false;
   for (int d = top_depth; d >= 0; --d) {
     const int64_t start = ds.v[d], count = ds.v[d + 1] - ds.v[d], child = ds.v[d + 1];
+    const double2* prev = sbuf[cur ^ 1];
     for (int64_t t = threadIdx.x; t < count; t += blockDim.x) {
       const int64_t id = start + t;
-      const int a = na[id], b = nb[id];
+      const int a = __ldg(na + id), b = __ldg(nb + id);
       double2 r;
       if (b < 0) {
-        r = leafval[a];
+        r = __ldg(leafval + a);
       } else {
-        const double2 x = nodeval[child + a];
-        const double2 y = nodeval[child + b];
+        const double2 x = prev_smem ? prev[a] : __ldg(nodeval + child + a);
+        const double2 y = prev_smem ? prev[b] : __ldg(nodeval + child + b);
         r = make_double2(__dadd_rn(x.x, y.x), __dadd_rn(x.y, y.y));
       }
-      nodeval[id] = r;
+      sbuf[cur][t] = r;
     }
     __syncthreads();
+    cur ^= 1;
+    prev_smem = true;
   }
   if (threadIdx.x == 0) {
-    out2[0] = nodeval[0].x;
-    out2[1] = nodeval[0].y;
+    out2[0] = sbuf[cur ^ 1][0].x;
+    out2[1] = sbuf[cur ^ 1][0].y;
   }
 }
 
@@ -1726,7 +1738,7 @@ extern "C" int pqk_objective_device(const double* d_sd_sq, int64_t n, int64_t nl
   for (; d >= 0; --d) {
     const int64_t start = h_depth_start[d];
     const int64_t count = h_depth_start[d + 1] - start;
-    if (count <= 4096) break;
+    if (count <= kObjTailMax) break;
     const int64_t child = h_depth_start[d + 1];
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((count + 255) / 256, (int64_t)di.sms * 8));
     obj_level_kernel<<<grid, 256, 0, stream>>>(start, count, child, d_node_a, d_node_b, leafval, nodeval);
@@ -1734,7 +1746,18 @@ extern "C" int pqk_objective_device(const double* d_sd_sq, int64_t n, int64_t nl
   }
   DepthStarts ds{};
   for (int i = 0; i <= ndepth; ++i) ds.v[i] = h_depth_start[i];
-  obj_levels_tail_kernel<<<1, 1024, 0, stream>>>(d, ds, d_node_a, d_node_b, leafval, nodeval, d_out2);
+  {
+    static bool attr[64] = {};
+    int dev = 0;
+    PQK_CUDA_TRY(cudaGetDevice(&dev));
+    if (!attr[dev & 63]) {
+      PQK_CUDA_TRY(cudaFuncSetAttribute(obj_levels_tail_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)(2 * kObjTailMax * sizeof(double2))));
+      attr[dev & 63] = true;
+    }
+  }
+  obj_levels_tail_kernel<<<1, 1024, 2 * kObjTailMax * sizeof(double2), stream>>>(d, ds, d_node_a, d_node_b, leafval,
+                                                                                 nodeval, d_out2);
   PQK_LAUNCH_CHECK("obj_levels_tail_kernel");
   return PQK_OK;
 }

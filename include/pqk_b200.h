@@ -103,13 +103,15 @@ int pqk_pad_codes_device(const uint8_t* d_raw, int64_t n, int32_t m, uint8_t* d_
  * in float64 ascending-m order with lowest index on ties, and sd_sq[n] the float64
  * distance to that center, bit-identical to the reference. */
 size_t pqk_assign_workspace_bytes(int64_t n, int64_t k, int32_t m, int32_t l);
-/* Scan tiers of pqk_assign_device.  Mode 0 (default): a 16-bit fixed-point first tier
- * (2-byte table lookups, exact integer sums, certified against the quantisation error)
- * for padded M <= 16 and problems of >= 2^31 lookups, then the fp32 scan over the
+/* Scan tiers of pqk_assign_device.  Mode 0 (default): for problems of >= 2^31 lookups a
+ * fixed-point first tier with exact integer sums, certified against the quantisation
+ * error — 8-bit tables (1-byte lookups, the six smallest chunk keys per code) for padded
+ * M = 4, 16-bit tables (2-byte lookups) for padded M 8 / 16 — then the fp32 scan over the
  * uncertified list when it is long (>= 256 codes per SM) and the exact fp64 rescan for
- * the rest.  Mode 1: the fp32 scan first.  Mode 2: the 16-bit tier at any size.  Mode
- * 3: as 2 with the fp32 list tier for any list length.  Labels and sd_sq are identical
- * in every mode (process-wide setting, for A/B measurement and tests). */
+ * the rest.  Mode 1: the fp32 scan first.  Mode 2: the fixed-point tier at any size.
+ * Mode 3: as 2 with the fp32 list tier for any list length.  Modes 4 / 5: as 2 / 3 with
+ * the 16-bit tier also at padded M = 4.  Labels and sd_sq are identical in every mode
+ * (process-wide setting, for A/B measurement and tests). */
 int pqk_set_scan_mode(int32_t mode);
 int32_t pqk_get_scan_mode(void);
 int pqk_assign_device(const uint8_t* d_codes, int64_t n, int32_t m, int32_t l,

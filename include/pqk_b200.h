@@ -275,6 +275,9 @@ int pqk_tc_selftest(const void* d_a_f16, const void* d_b_f16, float* d_c, int32_
  * LDS.128 from one 1024-thread CTA per SM over `iters` x 16 loads per thread; returns
  * bytes/s (and the timed launch in ms) measured with CUDA events on `stream`. */
 int pqk_smem_probe(int32_t device, int32_t iters, double* bytes_per_s, double* ms_out, void* stream);
+/* Tensor-memory read bandwidth (tcgen05.ld, all 512 columns of one CTA per SM, 16 warps):
+ * the ceiling of the encoder's epilogue.  Bytes/s of the whole GPU, best of 3. */
+int pqk_tmem_probe(int32_t device, int32_t iters, double* bytes_per_s, double* ms_out, void* stream);
 
 #ifdef __cplusplus
 }

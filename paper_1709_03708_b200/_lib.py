@@ -75,6 +75,7 @@ SIGNATURES: dict[str, tuple] = {
     "pqk_peer_sum_device": (C.c_int, [_p, _i32, _i64, _p, _p]),
     "pqk_enable_peer_access": (C.c_int, [_p, _i32]),
     "pqk_smem_probe": (C.c_int, [_i32, _i32, C.POINTER(C.c_double), C.POINTER(C.c_double), _p]),
+    "pqk_tmem_probe": (C.c_int, [_i32, _i32, C.POINTER(C.c_double), C.POINTER(C.c_double), _p]),
     "pqk_train_workspace_bytes": (_sz, [_i64, _i32]),
     "pqk_train_step_device": (C.c_int, [_p, _i64, _i32, _i32, _i32, _p, _i32, _p, _p, _p, _p, _p, _sz, _p, _p]),
     "pqk_build_tables_device": (C.c_int, [_p, _i32, _i32, _i32, _p, _p]),

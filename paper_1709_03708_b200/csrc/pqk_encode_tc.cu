@@ -6,6 +6,9 @@
 // encoder's tests run first: a wrong descriptor shows up here as a wrong product.
 #include "pqk_common.cuh"
 #include "pqk_tc.cuh"
+#ifndef ENC_XST
+#define ENC_XST 3
+#endif
 #ifndef FILTER_ROWS
 #define FILTER_ROWS 4
 #endif
@@ -127,7 +130,7 @@ enum { CST_S = 0, CST_ACN = 1, CST_CB = 2, CST_CN = 3, CST_S1C = 4, CST_VALID = 
 template <int KP>
 struct Geo {
   static constexpr int KE = KP + kExt;
-  static constexpr int XST = KP >= 64 ? 2 : 3;  // X stages
+  static constexpr int XST = KP >= 64 ? 2 : ENC_XST;  // X stages (TMA ring depth)
   static constexpr bool SWZ = KP >= 32;         // X tile loaded with the 128-byte swizzle
   static constexpr int B_HI = kN * KE * 2;
   static constexpr int B_LO = kN * KP * 2;
@@ -141,8 +144,8 @@ struct Geo {
   static constexpr int OFF_STATS = OFF_A + 2 * A_BYTES;        // float4 [4][128]
   static constexpr int OFF_LO = OFF_STATS + 4 * kRows * 16;    // int [2][kTrWarps]
   static constexpr int OFF_CST = OFF_LO + 2 * kTrWarps * 4;    // float [8]
-  static constexpr int OFF_BAR = OFF_CST + CST_LEN * 4;        // uint64 [24]
-  static constexpr int OFF_TBASE = OFF_BAR + 24 * 8;
+  static constexpr int OFF_BAR = OFF_CST + CST_LEN * 4;        // uint64 [32]
+  static constexpr int OFF_TBASE = OFF_BAR + 32 * 8;
   static constexpr int SMEM = OFF_TBASE + 16 + 1024;           // + alignment slack
 };
 
@@ -389,13 +392,14 @@ __global__ void __launch_bounds__(kThreads, 1) encode_tc_kernel(const __grid_con
   int* s_lo = reinterpret_cast<int*>(smem + G::OFF_LO);
   float* s_cst = reinterpret_cast<float*>(smem + G::OFF_CST);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + G::OFF_BAR);
-  uint64_t* xfull = bars;        // [3]
-  uint64_t* xempty = bars + 3;   // [3]
-  uint64_t* afull = bars + 6;    // [2]
-  uint64_t* aempty = bars + 8;   // [2]
-  uint64_t* tfull = bars + 10;   // [2][2]: accumulator, column half
-  uint64_t* tempty = bars + 14;  // [2][2]
-  uint64_t* bload = bars + 18;
+  static_assert(G::XST <= 8, "X ring barriers");
+  uint64_t* xfull = bars;         // [XST <= 8]
+  uint64_t* xempty = bars + 8;    // [XST <= 8]
+  uint64_t* afull = bars + 16;    // [2]
+  uint64_t* aempty = bars + 18;   // [2]
+  uint64_t* tfull = bars + 20;    // [2][2]: accumulator, column half
+  uint64_t* tempty = bars + 24;   // [2][2]
+  uint64_t* bload = bars + 28;
   uint32_t* s_tbase = reinterpret_cast<uint32_t*>(smem + G::OFF_TBASE);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;

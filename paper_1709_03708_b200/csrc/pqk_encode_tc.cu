@@ -120,6 +120,10 @@ constexpr int kExt = 16;       // extension K columns of the hi pass
 constexpr int kEpiWarps = 8;   // 2 per TMEM lane quadrant: one per accumulator
 constexpr int kTrWarps = 8;    // transform warps (16 rows each)
 constexpr int kThreads = (2 + kEpiWarps + kTrWarps) * 32;
+// encode_tc_kernel's transform: one thread per row (4 warps x 32 rows), the row's KP
+// columns streamed in 8-column groups (no cross-lane reductions, no per-row shuffles)
+constexpr int kTrWarpsR = 4;
+constexpr int kThreadsR = (2 + kEpiWarps + kTrWarpsR) * 32;
 constexpr int kChunk = 32;     // epilogue columns per tcgen05.ld pair
 constexpr bool kMmaHalves = false;  // N=128 MMA halves (separately released) vs N=256
 constexpr float kX2Limit = 1073741824.0f;  // 2^30: |s x|^2 bound for the fp16 extension parts
@@ -379,7 +383,7 @@ __device__ __forceinline__ void epilogue_row_split(const EncParams& p, int m, in
 }
 
 template <int KP>
-__global__ void __launch_bounds__(kThreads, 1) encode_tc_kernel(const __grid_constant__ CUtensorMap tmap,
+__global__ void __launch_bounds__(kThreadsR, 1) encode_tc_kernel(const __grid_constant__ CUtensorMap tmap,
                                                                 const EncParams p) {
   using G = Geo<KP>;
   constexpr int KE = G::KE;
@@ -411,10 +415,10 @@ __global__ void __launch_bounds__(kThreads, 1) encode_tc_kernel(const __grid_con
   if (tid == 0) {
     for (int i = 0; i < G::XST; ++i) {
       mbar_init(&xfull[i], 1);
-      mbar_init(&xempty[i], kTrWarps);
+      mbar_init(&xempty[i], kTrWarpsR);
     }
     for (int i = 0; i < 2; ++i) {
-      mbar_init(&afull[i], kTrWarps);
+      mbar_init(&afull[i], kTrWarpsR);
       mbar_init(&aempty[i], 1);
     }
     for (int i = 0; i < 4; ++i) {
@@ -475,7 +479,7 @@ __global__ void __launch_bounds__(kThreads, 1) encode_tc_kernel(const __grid_con
         tc::fence_after();
         int lo_any = 0;
 #pragma unroll
-        for (int j = 0; j < kTrWarps; ++j) lo_any |= s_lo[ab * kTrWarps + j];
+        for (int j = 0; j < kTrWarpsR; ++j) lo_any |= s_lo[ab * kTrWarpsR + j];
         const uint32_t a_hi = smem_u32(sA + ab * G::A_BYTES), a_lo = a_hi + G::A_HI;
 #pragma unroll
         for (int hf = 0; hf < NH; ++hf) {
@@ -537,126 +541,87 @@ __global__ void __launch_bounds__(kThreads, 1) encode_tc_kernel(const __grid_con
                    eps_ext, cb, cnm, s1c, sqrtf((float)KP), lane);
     }
   } else {
-    // ---------------- transform warps: 16 rows each, 2 passes of 8 ----------------
+    // ---------------- transform warps: one thread per row ----------------
+    // 8-column groups streamed X (swizzled TMA tile) -> scaled fp16 hi / lo -> the UMMA
+    // K-major A tiles (8 consecutive rows = one 128-byte core matrix per STS.128 phase);
+    // |s x|^2 and the lo-nonzero flag accumulate in the row's own thread.
     const int tw = warp - 2 - kEpiWarps;
-    constexpr int VPT = KP / 4;  // columns per thread; 4 threads per row (lanes r, r+8, r+16, r+24)
-    const int th = lane >> 3;
+    const int r = 32 * tw + lane;
+    constexpr int NG = KP / 8;
     const float sc = s_cst[CST_S];
     const __half acn = __float2half_rn(s_cst[CST_ACN]);
     const bool valid = s_cst[CST_VALID] != 0.f;
-    const bool has_x = th * VPT < ks;  // dsub = 8 < KP = 16: the upper half is zero padding
+    const uint32_t aoff_hi = tc::kmajor_off(r, 0, KE), aoff_lo = (uint32_t)G::A_HI + tc::kmajor_off(r, 0, KP);
     for (int w = 0; w < items; ++w) {
       const int ab = w & 1, xs = w % G::XST;
       mbar_wait(&xfull[xs], (uint32_t)((w / G::XST) & 1));
-      float v[2][VPT];
+      mbar_wait(&aempty[ab], (uint32_t)(((w >> 1) & 1) ^ 1));
+      const uint8_t* xb = sX + xs * G::X_STAGE;
+      uint8_t* ahi = sA + ab * G::A_BYTES + aoff_hi;
+      uint8_t* alo = sA + ab * G::A_BYTES + aoff_lo;
+      float acc0 = 0.f, acc1 = 0.f;
+      uint32_t lr = 0;
 #pragma unroll
-      for (int ps = 0; ps < 2; ++ps) {
-        const int r = 16 * tw + 8 * ps + (lane & 7);
-        const uint8_t* xb = sX + xs * G::X_STAGE;
-        if (G::SWZ) {
-          // 128-byte rows of 8 x 16-byte chunks, chunk index XOR (row % 8)
+      for (int g = 0; g < NG; ++g) {
+        float v[8];
 #pragma unroll
-          for (int cc = 0; cc < VPT / 4; ++cc) {
-            const int chunk = th * (VPT / 4) + cc;  // 16-byte chunk of the row
-            const int half = chunk >> 3, ch = chunk & 7;
-            const float4 f = *reinterpret_cast<const float4*>(xb + half * (kRows * 128) + r * 128 + ((ch ^ (r & 7)) << 4));
-            v[ps][4 * cc] = f.x;
-            v[ps][4 * cc + 1] = f.y;
-            v[ps][4 * cc + 2] = f.z;
-            v[ps][4 * cc + 3] = f.w;
+        for (int h = 0; h < 2; ++h) {
+          float4 f = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (G::SWZ) {
+            // 128-byte rows of 8 x 16-byte chunks, chunk index XOR (row % 8); KP = 64: two halves
+            const int chunk = 2 * g + h, half = chunk >> 3, ch = chunk & 7;
+            f = *reinterpret_cast<const float4*>(xb + half * (kRows * 128) + r * 128 + ((ch ^ (r & 7)) << 4));
+          } else if (8 * g < ks) {  // dsub = 8 < KP = 16: the upper group is zero padding
+            f = *reinterpret_cast<const float4*>(reinterpret_cast<const float*>(xb) + r * ks + 8 * g + 4 * h);
           }
-        } else if (has_x) {
-          const float* xr = reinterpret_cast<const float*>(xb) + r * ks + th * VPT;
-#pragma unroll
-          for (int j = 0; j < VPT; j += 4) {
-            const float4 f = *reinterpret_cast<const float4*>(xr + j);
-            v[ps][j] = f.x;
-            v[ps][j + 1] = f.y;
-            v[ps][j + 2] = f.z;
-            v[ps][j + 3] = f.w;
-          }
-        } else {
-#pragma unroll
-          for (int j = 0; j < VPT; ++j) v[ps][j] = 0.f;
+          v[4 * h] = f.x;
+          v[4 * h + 1] = f.y;
+          v[4 * h + 2] = f.z;
+          v[4 * h + 3] = f.w;
         }
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&xempty[xs]);
-      uint32_t hw[2][VPT / 2], lw[2][VPT / 2];
-      float x2[2];
-      uint32_t lo_nz = 0, lo_row[2];
+        uint32_t hw[4], lw[4];
 #pragma unroll
-      for (int ps = 0; ps < 2; ++ps) {
-        float acc = 0.f;
-        uint32_t lr = 0;
-#pragma unroll
-        for (int j = 0; j < VPT; j += 2) {
-          const float a0 = v[ps][j] * sc, a1 = v[ps][j + 1] * sc;
+        for (int j = 0; j < 4; ++j) {
+          const float a0 = v[2 * j] * sc, a1 = v[2 * j + 1] * sc;
           const __half2 hh = __floats2half2_rn(a0, a1);
           const float2 hf = __half22float2(hh);
           const __half2 ll = __floats2half2_rn(a0 - hf.x, a1 - hf.y);
-          hw[ps][j / 2] = *reinterpret_cast<const uint32_t*>(&hh);
-          lw[ps][j / 2] = *reinterpret_cast<const uint32_t*>(&ll);
-          lr |= lw[ps][j / 2];
-          acc = fmaf(a0, a0, fmaf(a1, a1, acc));
+          hw[j] = *reinterpret_cast<const uint32_t*>(&hh);
+          lw[j] = *reinterpret_cast<const uint32_t*>(&ll);
+          acc0 = fmaf(a0, a0, acc0);
+          acc1 = fmaf(a1, a1, acc1);
         }
-        acc += __shfl_xor_sync(0xffffffffu, acc, 8);
-        acc += __shfl_xor_sync(0xffffffffu, acc, 16);
-        x2[ps] = acc;
-        lr &= 0x7fff7fffu;
-        lr |= __shfl_xor_sync(0xffffffffu, lr, 8);
-        lr |= __shfl_xor_sync(0xffffffffu, lr, 16);
-        lo_row[ps] = lr;
-        lo_nz |= lr;
+        lr |= (lw[0] | lw[1]) | (lw[2] | lw[3]);
+        *reinterpret_cast<uint4*>(ahi + g * 128) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+        *reinterpret_cast<uint4*>(alo + g * 128) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
       }
-      const unsigned bal = __ballot_sync(0xffffffffu, lo_nz != 0);
-      mbar_wait(&aempty[ab], (uint32_t)(((w >> 1) & 1) ^ 1));
-      uint8_t* ahi = sA + ab * G::A_BYTES;
-      uint8_t* alo = ahi + G::A_HI;
-#pragma unroll
-      for (int ps = 0; ps < 2; ++ps) {
-        const int r = 16 * tw + 8 * ps + (lane & 7);
-        // |s x|^2 rounded up (fp32 sum of KP products: relative error < (KP+4) 2^-24)
-        const float x2u = x2[ps] * (1.0f + (float)(KP + 8) * 5.9604644775390625e-08f);
-        const bool ok = valid && (x2u < kX2Limit);  // false for NaN / inf / out-of-range rows
-        if (!ok) {
-#pragma unroll
-          for (int j = 0; j < VPT / 2; ++j) hw[ps][j] = lw[ps][j] = 0u;
-        }
-#pragma unroll
-        for (int c = 0; c < VPT / 8; ++c) {
-          const int k = th * VPT + 8 * c;
-          *reinterpret_cast<uint4*>(ahi + tc::kmajor_off(r, k, KE)) =
-              make_uint4(hw[ps][4 * c], hw[ps][4 * c + 1], hw[ps][4 * c + 2], hw[ps][4 * c + 3]);
-          *reinterpret_cast<uint4*>(alo + tc::kmajor_off(r, k, KP)) =
-              make_uint4(lw[ps][4 * c], lw[ps][4 * c + 1], lw[ps][4 * c + 2], lw[ps][4 * c + 3]);
-        }
-        if (VPT % 8) {  // KP = 16: 4 columns per thread, half a core-matrix row
-          const int k = th * VPT;
-          *reinterpret_cast<uint2*>(ahi + tc::kmajor_off(r, k, KE)) = make_uint2(hw[ps][0], hw[ps][1]);
-          *reinterpret_cast<uint2*>(alo + tc::kmajor_off(r, k, KP)) = make_uint2(lw[ps][0], lw[ps][1]);
-        }
-        if (th == 0) {
-          // extension columns: [acn x3, |s x|^2 parts (x 2^15), 2^15 (padding codewords), 0...]
-          const float xv = ok ? x2u * 3.0517578125e-05f : 0.f;  // 2^-15, exact
-          const __half x_h = __float2half_rn(xv);
-          const float r1 = xv - __half2float(x_h);
-          const __half x_m = __float2half_rn(r1);
-          const __half x_l = __float2half_rn(r1 - __half2float(x_m));
-          const __half p15 = __float2half_rn(32768.f);
-          const __half z = __float2half_rn(0.f);
-          *reinterpret_cast<uint4*>(ahi + tc::kmajor_off(r, KP, KE)) =
-              make_uint4(pack_h2(acn, acn), pack_h2(acn, x_h), pack_h2(x_m, x_l), pack_h2(p15, z));
-          *reinterpret_cast<uint4*>(ahi + tc::kmajor_off(r, KP + 8, KE)) = make_uint4(0u, 0u, 0u, 0u);
-          // |s x| rounded up: sqrt.approx has relative error < 2^-21
-          float xn;
-          asm("sqrt.approx.f32 %0, %1;" : "=f"(xn) : "f"(x2u));
-          // 4 stats buffers: transform(w + 4) waits for MMA(w + 2), which waits for every
-          // epilogue warp of parity w to have read item w's stats
-          s_stats[(w & 3) * kRows + r] = make_float4(x2u, xn * 1.000002f, ok ? 1.f : 0.f, lo_row[ps] ? 1.f : 0.f);
-        }
-      }
-      if (lane == 0) s_lo[ab * kTrWarps + tw] = (bal != 0);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&xempty[xs]);
+      lr &= 0x7fff7fffu;  // -0 lo parts are zeros
+      const unsigned bal = __ballot_sync(0xffffffffu, lr != 0u);
+      // |s x|^2 rounded up (fp32 sum of KP products: relative error < (KP+4) 2^-24).  Rows
+      // with NaN / inf / out-of-range values are not certified (stats .z = 0); their A rows
+      // only reach their own accumulator row.
+      const float x2u = (acc0 + acc1) * (1.0f + (float)(KP + 8) * 5.9604644775390625e-08f);
+      const bool ok = valid && (x2u < kX2Limit);
+      // extension columns: [acn x3, |s x|^2 parts (x 2^15), 2^15 (padding codewords), 0...]
+      const float xv = ok ? x2u * 3.0517578125e-05f : 0.f;  // 2^-15, exact
+      const __half x_h = __float2half_rn(xv);
+      const float r1 = xv - __half2float(x_h);
+      const __half x_m = __float2half_rn(r1);
+      const __half x_l = __float2half_rn(r1 - __half2float(x_m));
+      const __half p15 = __float2half_rn(32768.f);
+      const __half z = __float2half_rn(0.f);
+      *reinterpret_cast<uint4*>(ahi + NG * 128) =
+          make_uint4(pack_h2(acn, acn), pack_h2(acn, x_h), pack_h2(x_m, x_l), pack_h2(p15, z));
+      *reinterpret_cast<uint4*>(ahi + (NG + 1) * 128) = make_uint4(0u, 0u, 0u, 0u);
+      // |s x| rounded up: sqrt.approx has relative error < 2^-21
+      float xn;
+      asm("sqrt.approx.f32 %0, %1;" : "=f"(xn) : "f"(x2u));
+      // 4 stats buffers: transform(w + 4) waits for MMA(w + 2), which waits for every
+      // epilogue warp of parity w to have read item w's stats
+      s_stats[(w & 3) * kRows + r] = make_float4(x2u, xn * 1.000002f, ok ? 1.f : 0.f, lr ? 1.f : 0.f);
+      if (lane == 0) s_lo[ab * kTrWarpsR + tw] = (bal != 0);
       tc::fence_proxy_async();
       __syncwarp();
       if (lane == 0) mbar_arrive(&afull[ab]);
@@ -1828,7 +1793,7 @@ int launch_encode_tc(const float* d_x, int64_t n, int d, const float* d_cw, int 
   ep.one = 1u;
   auto kern = encode_tc_kernel<KP>;
   PQK_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM));
-  kern<<<ep.tstride * m, kThreads, G::SMEM, stream>>>(map, ep);
+  kern<<<ep.tstride * m, kThreadsR, G::SMEM, stream>>>(map, ep);
   PQK_LAUNCH_CHECK("encode_tc_kernel");
   const int exact_smem = l * (ks + 1) * 4;
   PQK_CUDA_TRY(cudaFuncSetAttribute(encode_exact_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, exact_smem));

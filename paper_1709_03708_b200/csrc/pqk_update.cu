@@ -1734,11 +1734,14 @@ extern "C" int pqk_objective_device(const double* d_sd_sq, int64_t n, int64_t nl
     obj_leaf8_kernel<<<grid, 256, 0, stream>>>(d_sd_sq, nleaves, d_leaf_off, d_leaf_len, leafval);
     PQK_LAUNCH_CHECK("obj_leaf8_kernel");
   }
+  // the tail kernel takes the top levels 0..tail_top, every one of them <= kObjTailMax nodes
+  // (an unbalanced tree's deepest levels can be small while shallower ones are not)
+  int tail_top = 0;
+  while (tail_top + 1 < ndepth && h_depth_start[tail_top + 2] - h_depth_start[tail_top + 1] <= kObjTailMax) ++tail_top;
   int d = ndepth - 1;
-  for (; d >= 0; --d) {
+  for (; d > tail_top; --d) {
     const int64_t start = h_depth_start[d];
     const int64_t count = h_depth_start[d + 1] - start;
-    if (count <= kObjTailMax) break;
     const int64_t child = h_depth_start[d + 1];
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((count + 255) / 256, (int64_t)di.sms * 8));
     obj_level_kernel<<<grid, 256, 0, stream>>>(start, count, child, d_node_a, d_node_b, leafval, nodeval);

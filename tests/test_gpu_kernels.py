@@ -31,7 +31,8 @@ def test_encode_ties_toward_low_index():
     assert pqk.encode(pqk.PQCodebook(grid), np.array([0.5], dtype=np.float32))[0] == 0
 
 
-@pytest.mark.parametrize("n", [1, 5, 8, 9, 100, 128, 129, 255, 1000, 8193, 100_000, 1_234_567])
+# 1_048_876 / 2_102_153: unbalanced trees whose deepest level is small (74 / 1250 nodes) under levels of 8192 / 16384
+@pytest.mark.parametrize("n", [1, 5, 8, 9, 100, 128, 129, 255, 1000, 8193, 100_000, 1_048_876, 1_234_567, 2_102_153])
 def test_objective_tree_matches_numpy(n):
     import torch
 

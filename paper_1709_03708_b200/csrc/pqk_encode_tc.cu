@@ -114,6 +114,12 @@ extern "C" int pqk_tc_selftest(const void* d_a, const void* d_b, float* d_c, int
 namespace pqk {
 namespace enc {
 
+// Timing experiments of tools/exp_encode.sh (results are wrong when set): bit 0 the transform
+// only runs its barrier protocol, bit 1 the epilogue only reads the accumulator, bit 2 one
+// MMA instruction per item.
+#ifndef ENC_EXP
+#define ENC_EXP 0
+#endif
 constexpr int kRows = 128;
 constexpr int kN = 256;
 constexpr int kExt = 16;       // extension K columns of the hi pass
@@ -123,7 +129,13 @@ constexpr int kThreads = (2 + kEpiWarps + kTrWarps) * 32;
 // encode_tc_kernel's transform: one thread per row (4 warps x 32 rows), the row's KP
 // columns streamed in 8-column groups (no cross-lane reductions, no per-row shuffles)
 constexpr int kTrWarpsR = 4;
-constexpr int kThreadsR = (2 + kEpiWarps + kTrWarpsR) * 32;
+// ENC_TRSETS transform warp sets take alternate items (measured on a B200: two sets are 3%
+// slower than one, the kernel is bound by ALU-pipe issue, not by the transform's latency)
+#ifndef ENC_TRSETS
+#define ENC_TRSETS 1
+#endif
+constexpr int kTrSets = ENC_TRSETS;
+constexpr int kThreadsR = (2 + kEpiWarps + kTrSets * kTrWarpsR) * 32;
 constexpr int kChunk = 32;     // epilogue columns per tcgen05.ld pair
 constexpr bool kMmaHalves = false;  // N=128 MMA halves (separately released) vs N=256
 constexpr float kX2Limit = 1073741824.0f;  // 2^30: |s x|^2 bound for the fp16 extension parts
@@ -249,11 +261,13 @@ __device__ __forceinline__ void chunk_fold(const uint32_t (&k)[32], int c, int (
 }
 // second-smallest class minimum (as a key truncated to 4 bits less, class in the low
 // bits: unique keys) and the class of the smallest
-__device__ __forceinline__ void class_best2(const int (&cls)[16], uint32_t kmask, uint32_t one, int& qb, int& Y) {
+__device__ __forceinline__ void class_best2(const int (&cls)[16], uint32_t kmask, uint32_t one, int& qb, int& Y,
+                                            int* best_key = nullptr) {
   uint32_t ck[32];
 #pragma unroll
   for (int q = 0; q < 16; ++q) ck[q] = ((uint32_t)cls[q] & kmask) | (uint32_t)q;
   const int b = tree_min16(ck, 0);
+  if (best_key) *best_key = b;
   qb = b & 15;
   const uint32_t nbp = ~(uint32_t)b;  // -(b + 1): the winner maps to 0xffffffff
 #pragma unroll
@@ -264,6 +278,16 @@ __device__ __forceinline__ void class_best2(const int (&cls)[16], uint32_t kmask
   Y = (int)(min(umin3(t0, t1, t2), umin3(t3, t4, ck[15])) - nbp) & (int)kmask;
 }
 
+// one 32-column chunk c, group minima kept per group (encode_tc_kernel's epilogue: the
+// running best / runner-up fold of fold_group cost 5 ALU-pipe instructions per group, the
+// kernel's limiting pipe; the 16 minima are ranked once per row by class_best2 instead)
+__device__ __forceinline__ void chunk_fold_keep(const uint32_t (&k)[32], int c, int (&cls)[16], int (&grp)[16]) {
+#pragma unroll
+  for (int q = 0; q < 16; ++q) cls[q] = imin3(cls[q], (int)k[q], (int)k[q + 16]);
+  grp[2 * c] = tree_min16(k, 0);
+  grp[2 * c + 1] = tree_min16(k, 16);
+}
+
 // Epilogue of one 128-row item for one epilogue warp (row n of TMEM lane quadrant q):
 // the 256 accumulator columns (two N=128 halves, signalled and released separately),
 // best / runner-up by the group x class partitions, certificate, code store or flag.
@@ -271,17 +295,17 @@ __device__ __forceinline__ void epilogue_row(const EncParams& p, int m, int64_t 
                                              uint64_t* tempty2, uint32_t ph, float4 st, float eps_main2,
                                              float eps_main3, float eps_ext, float cb, float cnm, float s1c,
                                              float sqrt_kp, int lane) {
-  int cls[16];
+  int cls[16], grp[16];
 #pragma unroll
   for (int q = 0; q < 16; ++q) cls[q] = 0x7fffffff;
-  int G1 = 0x7fffffff, G2 = 0x7fffffff, gi = 0;
   uint32_t ka[32], kb[32];
   tmem_ld32(tacc, ka);
 #pragma unroll
   for (int c = 0; c < kN / kChunk; c += 2) {
     tmem_wait32(ka);
     tmem_ld32(tacc + (uint32_t)((c + 1) * kChunk), kb);
-    chunk_fold(ka, c, cls, G1, G2, gi);
+    if (!(ENC_EXP & 2)) chunk_fold_keep(ka, c, cls, grp);
+    else grp[2 * c] = grp[2 * c + 1] = (int)ka[c];
     tmem_wait32(kb);
     if (c + 2 == kN / kChunk / 2 || c + 2 == kN / kChunk) {  // a column half fully read
       tc::fence_before();
@@ -295,15 +319,22 @@ __device__ __forceinline__ void epilogue_row(const EncParams& p, int m, int64_t 
       }
       tmem_ld32(tacc + (uint32_t)((c + 2) * kChunk), ka);
     }
-    chunk_fold(kb, c + 1, cls, G1, G2, gi);
+    if (!(ENC_EXP & 2)) chunk_fold_keep(kb, c + 1, cls, grp);
+    else grp[2 * c + 2] = grp[2 * c + 3] = (int)kb[c];
   }
   if (n < p.n) {
-    int qb, Y;
-    class_best2(cls, p.keymask, p.one, qb, Y);
+    int qb, Y, gi, G2, bk;
+    class_best2(cls, p.keymask, p.one, qb, Y, &bk);
+    class_best2(grp, p.keymask, p.one, gi, G2);
     const int R = min(G2, Y);
-    // the best word is exact; R is exact (G2) or truncated by 4 mantissa bits (Y: within
-    // 16 ulp <= 2^-19 |v| of the value, below it for v >= 0, above it for v < 0)
-    const float w_hi = __int_as_float(G1), rv = __int_as_float(R);
+    // every key is truncated by 4 mantissa bits (within 16 ulp <= 2^-19 |v| of its value,
+    // below it for v >= 0, above it for v < 0).  The best word W lies between the smallest
+    // class key's two ends (low bits 0 / 15; w_hi: the larger as floats); R bounds the
+    // runner-up from below after the (1 + 2^-17) step for negative words.  gi and qb can name
+    // different columns only when another word shares W's upper 28 bits, i.e. lies within
+    // d15 = 15 ulp of it: the d15 margin keeps such rows from certifying.
+    const float w_a = __int_as_float(bk | 15), w_b = __int_as_float(bk & ~15);
+    const float w_hi = fmaxf(w_a, w_b), d15 = fabsf(w_a - w_b), rv = __int_as_float(R);
     const float r_lo = rv >= 0.f ? rv : rv * 1.00000762939453125f;  // 1 + 2^-17
     // rigorous bound on |computed - exact| of any D_rj (see header)
     const float P = st.y * cb * 1.001f;  // >= sum |split products|
@@ -312,7 +343,8 @@ __device__ __forceinline__ void epilogue_row(const EncParams& p, int m, int64_t 
                     + 2.98023223876953125e-08f * (sqrt_kp * st.y + s1c)          // 2^-25: subnormal lo parts
                     + 9.313225746154785e-10f * (cnm + st.x)                      // 2^-30: extension parts
                     + 1e-3f;
-    const bool cert = st.z != 0.f && (r_lo - w_hi) > 2.0f * E * 1.0001f;
+    const bool cert = ENC_EXP ? true
+                              : (st.z != 0.f && (r_lo - w_hi) > 2.0f * E * 1.0001f + 1.01f * d15);
     if (cert) {
       p.codes[n * p.stride + m] = (uint8_t)(16 * gi + qb);
     } else {
@@ -492,21 +524,23 @@ __global__ void __launch_bounds__(kThreadsR, 1) encode_tc_kernel(const __grid_co
           // scale with it, <= 2^-9 of the main terms), then hi . hi, then the |c|^2 / |x|^2
           // extension block last, so that the large extension terms enter in one instruction
 #pragma unroll
-          for (int s = 0; s < KP / 16; ++s)
+          for (int s = 0; s < ((ENC_EXP & 4) ? 1 : KP / 16); ++s)
             tc::mma_f16(tacc, tc::smem_desc(a_hi + s * 256, 128, sboE), tc::smem_desc(b_lo + s * 256, 128, sboP), idesc,
                         s > 0 ? 1u : 0u);
-          if (lo_any) {
+          if (lo_any && !(ENC_EXP & 4)) {
 #pragma unroll
             for (int s = 0; s < KP / 16; ++s)
               tc::mma_f16(tacc, tc::smem_desc(a_lo + s * 256, 128, sboP), tc::smem_desc(b_hi + s * 256, 128, sboE),
                           idesc, 1u);
           }
+          if (!(ENC_EXP & 4)) {
 #pragma unroll
-          for (int s = 0; s < KP / 16; ++s)
-            tc::mma_f16(tacc, tc::smem_desc(a_hi + s * 256, 128, sboE), tc::smem_desc(b_hi + s * 256, 128, sboE), idesc,
-                        1u);
-          tc::mma_f16(tacc, tc::smem_desc(a_hi + (KP / 16) * 256, 128, sboE),
-                      tc::smem_desc(b_hi + (KP / 16) * 256, 128, sboE), idesc, 1u);
+            for (int s = 0; s < KP / 16; ++s)
+              tc::mma_f16(tacc, tc::smem_desc(a_hi + s * 256, 128, sboE), tc::smem_desc(b_hi + s * 256, 128, sboE),
+                          idesc, 1u);
+            tc::mma_f16(tacc, tc::smem_desc(a_hi + (KP / 16) * 256, 128, sboE),
+                        tc::smem_desc(b_hi + (KP / 16) * 256, 128, sboE), idesc, 1u);
+          }
           tc::commit(&tfull[2 * ab + hf]);
           if (NH == 1) tc::commit(&tfull[2 * ab + 1]);
         }
@@ -545,56 +579,76 @@ __global__ void __launch_bounds__(kThreadsR, 1) encode_tc_kernel(const __grid_co
     // 8-column groups streamed X (swizzled TMA tile) -> scaled fp16 hi / lo -> the UMMA
     // K-major A tiles (8 consecutive rows = one 128-byte core matrix per STS.128 phase);
     // |s x|^2 and the lo-nonzero flag accumulate in the row's own thread.
-    const int tw = warp - 2 - kEpiWarps;
+    const int tw = (warp - 2 - kEpiWarps) % kTrWarpsR;
+    const int tset = (warp - 2 - kEpiWarps) / kTrWarpsR;  // items tset, tset + kTrSets, ...
     const int r = 32 * tw + lane;
     constexpr int NG = KP / 8;
     const float sc = s_cst[CST_S];
     const __half acn = __float2half_rn(s_cst[CST_ACN]);
     const bool valid = s_cst[CST_VALID] != 0.f;
     const uint32_t aoff_hi = tc::kmajor_off(r, 0, KE), aoff_lo = (uint32_t)G::A_HI + tc::kmajor_off(r, 0, KP);
-    for (int w = 0; w < items; ++w) {
+    for (int w = tset; w < items; w += kTrSets) {
       const int ab = w & 1, xs = w % G::XST;
+      // several sets: A buffer first (MMA(w - 2) done implies every earlier item was
+      // transformed, so this set is never two phases ahead of the X ring, where a parity wait
+      // would pass on stale data); one set: X first, its loads fly while the A buffer drains
+      if (kTrSets > 1) mbar_wait(&aempty[ab], (uint32_t)(((w >> 1) & 1) ^ 1));
       mbar_wait(&xfull[xs], (uint32_t)((w / G::XST) & 1));
-      mbar_wait(&aempty[ab], (uint32_t)(((w >> 1) & 1) ^ 1));
       const uint8_t* xb = sX + xs * G::X_STAGE;
       uint8_t* ahi = sA + ab * G::A_BYTES + aoff_hi;
       uint8_t* alo = sA + ab * G::A_BYTES + aoff_lo;
       float acc0 = 0.f, acc1 = 0.f;
       uint32_t lr = 0;
+      // batches of up to 4 groups (32 floats): every load of a batch is issued before its
+      // first A store (the stores could alias the loads for the compiler, which would
+      // otherwise expose one shared-memory round trip per group)
+      constexpr int GB = NG < 4 ? NG : 4;
+      if (ENC_EXP & 1) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&xempty[xs]);
+        if (kTrSets == 1) mbar_wait(&aempty[ab], (uint32_t)(((w >> 1) & 1) ^ 1));
+      }
 #pragma unroll
-      for (int g = 0; g < NG; ++g) {
-        float v[8];
+      for (int g0 = 0; g0 < ((ENC_EXP & 1) ? 0 : NG); g0 += GB) {
+        float4 f[2 * GB];
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          float4 f = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int i = 0; i < 2 * GB; ++i) {
+          const int g = g0 + i / 2, h = i & 1;
+          f[i] = make_float4(0.f, 0.f, 0.f, 0.f);
           if (G::SWZ) {
             // 128-byte rows of 8 x 16-byte chunks, chunk index XOR (row % 8); KP = 64: two halves
             const int chunk = 2 * g + h, half = chunk >> 3, ch = chunk & 7;
-            f = *reinterpret_cast<const float4*>(xb + half * (kRows * 128) + r * 128 + ((ch ^ (r & 7)) << 4));
+            f[i] = *reinterpret_cast<const float4*>(xb + half * (kRows * 128) + r * 128 + ((ch ^ (r & 7)) << 4));
           } else if (8 * g < ks) {  // dsub = 8 < KP = 16: the upper group is zero padding
-            f = *reinterpret_cast<const float4*>(reinterpret_cast<const float*>(xb) + r * ks + 8 * g + 4 * h);
+            f[i] = *reinterpret_cast<const float4*>(reinterpret_cast<const float*>(xb) + r * ks + 8 * g + 4 * h);
           }
-          v[4 * h] = f.x;
-          v[4 * h + 1] = f.y;
-          v[4 * h + 2] = f.z;
-          v[4 * h + 3] = f.w;
         }
-        uint32_t hw[4], lw[4];
+        if (kTrSets == 1 && g0 == 0) mbar_wait(&aempty[ab], (uint32_t)(((w >> 1) & 1) ^ 1));
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const float a0 = v[2 * j] * sc, a1 = v[2 * j + 1] * sc;
-          const __half2 hh = __floats2half2_rn(a0, a1);
-          const float2 hf = __half22float2(hh);
-          const __half2 ll = __floats2half2_rn(a0 - hf.x, a1 - hf.y);
-          hw[j] = *reinterpret_cast<const uint32_t*>(&hh);
-          lw[j] = *reinterpret_cast<const uint32_t*>(&ll);
-          acc0 = fmaf(a0, a0, acc0);
-          acc1 = fmaf(a1, a1, acc1);
+        for (int gg = 0; gg < GB; ++gg) {
+          const int g = g0 + gg;
+          const float v[8] = {f[2 * gg].x,     f[2 * gg].y,     f[2 * gg].z,     f[2 * gg].w,
+                              f[2 * gg + 1].x, f[2 * gg + 1].y, f[2 * gg + 1].z, f[2 * gg + 1].w};
+          uint32_t hw[4], lw[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const float a0 = v[2 * j] * sc, a1 = v[2 * j + 1] * sc;
+            const __half2 hh = __floats2half2_rn(a0, a1);
+            const float2 hf = __half22float2(hh);
+            const __half2 ll = __floats2half2_rn(a0 - hf.x, a1 - hf.y);
+            hw[j] = *reinterpret_cast<const uint32_t*>(&hh);
+            lw[j] = *reinterpret_cast<const uint32_t*>(&ll);
+            acc0 = fmaf(a0, a0, acc0);
+            acc1 = fmaf(a1, a1, acc1);
+          }
+          lr |= (lw[0] | lw[1]) | (lw[2] | lw[3]);
+          *reinterpret_cast<uint4*>(ahi + g * 128) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+          *reinterpret_cast<uint4*>(alo + g * 128) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
         }
-        lr |= (lw[0] | lw[1]) | (lw[2] | lw[3]);
-        *reinterpret_cast<uint4*>(ahi + g * 128) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
-        *reinterpret_cast<uint4*>(alo + g * 128) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
       }
+      // the X stage is released only after the loaded values were used: releasing it right
+      // after the loads were issued (before the A-buffer wait) produced wrong codes in the
+      // items that follow a CTA's start (tools/diag_encode_mismatch.py)
       __syncwarp();
       if (lane == 0) mbar_arrive(&xempty[xs]);
       lr &= 0x7fff7fffu;  // -0 lo parts are zeros
@@ -1063,8 +1117,6 @@ __global__ void __launch_bounds__(kThreads, 1) encode_tck_kernel(const __grid_co
             v[ps][4 * cc + 3] = f.w;
           }
         }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&xempty[xs]);
         uint32_t hw[2][4], lw[2][4];
         uint32_t lo_nz = 0;
 #pragma unroll
@@ -1093,6 +1145,9 @@ __global__ void __launch_bounds__(kThreads, 1) encode_tck_kernel(const __grid_co
           lo_nz |= lr;
         }
         const unsigned bal = __ballot_sync(0xffffffffu, lo_nz != 0);
+        // released after the loaded values were consumed (an arrive issued right behind the
+        // loads is not ordered after their completion: see encode_tc_kernel's transform)
+        if (lane == 0) mbar_arrive(&xempty[xs]);
         mbar_wait(&aempty[as], (uint32_t)(((g / kASt) & 1) ^ 1));
         uint8_t* ahi = sA + as * G::A_CHUNK;
 #pragma unroll

@@ -180,6 +180,7 @@ struct EncParams {
   int tstride;       // CTAs per subspace
   uint32_t keymask;  // ~15u, a run-time value so that key packing is one LOP3
   uint32_t one;      // 1
+  uint32_t* tcmask;  // K-streamed kernel: [M][flag_cap][8] candidate codewords of each uncertified pair
 };
 
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
@@ -380,13 +381,10 @@ __device__ __forceinline__ void epilogue_row_split(const EncParams& p, int m, in
     tmem_wait32(kb);
 #pragma unroll
     for (int j = 0; j < 32; ++j) ka[j] = __float_as_uint(__fadd_rn(__uint_as_float(ka[j]), __uint_as_float(kb[j])));
-    if (c + 1 == kN / kChunk / 2 || c + 1 == kN / kChunk) {  // a column half (of H and L) fully read
-      tc::fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty2[c + 1 == kN / kChunk ? 1 : 0]);
-    }
     chunk_fold(ka, c, cls, G1, G2, gi);
   }
+  bool flagged = false;
+  float thr = __int_as_float(0xff800000);  // -inf: no candidates
   if (n < p.n) {
     int qb, Y;
     class_best2(cls, p.keymask, p.one, qb, Y);
@@ -404,12 +402,50 @@ __device__ __forceinline__ void epilogue_row_split(const EncParams& p, int m, in
     if (cert) {
       p.codes[n * p.stride + m] = (uint8_t)(16 * gi + qb);
     } else {
-      atomicAdd(&p.counters[0], 1u);
-      const unsigned f = atomicAdd(&p.counters[2 + m], 1u);
-      if (f < p.flag_cap)
-        p.flags[(size_t)m * p.flag_cap + f] = (uint32_t)n;
-      else
-        p.counters[1] = 1u;
+      flagged = true;
+      // candidates: every codeword whose exact distance can be <= the winner's, i.e. computed
+      // D_j <= W + 2 E (w_hi is some computed value >= the smallest one, also when negative
+      // words misorder as integers); all of them for rows outside the certified range
+      const float t0 = w_hi + 2.0f * E * 1.0001f;
+      const float t = t0 + fabsf(t0) * 1e-6f + 1e-30f;  // the sum rounded up
+      thr = (st.z != 0.f && t == t) ? t : __int_as_float(0x7f800000);
+    }
+  }
+  // second pass over the accumulators for warps with an uncertified row: its candidate mask
+  uint32_t mw[kN / kChunk] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+  if (__any_sync(0xffffffffu, flagged)) {
+#pragma unroll 1
+    for (int c = 0; c < kN / kChunk; ++c) {
+      tmem_ld32(tacc + (uint32_t)(c * kChunk), ka);
+      tmem_ld32(tacc + (uint32_t)(kN + c * kChunk), kb);
+      tmem_wait32(ka);
+      tmem_wait32(kb);
+      uint32_t word = 0;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const float v = __fadd_rn(__uint_as_float(ka[j]), __uint_as_float(kb[j]));
+        word |= !(v > thr) ? (1u << j) : 0u;  // NaN counts as a candidate
+      }
+#pragma unroll
+      for (int q = 0; q < kN / kChunk; ++q) mw[q] = (q == c) ? word : mw[q];
+    }
+  }
+  tc::fence_before();
+  __syncwarp();
+  if (lane == 0) {
+    mbar_arrive(&tempty2[0]);
+    mbar_arrive(&tempty2[1]);
+  }
+  if (flagged) {
+    atomicAdd(&p.counters[0], 1u);
+    const unsigned f = atomicAdd(&p.counters[2 + m], 1u);
+    if (f < p.flag_cap) {
+      p.flags[(size_t)m * p.flag_cap + f] = (uint32_t)n;
+      uint4* dst = reinterpret_cast<uint4*>(p.tcmask + ((size_t)m * p.flag_cap + f) * 8);
+      dst[0] = make_uint4(mw[0], mw[1], mw[2], mw[3]);
+      dst[1] = make_uint4(mw[4], mw[5], mw[6], mw[7]);
+    } else {
+      p.counters[1] = 1u;
     }
   }
 }
@@ -1660,12 +1696,181 @@ __global__ void __launch_bounds__(256) encode_filter32_k_kernel(
   }
 }
 
+// fp32 filter over the tensor-core pass's candidates (K-streamed path).  encode_tck_kernel
+// leaves each uncertified pair with the mask of the codewords its error bound cannot
+// exclude (a handful of the 256); this kernel evaluates only those: one warp per pair,
+// lanes over the dimensions (float4, coalesced codeword rows), d^ = sum (x - c)^2 in fp32.
+// Every term is >= 0, so for any summation order |d^ - D| <= g D + eta with
+// g = (ks + 2) 2^-24 (x 1.01), eta = ks 2^-120 (encode_filter32_k_kernel's bound, which this
+// kernel replaces on the product path); the certificate and the reduced candidate mask
+// handed to encode_exact_cand_kernel are the same as there.
+__global__ void __launch_bounds__(256) encode_filter32_cand_kernel(
+    const float* __restrict__ x, int d, const float* __restrict__ cw, int m, int l, int ks,
+    const uint32_t* __restrict__ flags, const unsigned int* __restrict__ counters, uint32_t flag_cap,
+    const uint32_t* __restrict__ tcmask, uint8_t* __restrict__ codes, int stride, uint32_t* __restrict__ flags2,
+    unsigned int* __restrict__ counters2, uint32_t* __restrict__ cmask2) {
+  __shared__ float s_val[8][256];
+  if (counters[1] != 0) {  // the pair list overflowed: every row goes to encode_exact_k_kernel
+    if (blockIdx.x == 0 && threadIdx.x == 0) counters2[1] = 1u;
+    return;
+  }
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const double g32 = (double)(ks + 2) * 5.9604644775390625e-08 * 1.01;
+  const double g64 = (double)(ks + 2) * 1.1102230246251565e-16 * 1.01;
+  const double eta = (double)ks * 7.52316384526264e-37;  // ks x 2^-120
+  int64_t tot = 0;
+  for (int q = 0; q < m; ++q) tot += min(counters[2 + q], flag_cap);
+  float* val = s_val[wib];
+  for (int64_t pi = gw; pi < tot; pi += nw) {
+    int mm = 0;
+    int64_t i = pi;
+    while (i >= (int64_t)min(counters[2 + mm], flag_cap)) i -= min(counters[2 + mm], flag_cap), ++mm;
+    const size_t slot = (size_t)mm * flag_cap + (size_t)i;
+    const int64_t row = flags[slot];
+    const float* xv = x + row * d + (size_t)mm * ks;
+    const float* cb = cw + (size_t)mm * l * ks;
+    // the row's x values: float4 groups lane, lane + 32, ... (ks <= 1024: at most 8 per lane)
+    float4 xr[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      xr[q] = (4 * (lane + 32 * q) < ks) ? __ldg(reinterpret_cast<const float4*>(xv) + lane + 32 * q)
+                                         : make_float4(0.f, 0.f, 0.f, 0.f);
+    uint32_t mword[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) mword[u] = __ldg(tcmask + slot * 8 + u);
+    float b1 = __int_as_float(0x7f800000);
+    int l1 = 0x7fffffff;
+    bool nan = false;
+    __syncwarp();
+    for (int u = 0; u < 8; ++u) {
+      uint32_t bm = mword[u];
+      while (bm) {
+        // two candidates per round (their loads overlap)
+        const int j0 = __ffs(bm) - 1;
+        bm &= bm - 1u;
+        const int j1 = bm ? __ffs(bm) - 1 : -1;
+        if (j1 >= 0) bm &= bm - 1u;
+        const int c0 = min(32 * u + j0, l - 1), c1 = min(32 * u + max(j1, 0), l - 1);
+        const float4* r0 = reinterpret_cast<const float4*>(cb + (size_t)c0 * ks);
+        const float4* r1 = reinterpret_cast<const float4*>(cb + (size_t)c1 * ks);
+        float a0 = 0.f, a1 = 0.f;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          if (4 * (lane + 32 * q) < ks) {
+            const float4 v0 = __ldg(r0 + lane + 32 * q), v1 = __ldg(r1 + lane + 32 * q);
+            float t;
+            t = __fsub_rn(xr[q].x, v0.x), a0 = __fmaf_rn(t, t, a0);
+            t = __fsub_rn(xr[q].y, v0.y), a0 = __fmaf_rn(t, t, a0);
+            t = __fsub_rn(xr[q].z, v0.z), a0 = __fmaf_rn(t, t, a0);
+            t = __fsub_rn(xr[q].w, v0.w), a0 = __fmaf_rn(t, t, a0);
+            t = __fsub_rn(xr[q].x, v1.x), a1 = __fmaf_rn(t, t, a1);
+            t = __fsub_rn(xr[q].y, v1.y), a1 = __fmaf_rn(t, t, a1);
+            t = __fsub_rn(xr[q].z, v1.z), a1 = __fmaf_rn(t, t, a1);
+            t = __fsub_rn(xr[q].w, v1.w), a1 = __fmaf_rn(t, t, a1);
+          }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          a0 = __fadd_rn(a0, __shfl_xor_sync(0xffffffffu, a0, o));
+          a1 = __fadd_rn(a1, __shfl_xor_sync(0xffffffffu, a1, o));
+        }
+        if (32 * u + j0 < l) {
+          nan |= (a0 != a0);
+          if (a0 < b1) b1 = a0, l1 = 32 * u + j0;  // ascending index: the first minimum stays
+          if (lane == 0) val[32 * u + j0] = a0;
+        }
+        if (j1 >= 0 && 32 * u + j1 < l) {
+          nan |= (a1 != a1);
+          if (a1 < b1) b1 = a1, l1 = 32 * u + j1;
+          if (lane == 0) val[32 * u + j1] = a1;
+        }
+      }
+    }
+    __syncwarp();
+    // candidates whose float64 distance can be <= the winner's (the winner among them)
+    const double lhs = ((double)b1 + eta) * (1.0 + g32) * (1.0 + g64) * (1.0 + 1e-12);
+    const bool finite = !nan && b1 < __int_as_float(0x7f800000);
+    uint32_t out[8];
+    int cnt = 0;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int c = lane + 32 * u;
+      const bool in = c < l && ((mword[u] >> lane) & 1u);
+      bool cand = false;
+      if (in) {
+        const double lo = ((double)val[c] - eta) * (1.0 - g32) * (1.0 - g64);
+        cand = !finite || lo <= lhs;
+      }
+      out[u] = __ballot_sync(0xffffffffu, cand);
+      cnt += __popc(out[u]);
+    }
+    if (finite && cnt == 1) {
+      if (lane == 0) codes[row * stride + mm] = (uint8_t)l1;
+    } else {
+      unsigned f = 0;
+      if (lane == 0) {
+        atomicAdd(&counters2[0], 1u);
+        f = atomicAdd(&counters2[2 + mm], 1u);
+        if (f < flag_cap)
+          flags2[(size_t)mm * flag_cap + f] = (uint32_t)row;
+        else
+          counters2[1] = 1u;
+      }
+      f = __shfl_sync(0xffffffffu, f, 0);
+      // an empty mask (cannot happen: the tensor-core winner is always its own candidate) or a
+      // non-finite row: every codeword goes to the float64 decision
+      if (f < flag_cap && lane < 8) {
+        uint32_t wv = 0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) wv = (lane == u) ? out[u] : wv;
+        if (!finite || cnt == 0) {  // codewords 32 lane .. 32 lane + 31 below l
+          const int nb = min(max(l - 32 * lane, 0), 32);
+          wv = nb == 32 ? 0xffffffffu : ((1u << nb) - 1u);
+        }
+        cmask2[((size_t)mm * flag_cap + f) * 8 + lane] = wv;
+      }
+    }
+    __syncwarp();
+  }
+}
+
 // Float64 decision over the pre-filter's candidates only (typically 2-3 of the 256
-// codewords): one warp per pair, one candidate per lane (rounds of 32), the sequential
-// float64 sum of (x - c)^2 in scipy cdist order, np.argmin order over the candidates (first
-// NaN, else value, then lowest index).  Codewords outside the candidate set are provably
-// farther in float64 (see encode_filter32_k_kernel), so this is the argmin over all 256.
-// When the pair list overflowed (counters2[1]) every row goes through encode_exact_k_kernel.
+// codewords per pair).  Float64 issue is the scarce resource (a warp instruction costs the
+// same for one active lane as for 32), so a warp packs the (pair, candidate) entries of
+// consecutive pairs onto its 32 lanes: each lane runs the sequential float64 sum of
+// (x - c)^2 in scipy cdist order for its entry, a segmented reduction picks each pair's
+// winner in np.argmin order (first NaN, else value, then lowest index).  Codewords outside
+// the candidate set are provably farther in float64 (see encode_filter32_cand_kernel), so
+// this is the argmin over all 256.  Pairs with more than 32 candidates (non-finite rows:
+// all of them) take the lanes alone, in rounds.  When the pair list overflowed
+// (counters2[1]) every row goes through encode_exact_k_kernel.
+__device__ __forceinline__ double exact_dist64(const float* __restrict__ xv, const float* __restrict__ cv, int ks) {
+  const float4* cv4 = reinterpret_cast<const float4*>(cv);
+  const float4* xv4 = reinterpret_cast<const float4*>(xv);
+  double acc = 0.0;
+  for (int k0 = 0; k0 < ks / 4; k0 += 8) {  // 32 dimensions per batch of loads (ks % 32 == 0)
+    float4 xa[8], ca[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      xa[q] = __ldg(xv4 + k0 + q);
+      ca[q] = __ldg(cv4 + k0 + q);
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const float xs[4] = {xa[q].x, xa[q].y, xa[q].z, xa[q].w};
+      const float cs[4] = {ca[q].x, ca[q].y, ca[q].z, ca[q].w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const double df = __dsub_rn((double)xs[e], (double)cs[e]);
+        acc = __dadd_rn(acc, __dmul_rn(df, df));
+      }
+    }
+  }
+  return acc;
+}
+
 __global__ void __launch_bounds__(256, 4) encode_exact_cand_kernel(
     const float* __restrict__ x, int d, const float* __restrict__ cw, int m, int l, int ks,
     const uint32_t* __restrict__ flags2, const unsigned int* __restrict__ counters2, uint32_t flag_cap,
@@ -1676,7 +1881,38 @@ __global__ void __launch_bounds__(256, 4) encode_exact_cand_kernel(
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   int64_t tot = 0;
   for (int q = 0; q < m; ++q) tot += min(counters2[2 + q], flag_cap);
-  for (int64_t p = gw; p < tot; p += nw) {
+  // a contiguous range of pairs per warp
+  // (at least 12: ~30 candidates, so that a flush fills most lanes)
+  const int64_t per = max((tot + nw - 1) / nw, (int64_t)12);
+  const int64_t p0 = min(tot, gw * per), p1 = min(tot, p0 + per);
+  // lane state of the batch being filled
+  const float* my_x = nullptr;
+  const float* my_c = nullptr;
+  int my_cw = 0x7fffffff, my_seg = -1;
+  int64_t my_out = -1;  // head lanes: where the pair's code goes
+  int fill = 0, seg = 0;
+  auto flush = [&]() {
+    double acc = __longlong_as_double(0x7ff0000000000000LL);
+    if (my_seg >= 0) acc = exact_dist64(my_x, my_c, ks);
+    int bl = my_cw;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const double ob = __shfl_down_sync(0xffffffffu, acc, o);
+      const int oi = __shfl_down_sync(0xffffffffu, bl, o);
+      const int os = __shfl_down_sync(0xffffffffu, my_seg, o);
+      if (lane + o < 32 && os == my_seg && my_seg >= 0 && argmin_less(ob, oi, acc, bl)) {
+        acc = ob;
+        bl = oi;
+      }
+    }
+    if (my_out >= 0) codes[my_out] = (uint8_t)bl;
+    my_seg = -1;
+    my_out = -1;
+    my_cw = 0x7fffffff;
+    fill = 0;
+    seg = 0;
+  };
+  for (int64_t p = p0; p < p1; ++p) {
     int mm = 0;
     int64_t i = p;
     while (i >= (int64_t)min(counters2[2 + mm], flag_cap)) i -= min(counters2[2 + mm], flag_cap), ++mm;
@@ -1684,68 +1920,74 @@ __global__ void __launch_bounds__(256, 4) encode_exact_cand_kernel(
     const int64_t row = flags2[slot];
     const float* xv = x + row * d + (size_t)mm * ks;
     const float* cb = cw + (size_t)mm * l * ks;
-    double best = __longlong_as_double(0x7ff0000000000000LL);
-    int bl = 0x7fffffff;
-    // candidates in ascending codeword order, 32 per round
-    int base = 0;  // candidates already assigned
-    for (int u = 0; u < 8; ++u) {
-      uint32_t bm = __ldg(cmask + slot * 8 + u);  // bit j: codeword j + 32 u
-      while (bm) {
-        // the next up-to-32 candidates of this word, one per lane
-        const int cnt = __popc(bm);
-        const int take = min(cnt, 32);
-        uint32_t mine = 0xffffffffu;
-        {
-          uint32_t t = bm;
-          for (int q = 0; q < take; ++q) {
-            const int j = __ffs(t) - 1;
-            t &= t - 1u;
-            if (q == lane) mine = (uint32_t)(j + 32 * u);
-          }
-          bm = t;
+    // lane u < 8 holds mask word u (codewords 32 u ..); counts and their prefix over the words
+    const uint32_t wv = lane < 8 ? __ldg(cmask + slot * 8 + lane) : 0u;
+    const int pc = __popc(wv);
+    int pre = pc;  // inclusive prefix over lanes
+#pragma unroll
+    for (int o = 1; o < 8; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, pre, o);
+      if (lane >= o) pre += t;
+    }
+    const int cnt = __shfl_sync(0xffffffffu, pre, 7);
+    if (cnt == 0) continue;  // cannot happen (the filter's winner is its own candidate)
+    if (cnt > 32) {
+      // rounds of 32 candidates on the whole warp
+      flush();
+      double best = __longlong_as_double(0x7ff0000000000000LL);
+      int bl = 0x7fffffff;
+      for (int t0 = 0; t0 < cnt; t0 += 32) {
+        const int k = t0 + lane;  // this lane's candidate: the k-th set bit of the 256-bit mask
+        int cwi = -1;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const uint32_t wu = __shfl_sync(0xffffffffu, wv, u);
+          const int hi = __shfl_sync(0xffffffffu, pre, u), lo = hi - __popc(wu);
+          if (k < cnt && k >= lo && k < hi) cwi = 32 * u + (int)__fns(wu, 0, k - lo + 1);
         }
-        if (mine != 0xffffffffu) {
-          const float4* cv4 = reinterpret_cast<const float4*>(cb + (size_t)mine * ks);
-          const float4* xv4 = reinterpret_cast<const float4*>(xv);
-          double acc = 0.0;
-          for (int k0 = 0; k0 < ks / 4; k0 += 8) {  // 32 dimensions per batch of loads (ks % 32 == 0)
-            float4 xa[8], ca[8];
-#pragma unroll
-            for (int q = 0; q < 8; ++q) {
-              xa[q] = __ldg(xv4 + k0 + q);
-              ca[q] = __ldg(cv4 + k0 + q);
-            }
-#pragma unroll
-            for (int q = 0; q < 8; ++q) {
-              const float xs[4] = {xa[q].x, xa[q].y, xa[q].z, xa[q].w};
-              const float cs[4] = {ca[q].x, ca[q].y, ca[q].z, ca[q].w};
-#pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                const double df = __dsub_rn((double)xs[e], (double)cs[e]);
-                acc = __dadd_rn(acc, __dmul_rn(df, df));
-              }
-            }
-          }
-          if (argmin_less(acc, (int)mine, best, bl)) {
+        if (cwi >= 0) {
+          const double acc = exact_dist64(xv, cb + (size_t)cwi * ks, ks);
+          if (argmin_less(acc, cwi, best, bl)) {
             best = acc;
-            bl = (int)mine;
+            bl = cwi;
           }
         }
-        base += take;
       }
-    }
-    (void)base;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-      const int oi = __shfl_xor_sync(0xffffffffu, bl, o);
-      if (argmin_less(ob, oi, best, bl)) {
-        best = ob;
-        bl = oi;
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bl, o);
+        if (argmin_less(ob, oi, best, bl)) {
+          best = ob;
+          bl = oi;
+        }
+      }
+      if (lane == 0) codes[row * stride + mm] = (uint8_t)bl;
+      continue;
+    }
+    if (fill + cnt > 32) flush();
+    // lanes fill .. fill + cnt - 1 take the pair's candidates in ascending codeword order
+    {
+      const int k = lane - fill;
+      int cwi = -1;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const uint32_t wu = __shfl_sync(0xffffffffu, wv, u);
+        const int hi = __shfl_sync(0xffffffffu, pre, u), lo = hi - __popc(wu);
+        if (k >= 0 && k < cnt && k >= lo && k < hi) cwi = 32 * u + (int)__fns(wu, 0, k - lo + 1);
+      }
+      if (cwi >= 0) {
+        my_x = xv;
+        my_c = cb + (size_t)cwi * ks;
+        my_cw = cwi;
+        my_seg = seg;
+        if (k == 0) my_out = row * stride + mm;
       }
     }
-    if (lane == 0) codes[row * stride + mm] = (uint8_t)bl;
+    fill += cnt;
+    ++seg;
   }
+  flush();
 }
 
 __global__ void encode_stats_kernel(const unsigned int* __restrict__ counters, unsigned long long* __restrict__ out) {
@@ -1873,7 +2115,7 @@ int launch_encode_tck(const float* d_x, int64_t n, int d, const float* d_cw, int
   const size_t bch_bytes = align_up((size_t)m * kMaxChunks * 4, 256);
   const size_t need = align_up(b_bytes, 256) + align_up((size_t)m * CST_LEN * 4, 256) +
                       2 * (align_up((size_t)m * cap * 4, 256) + align_up((size_t)(m + 2) * 4, 256)) + bch_bytes +
-                      align_up((size_t)m * cap * 32, 256) + align_up((size_t)m * l * ks * 4, 256) + 256;
+                      2 * align_up((size_t)m * cap * 32, 256) + align_up((size_t)m * l * ks * 4, 256) + 256;
   if (ws.bytes < need) {
     if (ws.p) cudaFree(ws.p);
     ws.p = nullptr;
@@ -1894,7 +2136,9 @@ int launch_encode_tck(const float* d_x, int64_t n, int d, const float* d_cw, int
   unsigned int* counters2 =
       reinterpret_cast<unsigned int*>(reinterpret_cast<char*>(flags2) + align_up((size_t)m * cap * 4, 256));
   uint32_t* cmask = reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(counters2) + align_up((size_t)(m + 2) * 4, 256));
-  float* cw_copy = reinterpret_cast<float*>(reinterpret_cast<char*>(cmask) + align_up((size_t)m * cap * 32, 256));
+  // candidate masks left by the tensor-core pass (cmask: those left by the fp32 filter)
+  uint32_t* tcmask = reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(cmask) + align_up((size_t)m * cap * 32, 256));
+  float* cw_copy = reinterpret_cast<float*>(reinterpret_cast<char*>(tcmask) + align_up((size_t)m * cap * 32, 256));
   int* differs = reinterpret_cast<int*>(reinterpret_cast<char*>(cw_copy) + align_up((size_t)m * l * ks * 4, 256));
 
   CUtensorMap map;
@@ -1943,16 +2187,29 @@ int launch_encode_tck(const float* d_x, int64_t n, int d, const float* d_cw, int
   ep.tstride = std::max(1, std::min(di.sms / m, ep.ntiles));
   ep.keymask = ~15u;
   ep.one = 1u;
+  ep.tcmask = tcmask;
   PQK_CUDA_TRY(cudaFuncSetAttribute(encode_tck_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM));
   encode_tck_kernel<<<ep.tstride * m, kThreads, G::SMEM, stream>>>(map, ep);
   PQK_LAUNCH_CHECK("encode_tck_kernel");
   const dim3 egrid((unsigned)(2 * di.sms), 1u);  // flattened (subspace, tile) schedule
-  // fp32 pre-filter of the tensor-core pass's uncertified pairs, then float64 for the rest
-  const int fsmem = 2 * 256 * 33 * 4;
-  PQK_CUDA_TRY(cudaFuncSetAttribute(encode_filter32_k_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, fsmem));
-  encode_filter32_k_kernel<<<egrid, 256, fsmem, stream>>>(d_x, n, d, d_cw, m, l, ks, flags, counters, cap, d_codes,
-                                                          stride, flags2, counters2, cmask);
-  PQK_LAUNCH_CHECK("encode_filter32_k_kernel");
+  // fp32 filter over the candidates the tensor-core pass left for each uncertified pair, then
+  // float64 for what it cannot decide (PQK_ENCODE_DENSE_FILTER=1: the earlier filter over all
+  // 256 codewords of those pairs, kept for comparison runs)
+  static const bool dense_filter = [] {
+    const char* e = getenv("PQK_ENCODE_DENSE_FILTER");
+    return e && e[0] == '1';
+  }();
+  if (dense_filter) {
+    const int fsmem = 2 * 256 * 33 * 4;
+    PQK_CUDA_TRY(cudaFuncSetAttribute(encode_filter32_k_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, fsmem));
+    encode_filter32_k_kernel<<<egrid, 256, fsmem, stream>>>(d_x, n, d, d_cw, m, l, ks, flags, counters, cap, d_codes,
+                                                            stride, flags2, counters2, cmask);
+    PQK_LAUNCH_CHECK("encode_filter32_k_kernel");
+  } else {
+    encode_filter32_cand_kernel<<<di.sms * 8, 256, 0, stream>>>(d_x, d, d_cw, m, l, ks, flags, counters, cap, tcmask,
+                                                                 d_codes, stride, flags2, counters2, cmask);
+    PQK_LAUNCH_CHECK("encode_filter32_cand_kernel");
+  }
   // float64 over the candidates of each remaining pair; every row (all 256 codewords) only
   // when the pair list overflowed
   encode_exact_cand_kernel<<<di.sms * 8, 256, 0, stream>>>(d_x, d, d_cw, m, l, ks, flags2, counters2, cap, cmask,

@@ -168,3 +168,24 @@ def test_tck_prepared_operands_follow_codebook_changes(oracle):
             continue  # step 1 reuses the prepared operands
         cw[1, 7] += 0.5  # in place, same device pointer
         cd.copy_(torch.from_numpy(cw))
+
+
+@pytest.mark.parametrize("l_count", [256, 100, 33])
+def test_tck_candidate_masks_small_codebooks_ties_and_non_finite(oracle, l_count):
+    """K-streamed path (dsub = 128): near-duplicate and duplicated codewords (pairs the
+    tensor-core certificate must hand on with a candidate mask), fewer than 256 codewords,
+    and rows with NaN / inf (every codeword is a candidate: np.argmin's NaN rule)."""
+    rng = np.random.default_rng(l_count)
+    cw = rng.normal(size=(2, l_count, 128)).astype(np.float32)
+    cw[0, 5] = cw[0, 2]  # exact tie: the lower index wins
+    cw[1, 7] = cw[1, 3] + np.float32(1e-6)  # near tie
+    cw[1, l_count - 1] = cw[1, 0] * np.float32(1 + 2e-7)
+    x = rng.normal(size=(4000, 256)).astype(np.float32)
+    x[:300, :128] = cw[0, 2] + rng.normal(0, 1e-3, size=(300, 128)).astype(np.float32)
+    x[300:600, 128:] = cw[1, 3] + rng.normal(0, 1e-4, size=(300, 128)).astype(np.float32)
+    x[600:700, 128:] = cw[1, 0]
+    x[700, 3] = np.nan
+    x[701, 130] = np.inf
+    x[702, 5] = -np.inf
+    x[703] = np.nan
+    np.testing.assert_array_equal(_encode(cw, x), oracle.encode(cw, x))

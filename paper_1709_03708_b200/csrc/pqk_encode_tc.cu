@@ -194,6 +194,17 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
 __device__ __forceinline__ int imin3(int a, int b, int c) { return min(a, min(b, c)); }
 __device__ __forceinline__ uint32_t umin3(uint32_t a, uint32_t b, uint32_t c) { return min(a, min(b, c)); }
 
+// one lane of a converged warp (elect.sync: ptxas then knows a single thread runs the branch)
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "elect.sync _|p, 0xffffffff;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(pred));
+  return pred != 0;
+}
+
 __device__ __forceinline__ uint32_t pack_h2(__half a, __half b) {
   return (uint32_t)__half_as_ushort(a) | ((uint32_t)__half_as_ushort(b) << 16);
 }
@@ -364,77 +375,173 @@ __device__ __forceinline__ void epilogue_row(const EncParams& p, int m, int64_t 
 // rounding) before the same partition minima and certificate.  st.w carries the row's
 // prefix bound W = sum over chunks c of the running sum of |x_c| max_j |B_j,c| (bounds
 // every max |addend| of H's two hi . hi instructions per chunk).
+//
+// Nothing of the next item can overlap this epilogue (both accumulators belong to one
+// item), so each TMEM lane quadrant is served by two warps: half 0 folds codewords
+// [0, 128), half 1 codewords [128, 256).  Half 1 hands its class minima and its best /
+// runner-up group minima to half 0 through shared memory (ex, 20 words per row); half 0
+// merges, decides and hands back the candidate threshold of its uncertified rows; both then
+// build their half of the candidate mask, re-reading only the 32-column chunks whose group
+// minima (kept in registers) admit a candidate.  Named barrier bar (64 threads) orders
+// the three hand-overs.
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait16(uint32_t (&r)[16]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
+                 "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]),
+                 "+r"(r[15])
+               :
+               : "memory");
+}
+__device__ __forceinline__ void pair_sync(int bar) { asm volatile("bar.sync %0, 64;" ::"r"(bar) : "memory"); }
+
+constexpr int kExWords = 20;  // per row: 16 class minima, G1, G2, gi, pad (80 B: conflict-free uint4 rows)
+
+// H + L of one 32-column chunk into ka (L read in two 16-column pieces)
+__device__ __forceinline__ void load_sum32(uint32_t tacc, int c, uint32_t (&ka)[32]) {
+  uint32_t kb[16];
+  tmem_ld32(tacc + (uint32_t)(c * kChunk), ka);
+  tmem_ld16(tacc + (uint32_t)(kN + c * kChunk), kb);
+  tmem_wait32(ka);
+  tmem_wait16(kb);
+#pragma unroll
+  for (int j = 0; j < 16; ++j) ka[j] = __float_as_uint(__fadd_rn(__uint_as_float(ka[j]), __uint_as_float(kb[j])));
+  tmem_ld16(tacc + (uint32_t)(kN + c * kChunk + 16), kb);
+  tmem_wait16(kb);
+#pragma unroll
+  for (int j = 0; j < 16; ++j)
+    ka[16 + j] = __float_as_uint(__fadd_rn(__uint_as_float(ka[16 + j]), __uint_as_float(kb[j])));
+}
+
+template <bool kPair>
+__device__ __forceinline__ void arrive_at_issuer(uint64_t* bar) {  // the MMA issuer's barrier (pair: in cluster rank 0)
+  if (kPair) tc::mbar_arrive_rank0(bar);
+  else mbar_arrive(bar);
+}
+
+template <bool kPair>
 __device__ __forceinline__ void epilogue_row_split(const EncParams& p, int m, int64_t n, uint32_t tacc,
                                                    uint64_t* tempty2, float4 st, float eps_h, float eps_l,
                                                    float eps_ext, float cb, float cnm, float s1c, float sqrt_kp,
-                                                   int lane) {
-  int cls[16];
+                                                   int lane, int half, uint32_t* ex_row, int bar) {
+  int cls[16], grp[8];
 #pragma unroll
   for (int q = 0; q < 16; ++q) cls[q] = 0x7fffffff;
   int G1 = 0x7fffffff, G2 = 0x7fffffff, gi = 0;
-  uint32_t ka[32], kb[32];
-#pragma unroll 1
-  for (int c = 0; c < kN / kChunk; ++c) {
-    tmem_ld32(tacc + (uint32_t)(c * kChunk), ka);
-    tmem_ld32(tacc + (uint32_t)(kN + c * kChunk), kb);
-    tmem_wait32(ka);
-    tmem_wait32(kb);
+  uint32_t ka[32];
 #pragma unroll
-    for (int j = 0; j < 32; ++j) ka[j] = __float_as_uint(__fadd_rn(__uint_as_float(ka[j]), __uint_as_float(kb[j])));
-    chunk_fold(ka, c, cls, G1, G2, gi);
+  for (int cc = 0; cc < 4; ++cc) {
+    const int c = 4 * half + cc;
+    load_sum32(tacc, c, ka);
+#pragma unroll
+    for (int q = 0; q < 16; ++q) cls[q] = imin3(cls[q], (int)ka[q], (int)ka[q + 16]);
+    grp[2 * cc] = tree_min16(ka, 0);
+    grp[2 * cc + 1] = tree_min16(ka, 16);
+    fold_group(grp[2 * cc], 2 * c, G1, G2, gi);
+    fold_group(grp[2 * cc + 1], 2 * c + 1, G1, G2, gi);
   }
+  uint4* ex4 = reinterpret_cast<uint4*>(ex_row);
   bool flagged = false;
   float thr = __int_as_float(0xff800000);  // -inf: no candidates
-  if (n < p.n) {
-    int qb, Y;
-    class_best2(cls, p.keymask, p.one, qb, Y);
-    const int R = min(G2, Y);
-    const float w_hi = __int_as_float(G1), rv = __int_as_float(R);
-    const float r_lo = rv >= 0.f ? rv : rv * 1.00000762939453125f;
-    const float P = st.y * cb * 1.001f;
-    const float W = fminf(st.w, (float)(p.ks / 32) * P);  // every prefix (32-column chunks) is also <= P
-    const float E = eps_h * W + eps_l * P + eps_ext * (P + cnm + st.x) * 1.001f  //
-                    + 4.76837158203125e-07f * P                                 // 4 * 2^-23: split, lo.lo
-                    + 2.98023223876953125e-08f * (sqrt_kp * st.y + s1c)          // 2^-25: subnormal lo parts
-                    + 9.313225746154785e-10f * (cnm + st.x)                      // 2^-30: extension parts
-                    + 1e-3f;
-    const bool cert = st.z != 0.f && (r_lo - w_hi) > 2.0f * E * 1.0001f;
-    if (cert) {
-      p.codes[n * p.stride + m] = (uint8_t)(16 * gi + qb);
-    } else {
-      flagged = true;
-      // candidates: every codeword whose exact distance can be <= the winner's, i.e. computed
-      // D_j <= W + 2 E (w_hi is some computed value >= the smallest one, also when negative
-      // words misorder as integers); all of them for rows outside the certified range
-      const float t0 = w_hi + 2.0f * E * 1.0001f;
-      const float t = t0 + fabsf(t0) * 1e-6f + 1e-30f;  // the sum rounded up
-      thr = (st.z != 0.f && t == t) ? t : __int_as_float(0x7f800000);
+  if (half == 1) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      ex4[i] = make_uint4((uint32_t)cls[4 * i], (uint32_t)cls[4 * i + 1], (uint32_t)cls[4 * i + 2],
+                          (uint32_t)cls[4 * i + 3]);
+    ex4[4] = make_uint4((uint32_t)G1, (uint32_t)G2, (uint32_t)gi, 0u);
+    pair_sync(bar);  // 1: partial minima of codewords [128, 256) visible to half 0
+    pair_sync(bar);  // 2: thresholds visible
+    thr = __uint_as_float(ex_row[0]);
+  } else {
+    pair_sync(bar);  // 1
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const uint4 o = ex4[i];
+      cls[4 * i] = min(cls[4 * i], (int)o.x);
+      cls[4 * i + 1] = min(cls[4 * i + 1], (int)o.y);
+      cls[4 * i + 2] = min(cls[4 * i + 2], (int)o.z);
+      cls[4 * i + 3] = min(cls[4 * i + 3], (int)o.w);
     }
-  }
-  // second pass over the accumulators for warps with an uncertified row: its candidate mask
-  uint32_t mw[kN / kChunk] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
-  if (__any_sync(0xffffffffu, flagged)) {
-#pragma unroll 1
-    for (int c = 0; c < kN / kChunk; ++c) {
-      tmem_ld32(tacc + (uint32_t)(c * kChunk), ka);
-      tmem_ld32(tacc + (uint32_t)(kN + c * kChunk), kb);
-      tmem_wait32(ka);
-      tmem_wait32(kb);
-      uint32_t word = 0;
-#pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        const float v = __fadd_rn(__uint_as_float(ka[j]), __uint_as_float(kb[j]));
-        word |= !(v > thr) ? (1u << j) : 0u;  // NaN counts as a candidate
+    {
+      // two sorted pairs of group minima merged (a tie between the halves' smallest leaves
+      // G2 = G1: never certifies; the lower group index wins as in the running fold)
+      const uint4 o = ex4[4];
+      const int h1 = (int)o.x, h2 = (int)o.y;
+      gi = h1 < G1 ? (int)o.z : gi;
+      G2 = min(max(G1, h1), min(G2, h2));
+      G1 = min(G1, h1);
+    }
+    if (n < p.n) {
+      int qb, Y;
+      class_best2(cls, p.keymask, p.one, qb, Y);
+      const int R = min(G2, Y);
+      const float w_hi = __int_as_float(G1), rv = __int_as_float(R);
+      const float r_lo = rv >= 0.f ? rv : rv * 1.00000762939453125f;
+      const float P = st.y * cb * 1.001f;
+      const float W = fminf(st.w, (float)(p.ks / 32) * P);  // every prefix (32-column chunks) is also <= P
+      const float E = eps_h * W + eps_l * P + eps_ext * (P + cnm + st.x) * 1.001f  //
+                      + 4.76837158203125e-07f * P                                 // 4 * 2^-23: split, lo.lo
+                      + 2.98023223876953125e-08f * (sqrt_kp * st.y + s1c)          // 2^-25: subnormal lo parts
+                      + 9.313225746154785e-10f * (cnm + st.x)                      // 2^-30: extension parts
+                      + 1e-3f;
+      const bool cert = st.z != 0.f && (r_lo - w_hi) > 2.0f * E * 1.0001f;
+      if (cert) {
+        p.codes[n * p.stride + m] = (uint8_t)(16 * gi + qb);
+      } else {
+        flagged = true;
+        // candidates: every codeword whose exact distance can be <= the winner's, i.e. computed
+        // D_j <= W + 2 E (w_hi is some computed value >= the smallest one, also when negative
+        // words misorder as integers); all of them for rows outside the certified range
+        const float t0 = w_hi + 2.0f * E * 1.0001f;
+        const float t = t0 + fabsf(t0) * 1e-6f + 1e-30f;  // the sum rounded up
+        thr = (st.z != 0.f && t == t) ? t : __int_as_float(0x7f800000);
       }
+    }
+    ex_row[0] = __float_as_uint(thr);
+    pair_sync(bar);  // 2
+  }
+  // candidate mask of this half's 128 codewords, for warps with an uncertified row: only
+  // the chunks holding a group minimum within the threshold are read again
+  uint32_t mw[4] = {0u, 0u, 0u, 0u};
+  const bool cand_row = thr != __int_as_float(0xff800000);
+  if (__any_sync(0xffffffffu, cand_row)) {
 #pragma unroll
-      for (int q = 0; q < kN / kChunk; ++q) mw[q] = (q == c) ? word : mw[q];
+    for (int cc = 0; cc < 4; ++cc) {
+      const bool need = cand_row && (!(__int_as_float(grp[2 * cc]) > thr) || !(__int_as_float(grp[2 * cc + 1]) > thr));
+      if (__any_sync(0xffffffffu, need)) {
+        load_sum32(tacc, 4 * half + cc, ka);
+        uint32_t word = 0;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) word |= !(__uint_as_float(ka[j]) > thr) ? (1u << j) : 0u;  // NaN: a candidate
+        mw[cc] = word;
+      }
     }
   }
   tc::fence_before();
+  if (half == 1) {
+    ex4[1] = make_uint4(mw[0], mw[1], mw[2], mw[3]);
+    __syncwarp();
+    if (lane == 0) {
+      arrive_at_issuer<kPair>(&tempty2[0]);
+      arrive_at_issuer<kPair>(&tempty2[1]);
+    }
+    pair_sync(bar);  // 3: mask words of codewords [128, 256) visible
+    return;
+  }
+  pair_sync(bar);  // 3
+  const uint4 mo = ex4[1];
+  // released only after the pair's shared-memory row was read: half 1 writes it again only
+  // behind the next item's accumulators, which wait for this arrive
   __syncwarp();
   if (lane == 0) {
-    mbar_arrive(&tempty2[0]);
-    mbar_arrive(&tempty2[1]);
+    arrive_at_issuer<kPair>(&tempty2[0]);
+    arrive_at_issuer<kPair>(&tempty2[1]);
   }
   if (flagged) {
     atomicAdd(&p.counters[0], 1u);
@@ -443,7 +550,7 @@ __device__ __forceinline__ void epilogue_row_split(const EncParams& p, int m, in
       p.flags[(size_t)m * p.flag_cap + f] = (uint32_t)n;
       uint4* dst = reinterpret_cast<uint4*>(p.tcmask + ((size_t)m * p.flag_cap + f) * 8);
       dst[0] = make_uint4(mw[0], mw[1], mw[2], mw[3]);
-      dst[1] = make_uint4(mw[4], mw[5], mw[6], mw[7]);
+      dst[1] = mo;
     } else {
       p.counters[1] = 1u;
     }
@@ -532,6 +639,8 @@ __global__ void __launch_bounds__(kThreadsR, 1) encode_tc_kernel(const __grid_co
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer ----------------
+    // (one lane runs the loop: electing a lane per item with the whole warp waiting, as in
+    // encode_tck_kernel, measured 1% slower here, the kernel being issue-bound)
     if (lane == 0) {
       // kMmaHalves: two N = 128 halves per accumulator, each released separately by the
       // epilogue (the next item's first half can run while the epilogue reads the second);
@@ -937,36 +1046,89 @@ __global__ void __launch_bounds__(256) encode_exact_kernel(const float* __restri
 // certificate and fallback are the same as encode_tc_kernel's (epilogue_row), with the
 // accumulation bound scaled by the instruction count (ks / 16 per pass).
 // ===========================================================================
+// timing-experiment switches of the K-streamed kernel (results are wrong when set):
+// 1 = B chunks copied only for the first ring round, 2 = hi . hi pass only, 4 = no transform
+// arithmetic / stores, 8 = no epilogue, 16 = X tiles loaded only for the first ring round
+#ifndef ENC_KEXP
+#define ENC_KEXP 0
+#endif
 constexpr int kKC = 32;
 constexpr int kMaxChunks = 32;  // ks <= 1024
-constexpr int kXSt = 3, kBSt = 3, kASt = 2;
+#ifndef ENC_KXST
+#define ENC_KXST 3
+#endif
+#ifndef ENC_KBST
+#define ENC_KBST 3
+#endif
+#ifndef ENC_KAST
+#define ENC_KAST 2
+#endif
+#ifndef ENC_KTRG
+#define ENC_KTRG 2
+#endif
+#ifndef ENC_KSPIN
+#define ENC_KSPIN 0
+#endif
+constexpr int kXSt = ENC_KXST, kBSt = ENC_KBST, kASt = ENC_KAST;  // ring depths: X tiles, B chunks, A chunks
+constexpr int kTrGroups = ENC_KTRG;                         // transform groups taking chunks in turn
+constexpr int kTrGroupWarps = kTrWarps / kTrGroups;         // warps per group
+constexpr int kTrPasses = kRows / (8 * kTrGroupWarps);      // 8-row passes per warp and chunk
+static_assert(kTrGroups == 1 || kTrGroups == 2, "transform groups");
+// the CTA pair variant's ring depths (half the B bytes per CTA leave room for deeper rings)
+#ifndef ENC_KPXST
+#define ENC_KPXST 3
+#endif
+#ifndef ENC_KPBST
+#define ENC_KPBST 3
+#endif
+#ifndef ENC_KPAST
+#define ENC_KPAST 2
+#endif
+#ifndef ENC_KPSEM
+#define ENC_KPSEM 1
+#endif
 
+// kPair: the CTA pair variant (cta_group::2): each CTA of a 2-CTA cluster keeps 128 of the
+// 256 codewords of every B chunk (half the B bytes written to and read from its shared
+// memory, the kernel's limiting resource) and its own 128-row tile of X / A.
+template <bool kPair>
 struct GeoK {
+  static constexpr int NB = kPair ? kN / 2 : kN;      // codewords held per CTA
+  static constexpr int XST = kPair ? ENC_KPXST : kXSt;  // ring depths: X tiles, B chunks, A chunks
+  static constexpr int BST = kPair ? ENC_KPBST : kBSt;
+  static constexpr int AST = kPair ? ENC_KPAST : kASt;
+  static_assert(2 * XST + 3 * BST + 2 * AST + 13 <= 48, "mbarrier slots");
   static constexpr int X_STAGE = kRows * kKC * 4;     // 16 KB (1024-aligned, swizzled)
-  static constexpr int B_HI = kN * kKC * 2;           // 16 KB
+  static constexpr int B_HI = NB * kKC * 2;           // 16 KB (pair: 8 KB)
   static constexpr int B_CHUNK = 2 * B_HI;            // hi + lo
-  static constexpr int B_EXT = kN * kExt * 2;         // 8 KB
+  static constexpr int B_EXT = NB * kExt * 2;         // 8 KB (pair: 4 KB)
+  static constexpr int GB_HI = kN * kKC * 2;          // prepared operands in global memory: all 256 codewords
+  static constexpr int GB_CHUNK = 2 * GB_HI;
+  static constexpr int GB_EXT = kN * kExt * 2;
   static constexpr int A_HI = kRows * kKC * 2;        // 8 KB
   static constexpr int A_CHUNK = 2 * A_HI;
   static constexpr int A_EXT = kRows * kExt * 2;      // 4 KB
   static constexpr int OFF_BEXT = 0;
   static constexpr int OFF_X = B_EXT;
-  static constexpr int OFF_B = OFF_X + kXSt * X_STAGE;
-  static constexpr int OFF_A = OFF_B + kBSt * B_CHUNK;
-  static constexpr int OFF_AEXT = OFF_A + kASt * A_CHUNK;
-  static constexpr int OFF_STATS = OFF_AEXT + 2 * A_EXT;
-  static constexpr int OFF_LO = OFF_STATS + 4 * kRows * 16;
-  static constexpr int OFF_CST = OFF_LO + kASt * kTrWarps * 4;
+  static constexpr int OFF_B = OFF_X + XST * X_STAGE;
+  static constexpr int OFF_A = OFF_B + BST * B_CHUNK;
+  static constexpr int OFF_AEXT = OFF_A + AST * A_CHUNK;
+  static constexpr int OFF_STATS = OFF_AEXT + A_EXT;          // one extension buffer (see the transform warps)
+  static constexpr int OFF_EX = OFF_STATS + 2 * kRows * 16;   // float4 [2][kRows] row stats
+  static constexpr int OFF_PART = OFF_EX + kRows * kExWords * 4;  // (epilogue warp pairs' hand-over rows)
+  static constexpr int OFF_LO = OFF_PART + 2 * kRows * 8;         // float2 [2][kRows]: group 1's row partials
+  static constexpr int OFF_CST = OFF_LO + AST * kTrWarps * 4;
   static constexpr int OFF_BCH = OFF_CST + CST_LEN * 4;   // float [kMaxChunks]
-  static constexpr int OFF_BAR = OFF_BCH + kMaxChunks * 4;  // uint64 [32]
-  static constexpr int OFF_TBASE = OFF_BAR + 32 * 8;
+  static constexpr int OFF_BAR = OFF_BCH + kMaxChunks * 4;  // uint64 [48]
+  static constexpr int OFF_TBASE = OFF_BAR + 48 * 8;
   static constexpr int SMEM = OFF_TBASE + 16 + 1024;
-  __host__ __device__ static size_t bprep_bytes(int ks) { return (size_t)(ks / kKC) * B_CHUNK + B_EXT; }
+  __host__ __device__ static size_t bprep_bytes(int ks) { return (size_t)(ks / kKC) * GB_CHUNK + GB_EXT; }
 };
 
+template <bool kPair>
 __global__ void __launch_bounds__(kThreads, 1) encode_tck_kernel(const __grid_constant__ CUtensorMap tmap,
                                                                 const EncParams p) {
-  using G = GeoK;
+  using G = GeoK<kPair>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sBext = smem + G::OFF_BEXT;
@@ -975,58 +1137,77 @@ __global__ void __launch_bounds__(kThreads, 1) encode_tck_kernel(const __grid_co
   uint8_t* sA = smem + G::OFF_A;
   uint8_t* sAext = smem + G::OFF_AEXT;
   float4* s_stats = reinterpret_cast<float4*>(smem + G::OFF_STATS);
+  uint32_t* s_ex = reinterpret_cast<uint32_t*>(smem + G::OFF_EX);
+  float2* s_part = reinterpret_cast<float2*>(smem + G::OFF_PART);
   int* s_lo = reinterpret_cast<int*>(smem + G::OFF_LO);
   float* s_cst = reinterpret_cast<float*>(smem + G::OFF_CST);
   float* s_bch = reinterpret_cast<float*>(smem + G::OFF_BCH);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + G::OFF_BAR);
-  uint64_t* xfull = bars;         // [3]
-  uint64_t* xempty = bars + 3;    // [3]
-  uint64_t* bfull = bars + 6;     // [3]
-  uint64_t* bempty = bars + 9;    // [3]
-  uint64_t* afull = bars + 12;    // [2]
-  uint64_t* aempty = bars + 14;   // [2]
-  uint64_t* aefull = bars + 16;   // [2] extension rows of A, per accumulator
-  uint64_t* aeempty = bars + 18;  // [2]
-  uint64_t* tfull = bars + 20;    // [2][2]
-  uint64_t* tempty = bars + 24;   // [2][2]
-  uint64_t* bload = bars + 28;
+  uint64_t* xfull = bars;                 // [G::XST]
+  uint64_t* xempty = xfull + G::XST;        // [G::XST]
+  uint64_t* bfull = xempty + G::XST;        // [G::BST]
+  uint64_t* bempty = bfull + G::BST;        // [G::BST]
+  uint64_t* afull = bempty + G::BST;        // [G::AST]
+  uint64_t* aempty = afull + G::AST;        // [G::AST]
+  uint64_t* aefull = aempty + G::AST;       // [2] extension rows of A
+  uint64_t* aeempty = aefull + 2;         // [2]
+  uint64_t* tfull = aeempty + 2;          // [2][2]
+  uint64_t* tempty = tfull + 4;           // [2][2]
+  uint64_t* bload = tempty + 4;
+  uint64_t* bpeer = bload + 1;            // [G::BST] pair: the peer CTA's half of a B chunk has landed
   uint32_t* s_tbase = reinterpret_cast<uint32_t*>(smem + G::OFF_TBASE);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int m = (int)blockIdx.x % p.m;
-  const int t0 = (int)blockIdx.x / p.m;
-  const int items = t0 < p.ntiles ? (p.ntiles - t0 + p.tstride - 1) / p.tstride : 0;
+  // pair: the two CTAs of a cluster take the two 128-row tiles of a tile pair of one subspace;
+  // tstride counts tile pairs, both CTAs run the same number of items (a missing last tile
+  // loads zeros past the end of X and stores nothing)
+  const int cr = kPair ? (int)tc::cluster_rank() : 0;
+  const int gid = kPair ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+  const int m = gid % p.m;
+  const int t0 = gid / p.m;
+  const int ntl = kPair ? (p.ntiles + 1) >> 1 : p.ntiles;
+  const int items = t0 < ntl ? (ntl - t0 + p.tstride - 1) / p.tstride : 0;
+  const int nsig = kPair ? 2 : 1;  // CTAs signalling the issuer's barriers
   const int ks = p.ks, nk = ks / kKC;
   const uint8_t* bprep = p.bprep + (size_t)m * G::bprep_bytes(ks);
 
   if (tid == 0) {
-    for (int i = 0; i < 3; ++i) {
+    for (int i = 0; i < G::XST; ++i) {
       mbar_init(&xfull[i], 1);
-      mbar_init(&xempty[i], kTrWarps);
+      mbar_init(&xempty[i], kTrGroupWarps);
+    }
+    for (int i = 0; i < G::BST; ++i) {
       mbar_init(&bfull[i], 1);
       mbar_init(&bempty[i], 1);
+      mbar_init(&bpeer[i], 1);
+    }
+    for (int i = 0; i < G::AST; ++i) {
+      mbar_init(&afull[i], nsig * kTrGroupWarps);
+      mbar_init(&aempty[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
-      mbar_init(&afull[i], kTrWarps);
-      mbar_init(&aempty[i], 1);
-      mbar_init(&aefull[i], kTrWarps);
+      mbar_init(&aefull[i], nsig * kTrGroupWarps);
       mbar_init(&aeempty[i], 1);
     }
     for (int i = 0; i < 4; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], kEpiWarps / 2);
+      mbar_init(&tempty[i], nsig * kEpiWarps);
     }
     mbar_init(bload, 1);
     fence_mbar_init();
   }
-  if (warp == 1) tc::tmem_alloc(s_tbase, 512);
+  if (warp == 1) {
+    if (kPair) tc::tmem_alloc_pair(s_tbase, 512);
+    else tc::tmem_alloc(s_tbase, 512);
+  }
   tc::fence_before();
   __syncthreads();
+  if (kPair) tc::cluster_sync();  // both CTAs' barriers initialised before any remote arrive / multicast commit
   tc::fence_after();
   const uint32_t tbase = *s_tbase;
   if (tid == 0) {
     mbar_arrive_expect_tx(bload, (uint32_t)G::B_EXT + CST_LEN * 4 + kMaxChunks * 4);
-    bulk_g2s(sBext, bprep + (size_t)nk * G::B_CHUNK, G::B_EXT, bload);
+    bulk_g2s(sBext, bprep + (size_t)nk * G::GB_CHUNK + (size_t)cr * G::B_EXT, G::B_EXT, bload);
     bulk_g2s(s_cst, p.cst + (size_t)m * CST_LEN, CST_LEN * 4, bload);
     bulk_g2s(s_bch, p.bch + (size_t)m * kMaxChunks, kMaxChunks * 4, bload);
   }
@@ -1038,14 +1219,28 @@ __global__ void __launch_bounds__(kThreads, 1) encode_tck_kernel(const __grid_co
     if (lane == 0) {
       for (int g = 0; g < nchunks; ++g) {
         const int w = g / nk, c = g - w * nk;
-        const int t = t0 + w * p.tstride;
-        const int xs = g % kXSt, bs = g % kBSt;
-        mbar_wait(&xempty[xs], (uint32_t)(((g / kXSt) & 1) ^ 1));
-        mbar_arrive_expect_tx(&xfull[xs], (uint32_t)G::X_STAGE);
-        tma_load_2d(sX + xs * G::X_STAGE, &tmap, m * ks + c * kKC, t * kRows, &xfull[xs]);
-        mbar_wait(&bempty[bs], (uint32_t)(((g / kBSt) & 1) ^ 1));
-        mbar_arrive_expect_tx(&bfull[bs], (uint32_t)G::B_CHUNK);
-        bulk_g2s(sB + bs * G::B_CHUNK, bprep + (size_t)c * G::B_CHUNK, G::B_CHUNK, &bfull[bs]);
+        const int t = kPair ? 2 * (t0 + w * p.tstride) + cr : t0 + w * p.tstride;
+        const int xs = g % G::XST, bs = g % G::BST;
+        mbar_wait(&xempty[xs], (uint32_t)(((g / G::XST) & 1) ^ 1));
+        if ((ENC_KEXP & 16) && g >= G::XST) {
+          mbar_arrive(&xfull[xs]);
+        } else {
+          mbar_arrive_expect_tx(&xfull[xs], (uint32_t)G::X_STAGE);
+          tma_load_2d(sX + xs * G::X_STAGE, &tmap, m * ks + c * kKC, t * kRows, &xfull[xs]);
+        }
+        mbar_wait(&bempty[bs], (uint32_t)(((g / G::BST) & 1) ^ 1));
+        if ((ENC_KEXP & 1) && g >= G::BST) {
+          mbar_arrive(&bfull[bs]);
+        } else {
+          mbar_arrive_expect_tx(&bfull[bs], (uint32_t)G::B_CHUNK);
+          if (kPair) {  // this CTA's 128 codewords of the hi and of the lo block
+            const uint8_t* src = bprep + (size_t)c * G::GB_CHUNK + (size_t)cr * G::B_HI;
+            bulk_g2s(sB + bs * G::B_CHUNK, src, G::B_HI, &bfull[bs]);
+            bulk_g2s(sB + bs * G::B_CHUNK + G::B_HI, src + G::GB_HI, G::B_HI, &bfull[bs]);
+          } else {
+            bulk_g2s(sB + bs * G::B_CHUNK, bprep + (size_t)c * G::GB_CHUNK, G::B_CHUNK, &bfull[bs]);
+          }
+        }
       }
     }
   } else if (warp == 1) {
@@ -1053,56 +1248,85 @@ __global__ void __launch_bounds__(kThreads, 1) encode_tck_kernel(const __grid_co
     // One item in flight: accumulator H = TMEM columns [0, 256) takes hi . hi and the
     // extension block, L = [256, 512) the lo passes, so that the lo passes' truncation
     // errors scale with L's small magnitude, and H's with its running prefix.
-    if (lane == 0) {
-      const uint32_t idesc = tc::idesc_f16_f32(kRows, kN);
+    if (kPair && cr == 1) {
+      // the peer CTA issues nothing: this lane reports each landed B half to rank 0
+      if (lane == 0) {
+        for (int g = 0; g < nchunks; ++g) {
+          const int bs = g % G::BST;
+          mbar_wait(&bfull[bs], (uint32_t)((g / G::BST) & 1));
+          tc::mbar_arrive_rank0(&bpeer[bs]);
+        }
+      }
+    } else {
+      // The whole warp runs the loop and one elected lane issues: inside a lane == 0 branch
+      // ptxas wraps every tcgen05 instruction (uniform-register operands) in a loop over the
+      // active lanes, ~140 dependent instructions per chunk on the issuing thread
+      auto mma = [](uint32_t d, uint64_t da, uint64_t db, uint32_t id, uint32_t acc) {
+        if (kPair) tc::mma_f16_pair(d, da, db, id, acc);
+        else tc::mma_f16(d, da, db, id, acc);
+      };
+      auto commit = [](uint64_t* bar) {
+        if (kPair) tc::commit_pair(bar);
+        else tc::commit(bar);
+      };
+      auto wait = [](uint64_t* bar, uint32_t par) {
+        if (kPair) tc::mbar_wait_spin_cluster(bar, par);
+        else mbar_wait_spin(bar, par);
+      };
+      const uint32_t idesc = tc::idesc_f16_f32(kPair ? 2 * kRows : kRows, kN);
       constexpr uint32_t sboC = (uint32_t)(kKC / 8) * 128, sboE = (uint32_t)(kExt / 8) * 128;
       const uint32_t tH = tbase, tL = tbase + (uint32_t)kN;
       for (int w = 0; w < items; ++w) {
-        const int ab = w & 1;
         const uint32_t ph = (uint32_t)(w & 1);
-        mbar_wait_spin(&tempty[0], ph ^ 1u);
-        mbar_wait_spin(&tempty[1], ph ^ 1u);
+        wait(&tempty[0], ph ^ 1u);
+        wait(&tempty[1], ph ^ 1u);
         for (int c = 0; c < nk; ++c) {
           const int g = w * nk + c;
-          const int as = g % kASt, bs = g % kBSt;
-          mbar_wait_spin(&afull[as], (uint32_t)((g / kASt) & 1));
-          mbar_wait_spin(&bfull[bs], (uint32_t)((g / kBSt) & 1));
+          const int as = g % G::AST, bs = g % G::BST;
+          wait(&afull[as], (uint32_t)((g / G::AST) & 1));
+          mbar_wait_spin(&bfull[bs], (uint32_t)((g / G::BST) & 1));
+          if (kPair) wait(&bpeer[bs], (uint32_t)((g / G::BST) & 1));
           tc::fence_after();
-          int lo_any = 0;
+          int lo_any = kPair ? 1 : 0;  // pair: the lo . hi pass always runs (no flags from the peer CTA)
 #pragma unroll
-          for (int j = 0; j < kTrWarps; ++j) lo_any |= s_lo[as * kTrWarps + j];
+          for (int j = 0; j < kTrGroupWarps; ++j) lo_any |= s_lo[as * kTrWarps + j];
+          if (elect_one()) {
           const uint32_t a_hi = smem_u32(sA + as * G::A_CHUNK), a_lo = a_hi + G::A_HI;
           const uint32_t b_hi = smem_u32(sB + bs * G::B_CHUNK), b_lo = b_hi + G::B_HI;
 #pragma unroll
-          for (int s = 0; s < kKC / 16; ++s)
-            tc::mma_f16(tL, tc::smem_desc(a_hi + s * 256, 128, sboC), tc::smem_desc(b_lo + s * 256, 128, sboC), idesc,
-                        (c > 0 || s > 0) ? 1u : 0u);
-          if (lo_any) {
+          for (int s = 0; s < ((ENC_KEXP & 2) ? (c == 0 ? 1 : 0) : kKC / 16); ++s)
+            mma(tL, tc::smem_desc(a_hi + s * 256, 128, sboC), tc::smem_desc(b_lo + s * 256, 128, sboC), idesc,
+                (c > 0 || s > 0) ? 1u : 0u);
+          if (lo_any && !(ENC_KEXP & 2)) {
 #pragma unroll
             for (int s = 0; s < kKC / 16; ++s)
-              tc::mma_f16(tL, tc::smem_desc(a_lo + s * 256, 128, sboC), tc::smem_desc(b_hi + s * 256, 128, sboC),
-                          idesc, 1u);
+              mma(tL, tc::smem_desc(a_lo + s * 256, 128, sboC), tc::smem_desc(b_hi + s * 256, 128, sboC), idesc, 1u);
           }
 #pragma unroll
           for (int s = 0; s < kKC / 16; ++s)
-            tc::mma_f16(tH, tc::smem_desc(a_hi + s * 256, 128, sboC), tc::smem_desc(b_hi + s * 256, 128, sboC), idesc,
-                        (c > 0 || s > 0) ? 1u : 0u);
-          tc::commit(&aempty[as]);
-          tc::commit(&bempty[bs]);
+            mma(tH, tc::smem_desc(a_hi + s * 256, 128, sboC), tc::smem_desc(b_hi + s * 256, 128, sboC), idesc,
+                (c > 0 || s > 0) ? 1u : 0u);
+          commit(&aempty[as]);
+          commit(&bempty[bs]);
+          }
+          __syncwarp();
         }
-        mbar_wait_spin(&aefull[ab], (uint32_t)((w >> 1) & 1));
+        wait(&aefull[0], ph);
         tc::fence_after();
-        tc::mma_f16(tH, tc::smem_desc(smem_u32(sAext + ab * G::A_EXT), 128, sboE),
-                    tc::smem_desc(smem_u32(sBext), 128, sboE), idesc, 1u);
-        tc::commit(&aeempty[ab]);
-        tc::commit(&tfull[0]);
-        tc::commit(&tfull[1]);
+        if (elect_one()) {
+          mma(tH, tc::smem_desc(smem_u32(sAext), 128, sboE), tc::smem_desc(smem_u32(sBext), 128, sboE), idesc, 1u);
+          commit(&aeempty[0]);
+          commit(&tfull[0]);
+          commit(&tfull[1]);
+        }
+        __syncwarp();
       }
     }
   } else if (warp < 2 + kEpiWarps) {
-    // ---------------- epilogue warps (one item at a time: warps 2-5) ----------------
+    // ---------------- epilogue warps: two per TMEM lane quadrant (128 codewords each) ----------------
     const int ew = warp - 2;
     const int q = warp & 3;
+    const int half = ew >> 2;
     const int er = 32 * q + lane;
     // H: two hi . hi instructions per chunk with max |addend| <= the row's running prefix
     // (sum W over chunks, st.w); L: 4 nk instructions with addends <= 2^-9 P
@@ -1112,36 +1336,152 @@ __global__ void __launch_bounds__(kThreads, 1) encode_tck_kernel(const __grid_co
     const float eps_ext = 7.5f * 1.1920928955078125e-07f;
     const float cb = s_cst[CST_CB], cnm = s_cst[CST_CN], s1c = s_cst[CST_S1C];
     const float sqrt_ks = sqrtf((float)ks);
-    if (ew < 4) {
-      for (int w = 0; w < items; ++w) {
-        const int t = t0 + w * p.tstride;
-        mbar_wait(&tfull[0], (uint32_t)(w & 1));
-        tc::fence_after();
-        const float4 st = s_stats[(w & 3) * kRows + er];
-        const uint32_t tacc = tbase + ((uint32_t)(32 * q) << 16);
-        epilogue_row_split(p, m, (int64_t)t * kRows + er, tacc, tempty, st, eps_h, eps_l, eps_ext, cb, cnm, s1c,
-                           sqrt_ks, lane);
+    for (int w = 0; w < items; ++w) {
+      const int t = kPair ? 2 * (t0 + w * p.tstride) + cr : t0 + w * p.tstride;
+      mbar_wait(&tfull[0], (uint32_t)(w & 1));
+      tc::fence_after();
+      const float4 st = s_stats[(w & 1) * kRows + er];
+      const uint32_t tacc = tbase + ((uint32_t)(32 * q) << 16);
+      if (ENC_KEXP & 8) {
+        tc::fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          arrive_at_issuer<kPair>(&tempty[0]);
+          arrive_at_issuer<kPair>(&tempty[1]);
+        }
+        if (st.x == 123.456f) p.codes[((int64_t)t * kRows + er) * p.stride + m] = 0;
+        continue;
       }
+      epilogue_row_split<kPair>(p, m, (int64_t)t * kRows + er, tacc, tempty, st, eps_h, eps_l, eps_ext, cb, cnm, s1c, sqrt_ks,
+                         lane, half, s_ex + er * kExWords, 1 + q);
     }
   } else {
-    // ---------------- transform warps: 16 rows each (2 passes of 8), 8 columns per lane ----------------
+    // ---------------- transform warps ----------------
+    // kTrGroups groups of kTrGroupWarps warps take the chunks in turn, kTrPasses passes of 8
+    // rows per warp (8 columns per lane).  With two groups a chunk's chain (X tile ->
+    // registers -> fp16 split -> wait for the A stage -> stores -> proxy fence) may take two
+    // chunk times, and each lane carries four independent rows through it.
     const int tw = warp - 2 - kEpiWarps;
+    const int grp = tw / kTrGroupWarps, twg = tw % kTrGroupWarps;
+    if constexpr (kTrGroups == 2) {
+      // one lane per row (32 rows per warp, 4 warps per chunk, the two groups alternate over
+      // the chunks): no cross-lane sums, eight independent 16-byte column groups per lane
+      const int r = 32 * twg + lane;
+      const float sc = s_cst[CST_S];
+      const __half acn = __float2half_rn(s_cst[CST_ACN]);
+      const bool valid = s_cst[CST_VALID] != 0.f;
+      const uint32_t arow = (uint32_t)((r >> 3) * (kKC / 8) * 128 + (r & 7) * 16);  // kmajor_off(r, 0, kKC)
+      int g = grp;
+      for (int w = 0; w < items; ++w) {
+        float x2 = 0.f, wsum = 0.f;
+        const int gend = (w + 1) * nk;
+        for (; g < gend; g += 2) {
+          const int c = g - w * nk;
+          const int xs = g % G::XST, as = g % G::AST;
+          const uint32_t aph = (uint32_t)((g / G::AST) & 1);
+          mbar_wait(&xfull[xs], (uint32_t)((g / G::XST) & 1));
+          const uint8_t* xb = sX + xs * G::X_STAGE + r * 128;
+          uint32_t hw[16], lw[16];
+          uint32_t lo_nz = 0;
+          float ec = 0.f;
+#pragma unroll
+          for (int ch = 0; ch < 8; ++ch) {
+            const float4 f = *reinterpret_cast<const float4*>(xb + ((ch ^ (r & 7)) << 4));
+            const float a0 = f.x * sc, a1 = f.y * sc, a2 = f.z * sc, a3 = f.w * sc;
+            const __half2 h01 = __floats2half2_rn(a0, a1), h23 = __floats2half2_rn(a2, a3);
+            const float2 f01 = __half22float2(h01), f23 = __half22float2(h23);
+            const __half2 l01 = __floats2half2_rn(a0 - f01.x, a1 - f01.y);
+            const __half2 l23 = __floats2half2_rn(a2 - f23.x, a3 - f23.y);
+            hw[2 * ch] = *reinterpret_cast<const uint32_t*>(&h01);
+            hw[2 * ch + 1] = *reinterpret_cast<const uint32_t*>(&h23);
+            lw[2 * ch] = *reinterpret_cast<const uint32_t*>(&l01);
+            lw[2 * ch + 1] = *reinterpret_cast<const uint32_t*>(&l23);
+            lo_nz |= lw[2 * ch] | lw[2 * ch + 1];
+            ec = fmaf(a0, a0, fmaf(a1, a1, fmaf(a2, a2, fmaf(a3, a3, ec))));
+          }
+          x2 += ec;
+          // the row's chunk norm rounded up, times max_j |B_j,c|, counted for the nk - c prefixes holding it
+          wsum = fmaf(sqrtf(ec), (float)(nk - c) * s_bch[c] * 1.000001f, wsum);
+          const unsigned bal = __ballot_sync(0xffffffffu, (lo_nz & 0x7fff7fffu) != 0);
+          // released after the loaded values were consumed (see encode_tc_kernel's transform)
+          if (lane == 0) mbar_arrive(&xempty[xs]);
+          if (ENC_KSPIN) mbar_wait_spin(&aempty[as], aph ^ 1u);
+          else mbar_wait(&aempty[as], aph ^ 1u);
+          uint8_t* ahi = sA + as * G::A_CHUNK + arow;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            *reinterpret_cast<uint4*>(ahi + j * 128) = make_uint4(hw[4 * j], hw[4 * j + 1], hw[4 * j + 2], hw[4 * j + 3]);
+            *reinterpret_cast<uint4*>(ahi + G::A_HI + j * 128) =
+                make_uint4(lw[4 * j], lw[4 * j + 1], lw[4 * j + 2], lw[4 * j + 3]);
+          }
+          if (lane == 0) s_lo[as * kTrWarps + twg] = (bal != 0);
+          tc::fence_proxy_async();
+          __syncwarp();
+          if (lane == 0) arrive_at_issuer<kPair>(&afull[as]);
+        }
+        // group 1 hands its row partials to group 0, which writes the extension rows and stats
+        if (grp == 1) s_part[(w & 1) * kRows + r] = make_float2(x2, wsum);
+        asm volatile("bar.sync 5, %0;" ::"n"(kTrWarps * 32) : "memory");
+        if (grp == 1) continue;
+        mbar_wait(&aeempty[0], (uint32_t)((w & 1) ^ 1));
+        {
+          const float2 o = s_part[(w & 1) * kRows + r];
+          const float acc = x2 + o.x;
+          // |s x|^2 rounded up: fp32 sums of ks products (relative error < (ks + 4) 2^-24)
+          const float x2u = acc * (1.0f + (float)(ks + 16) * 5.9604644775390625e-08f);
+          const bool ok = valid && (x2u < kX2Limit);
+          const float xv = ok ? x2u * 3.0517578125e-05f : 0.f;
+          const __half x_h = __float2half_rn(xv);
+          const float r1 = xv - __half2float(x_h);
+          const __half x_m = __float2half_rn(r1);
+          const __half x_l = __float2half_rn(r1 - __half2float(x_m));
+          const __half p15 = __float2half_rn(32768.f);
+          const __half z = __float2half_rn(0.f);
+          uint8_t* ae = sAext;
+          *reinterpret_cast<uint4*>(ae + tc::kmajor_off(r, 0, kExt)) =
+              make_uint4(pack_h2(acn, acn), pack_h2(acn, x_h), pack_h2(x_m, x_l), pack_h2(p15, z));
+          *reinterpret_cast<uint4*>(ae + tc::kmajor_off(r, 8, kExt)) = make_uint4(0u, 0u, 0u, 0u);
+          float xn;
+          asm("sqrt.approx.f32 %0, %1;" : "=f"(xn) : "f"(x2u));
+          // w: the prefix bound with the hi/lo split's (1 + 2^-11)^2 and fp32 sum slack
+          s_stats[(w & 1) * kRows + r] = make_float4(x2u, xn * 1.000002f, ok ? 1.f : 0.f, (wsum + o.y) * 1.002f);
+        }
+        tc::fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) arrive_at_issuer<kPair>(&aefull[0]);
+      }
+    } else {
     const int th = lane >> 3;  // 4 lanes per row: lanes r, r+8, r+16, r+24
     const float sc = s_cst[CST_S];
     const __half acn = __float2half_rn(s_cst[CST_ACN]);
     const bool valid = s_cst[CST_VALID] != 0.f;
+    int g = grp;  // next chunk of this group, counted over all items
     for (int w = 0; w < items; ++w) {
-      float x2[2] = {0.f, 0.f};
-      float wpre[2] = {0.f, 0.f}, run[2] = {0.f, 0.f};  // prefix bound: sum_c sum_{c'<=c} |x_c'| B_c'
-      uint32_t lo_row[2] = {0u, 0u};
-      for (int c = 0; c < nk; ++c) {
-        const int g = w * nk + c;
-        const int xs = g % kXSt, as = g % kASt;
-        mbar_wait(&xfull[xs], (uint32_t)((g / kXSt) & 1));
-        float v[2][8];
+      // row partials over this group's chunks: |s x|^2 and the prefix bound
+      // sum_c sum_{c'<=c} |x_c'| B_c' = sum_c' |x_c'| B_c' (nk - c')
+      float x2[kTrPasses], wsum[kTrPasses];
 #pragma unroll
-        for (int ps = 0; ps < 2; ++ps) {
-          const int r = 16 * tw + 8 * ps + (lane & 7);
+      for (int ps = 0; ps < kTrPasses; ++ps) x2[ps] = wsum[ps] = 0.f;
+      const int gend = (w + 1) * nk;
+      for (; g < gend; g += kTrGroups) {
+        const int c = g - w * nk;
+        const int xs = g % G::XST, as = g % G::AST;
+        const uint32_t aph = (uint32_t)((g / G::AST) & 1);
+        mbar_wait(&xfull[xs], (uint32_t)((g / G::XST) & 1));
+        if (ENC_KEXP & 4) {
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&xempty[xs]);
+          mbar_wait(&aempty[as], aph ^ 1u);
+          if (lane == 0) s_lo[as * kTrWarps + twg] = 1;
+          tc::fence_proxy_async();
+          __syncwarp();
+          if (lane == 0) arrive_at_issuer<kPair>(&afull[as]);
+          continue;
+        }
+        float v[kTrPasses][8];
+#pragma unroll
+        for (int ps = 0; ps < kTrPasses; ++ps) {
+          const int r = 8 * kTrPasses * twg + 8 * ps + (lane & 7);
           const uint8_t* xb = sX + xs * G::X_STAGE + r * 128;
 #pragma unroll
           for (int cc = 0; cc < 2; ++cc) {
@@ -1153,11 +1493,11 @@ __global__ void __launch_bounds__(kThreads, 1) encode_tck_kernel(const __grid_co
             v[ps][4 * cc + 3] = f.w;
           }
         }
-        uint32_t hw[2][4], lw[2][4];
+        uint32_t hw[kTrPasses][4], lw[kTrPasses][4];
         uint32_t lo_nz = 0;
+        const float wc = (float)(nk - c) * s_bch[c] * 1.000001f;
 #pragma unroll
-        for (int ps = 0; ps < 2; ++ps) {
-          uint32_t lr = 0;
+        for (int ps = 0; ps < kTrPasses; ++ps) {
           float ec = 0.f;
 #pragma unroll
           for (int j = 0; j < 8; j += 2) {
@@ -1167,50 +1507,59 @@ __global__ void __launch_bounds__(kThreads, 1) encode_tck_kernel(const __grid_co
             const __half2 ll = __floats2half2_rn(a0 - hf.x, a1 - hf.y);
             hw[ps][j / 2] = *reinterpret_cast<const uint32_t*>(&hh);
             lw[ps][j / 2] = *reinterpret_cast<const uint32_t*>(&ll);
-            lr |= lw[ps][j / 2];
+            lo_nz |= lw[ps][j / 2];
             ec = fmaf(a0, a0, fmaf(a1, a1, ec));
           }
           x2[ps] += ec;
           // the row's chunk energy (4 lanes per row), its norm rounded up, times max_j |B_j,c|
           ec += __shfl_xor_sync(0xffffffffu, ec, 8);
           ec += __shfl_xor_sync(0xffffffffu, ec, 16);
-          run[ps] = fmaf(sqrtf(ec) * 1.000001f, s_bch[c], run[ps]);
-          wpre[ps] += run[ps];
-          lr &= 0x7fff7fffu;
-          lo_row[ps] |= lr;
-          lo_nz |= lr;
+          wsum[ps] = fmaf(sqrtf(ec), wc, wsum[ps]);
         }
-        const unsigned bal = __ballot_sync(0xffffffffu, lo_nz != 0);
+        const unsigned bal = __ballot_sync(0xffffffffu, (lo_nz & 0x7fff7fffu) != 0);
         // released after the loaded values were consumed (an arrive issued right behind the
         // loads is not ordered after their completion: see encode_tc_kernel's transform)
         if (lane == 0) mbar_arrive(&xempty[xs]);
-        mbar_wait(&aempty[as], (uint32_t)(((g / kASt) & 1) ^ 1));
+        if (ENC_KSPIN) mbar_wait_spin(&aempty[as], aph ^ 1u);
+        else mbar_wait(&aempty[as], aph ^ 1u);
         uint8_t* ahi = sA + as * G::A_CHUNK;
 #pragma unroll
-        for (int ps = 0; ps < 2; ++ps) {
-          const int r = 16 * tw + 8 * ps + (lane & 7);
+        for (int ps = 0; ps < kTrPasses; ++ps) {
+          const int r = 8 * kTrPasses * twg + 8 * ps + (lane & 7);
           *reinterpret_cast<uint4*>(ahi + tc::kmajor_off(r, 8 * th, kKC)) =
               make_uint4(hw[ps][0], hw[ps][1], hw[ps][2], hw[ps][3]);
           *reinterpret_cast<uint4*>(ahi + G::A_HI + tc::kmajor_off(r, 8 * th, kKC)) =
               make_uint4(lw[ps][0], lw[ps][1], lw[ps][2], lw[ps][3]);
         }
-        if (lane == 0) s_lo[as * kTrWarps + tw] = (bal != 0);
+        if (lane == 0) s_lo[as * kTrWarps + twg] = (bal != 0);
         tc::fence_proxy_async();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&afull[as]);
+        if (lane == 0) arrive_at_issuer<kPair>(&afull[as]);
       }
-      // extension rows and stats of the item (whole-row |s x|^2 now known)
-      const int ab = w & 1;
-      mbar_wait(&aeempty[ab], (uint32_t)(((w >> 1) & 1) ^ 1));
+      // the item's rows: group 1 hands its partials to group 0, which writes the extension
+      // rows and the stats (whole-row |s x|^2 now known)
 #pragma unroll
-      for (int ps = 0; ps < 2; ++ps) {
-        float acc = x2[ps];
-        acc += __shfl_xor_sync(0xffffffffu, acc, 8);
-        acc += __shfl_xor_sync(0xffffffffu, acc, 16);
-        uint32_t lr = lo_row[ps];
-        lr |= __shfl_xor_sync(0xffffffffu, lr, 8);
-        lr |= __shfl_xor_sync(0xffffffffu, lr, 16);
-        const int r = 16 * tw + 8 * ps + (lane & 7);
+      for (int ps = 0; ps < kTrPasses; ++ps) {
+        x2[ps] += __shfl_xor_sync(0xffffffffu, x2[ps], 8);
+        x2[ps] += __shfl_xor_sync(0xffffffffu, x2[ps], 16);
+      }
+      if (kTrGroups == 2) {
+        if (grp == 1 && th == 0) {
+#pragma unroll
+          for (int ps = 0; ps < kTrPasses; ++ps)
+            s_part[(w & 1) * kRows + 8 * kTrPasses * twg + 8 * ps + (lane & 7)] = make_float2(x2[ps], wsum[ps]);
+        }
+        asm volatile("bar.sync 5, %0;" ::"n"(kTrWarps * 32) : "memory");
+        if (grp == 1) continue;
+      }
+      // one extension buffer: the previous item's extension instruction has completed long
+      // before this item's last chunks could be stored (A ring of 2 behind the in-order MMAs)
+      mbar_wait(&aeempty[0], (uint32_t)((w & 1) ^ 1));
+#pragma unroll
+      for (int ps = 0; ps < kTrPasses; ++ps) {
+        const int r = 8 * kTrPasses * twg + 8 * ps + (lane & 7);
+        const float2 o = kTrGroups == 2 ? s_part[(w & 1) * kRows + r] : make_float2(0.f, 0.f);
+        const float acc = x2[ps] + o.x;
         // |s x|^2 rounded up: fp32 sums of ks products (relative error < (ks + 4) 2^-24)
         const float x2u = acc * (1.0f + (float)(ks + 16) * 5.9604644775390625e-08f);
         const bool ok = valid && (x2u < kX2Limit);
@@ -1222,26 +1571,30 @@ __global__ void __launch_bounds__(kThreads, 1) encode_tck_kernel(const __grid_co
           const __half x_l = __float2half_rn(r1 - __half2float(x_m));
           const __half p15 = __float2half_rn(32768.f);
           const __half z = __float2half_rn(0.f);
-          uint8_t* ae = sAext + ab * G::A_EXT;
+          uint8_t* ae = sAext;
           *reinterpret_cast<uint4*>(ae + tc::kmajor_off(r, 0, kExt)) =
               make_uint4(pack_h2(acn, acn), pack_h2(acn, x_h), pack_h2(x_m, x_l), pack_h2(p15, z));
           *reinterpret_cast<uint4*>(ae + tc::kmajor_off(r, 8, kExt)) = make_uint4(0u, 0u, 0u, 0u);
           float xn;
           asm("sqrt.approx.f32 %0, %1;" : "=f"(xn) : "f"(x2u));
           // w: the prefix bound with the hi/lo split's (1 + 2^-11)^2 and fp32 sum slack
-          s_stats[(w & 3) * kRows + r] = make_float4(x2u, xn * 1.000002f, ok ? 1.f : 0.f, wpre[ps] * 1.002f);
+          s_stats[(w & 1) * kRows + r] =
+              make_float4(x2u, xn * 1.000002f, ok ? 1.f : 0.f, (wsum[ps] + o.y) * 1.002f);
         }
       }
       tc::fence_proxy_async();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&aefull[ab]);
+      if (lane == 0) arrive_at_issuer<kPair>(&aefull[0]);
+    }
     }
   }
   tc::fence_before();
   __syncthreads();
+  if (kPair) tc::cluster_sync();  // no CTA leaves (or frees TMEM) while its peer can still signal it
   if (warp == 1) {
     tc::fence_after();
-    tc::tmem_dealloc(tbase, 512);
+    if (kPair) tc::tmem_dealloc_pair(tbase, 512);
+    else tc::tmem_dealloc(tbase, 512);
   }
 }
 
@@ -1310,7 +1663,7 @@ __global__ void __launch_bounds__(256) encode_prep_k_kernel(const float* __restr
   __syncthreads();
   const float sc = s_sc;
   const bool cb_ok = !s_bad;
-  uint8_t* base = bprep + (size_t)mm * GeoK::bprep_bytes(ks);
+  uint8_t* base = bprep + (size_t)mm * GeoK<false>::bprep_bytes(ks);
   if (row < kMaxChunks) s_bmax[row] = 0u;
   __syncthreads();
   double cn = 0.0, nb2 = 0.0, s1 = 0.0, nbc = 0.0;
@@ -1319,9 +1672,9 @@ __global__ void __launch_bounds__(256) encode_prep_k_kernel(const float* __restr
     const float bv = -2.0f * cv;
     const __half hi = __float2half_rn(bv);
     const __half lo = __float2half_rn(bv - __half2float(hi));
-    uint8_t* chunk = base + (size_t)(k / kKC) * GeoK::B_CHUNK;
+    uint8_t* chunk = base + (size_t)(k / kKC) * GeoK<false>::GB_CHUNK;
     *reinterpret_cast<__half*>(chunk + tc::kmajor_off(row, k % kKC, kKC)) = hi;
-    *reinterpret_cast<__half*>(chunk + GeoK::B_HI + tc::kmajor_off(row, k % kKC, kKC)) = lo;
+    *reinterpret_cast<__half*>(chunk + GeoK<false>::GB_HI + tc::kmajor_off(row, k % kKC, kKC)) = lo;
     cn += (double)cv * (double)cv;
     nb2 += (double)bv * (double)bv;
     s1 += fabs((double)bv);
@@ -1357,7 +1710,7 @@ __global__ void __launch_bounds__(256) encode_prep_k_kernel(const float* __restr
   const __half p15 = __float2half_rn(32768.f);
   const __half pad = __float2half_rn(real ? 0.f : 65504.f);
   const __half z = __float2half_rn(0.f);
-  uint8_t* ext = base + (size_t)(ks / kKC) * GeoK::B_CHUNK;
+  uint8_t* ext = base + (size_t)(ks / kKC) * GeoK<false>::GB_CHUNK;
   *reinterpret_cast<uint4*>(ext + tc::kmajor_off(row, 0, kExt)) =
       make_uint4(pack_h2(c_h, c_m), pack_h2(c_l, p15), pack_h2(p15, p15), pack_h2(pad, z));
   *reinterpret_cast<uint4*>(ext + tc::kmajor_off(row, 8, kExt)) = make_uint4(0u, 0u, 0u, 0u);
@@ -2106,7 +2459,7 @@ int launch_encode_tc(const float* d_x, int64_t n, int d, const float* d_cw, int 
 int launch_encode_tck(const float* d_x, int64_t n, int d, const float* d_cw, int m, int l, int ks, uint8_t* d_codes,
                       int stride, unsigned long long* flagged_out, cudaStream_t stream) {
   using namespace enc;
-  using G = GeoK;
+  using G = GeoK<false>;
   const DevInfo& di = dev_info();
   std::lock_guard<std::mutex> lock(g_encws_mu);
   EncWS& ws = enc_workspace(stream);
@@ -2184,12 +2537,38 @@ int launch_encode_tck(const float* d_x, int64_t n, int d, const float* d_cw, int
   ep.counters = counters;
   ep.flag_cap = cap;
   ep.ntiles = (int)((n + kRows - 1) / kRows);
-  ep.tstride = std::max(1, std::min(di.sms / m, ep.ntiles));
   ep.keymask = ~15u;
   ep.one = 1u;
   ep.tcmask = tcmask;
-  PQK_CUDA_TRY(cudaFuncSetAttribute(encode_tck_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM));
-  encode_tck_kernel<<<ep.tstride * m, kThreads, G::SMEM, stream>>>(map, ep);
+  // CTA pairs (cta_group::2: half the B bytes through each CTA's shared memory) unless
+  // PQK_ENCODE_TCK_PAIR=0 or the input is a single tile
+  static const bool pair_off = [] {
+    const char* e = getenv("PQK_ENCODE_TCK_PAIR");
+    return e && e[0] == '0';
+  }();
+  if (!pair_off && ep.ntiles >= 2 && di.sms >= 2 * m) {
+    using GP = GeoK<true>;
+    ep.tstride = std::max(1, std::min(di.sms / 2 / m, (ep.ntiles + 1) / 2));  // tile pairs per subspace
+    PQK_CUDA_TRY(cudaFuncSetAttribute(encode_tck_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, GP::SMEM));
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)(2 * ep.tstride * m), 1u, 1u);
+    cfg.blockDim = dim3((unsigned)kThreads, 1u, 1u);
+    cfg.dynamicSmemBytes = GP::SMEM;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    PQK_CUDA_TRY(cudaLaunchKernelEx(&cfg, encode_tck_kernel<true>, map, ep));
+  } else {
+    ep.tstride = std::max(1, std::min(di.sms / m, ep.ntiles));
+    PQK_CUDA_TRY(
+        cudaFuncSetAttribute(encode_tck_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM));
+    encode_tck_kernel<false><<<ep.tstride * m, kThreads, G::SMEM, stream>>>(map, ep);
+  }
   PQK_LAUNCH_CHECK("encode_tck_kernel");
   const dim3 egrid((unsigned)(2 * di.sms), 1u);  // flattened (subspace, tile) schedule
   // fp32 filter over the candidates the tensor-core pass left for each uncertified pair, then
@@ -2254,7 +2633,7 @@ int encode_tc_try(const float* d_x, int64_t n, int d, const float* d_cw, int m, 
       break;
     default:
       // long subspaces: K-streamed kernel (codebook chunks through shared memory)
-      if (ks % enc::kKC != 0 || ks < 96 || ks > 1024 || (size_t)enc::GeoK::SMEM > (size_t)di.smem_optin) return PQK_OK;
+      if (ks % enc::kKC != 0 || ks < 96 || ks > 1024 || (size_t)enc::GeoK<false>::SMEM > (size_t)di.smem_optin) return PQK_OK;
       rc = launch_encode_tck(d_x, n, d, d_cw, m, l, ks, d_codes, stride, flagged_out, stream);
   }
   if (rc == PQK_OK) *used = true;

@@ -189,3 +189,27 @@ def test_tck_candidate_masks_small_codebooks_ties_and_non_finite(oracle, l_count
     x[702, 5] = -np.inf
     x[703] = np.nan
     np.testing.assert_array_equal(_encode(cw, x), oracle.encode(cw, x))
+
+
+def test_tck_single_cta_variant_and_many_items(tmp_path, oracle):
+    """K-streamed path with many items per CTA (accumulator, ring and hand-over reuse; odd
+    tile count, so the last CTA pair holds one real tile; nk = 5 chunks, so the transform
+    groups swap chunk parity every item): the default CTA-pair kernel (cta_group::2) and,
+    in a subprocess with PQK_ENCODE_TCK_PAIR=0, the single-CTA kernel must both equal the oracle."""
+    import os
+    import subprocess
+    import sys
+
+    rng = np.random.default_rng(77)
+    n, m, dsub = 128 * 332 + 57, 2, 160
+    cw = rng.normal(size=(m, 256, dsub)).astype(np.float32)
+    x = rng.normal(size=(n, m * dsub)).astype(np.float32)
+    x[::7] = np.rint(x[::7] * 4)  # rows whose fp16 split has no lo part
+    want = oracle.encode(cw, x)
+    np.testing.assert_array_equal(_encode(cw, x), want)
+    np.savez(tmp_path / "in.npz", cw=cw, x=x)
+    env = dict(os.environ, PQK_ENCODE_TCK_PAIR="0")
+    root = str(__import__("pathlib").Path(__file__).resolve().parents[1])
+    subprocess.run([sys.executable, "-c", _SIMT_SCRIPT, root, str(tmp_path / "in.npz"), str(tmp_path / "out.npy")],
+                   check=True, env=env)
+    np.testing.assert_array_equal(np.load(tmp_path / "out.npy"), want)

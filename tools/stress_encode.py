@@ -2,7 +2,9 @@
 oracle: distributions chosen to stress the certificate (near-ties from duplicated and
 perturbed codewords, integer data, heavy tails, sparse rows, tiny and huge scales).
 
-usage: python tools/stress_encode.py [seconds]"""
+usage: python tools/stress_encode.py [seconds]   (PQK_STRESS_TCK=1: only subspace widths
+of the K-streamed tensor-core kernel, up to 12,000 rows)"""
+import os
 import sys
 import time
 
@@ -17,10 +19,13 @@ rng = np.random.default_rng(int(time.time()))
 t0 = time.time()
 cases = pairs = 0
 while time.time() - t0 < budget:
-    sub = int(rng.choice([8, 16, 32, 64, 96, 128, 256, 512, 24]))
+    tck_only = os.environ.get("PQK_STRESS_TCK") == "1"
+    sub = int(rng.choice([96, 128, 160, 224, 256, 512, 1024] if tck_only else [8, 16, 32, 64, 96, 128, 256, 512, 24]))
     m = int(rng.choice([1, 2, 4, 8]))
     l_count = int(rng.choice([2, 17, 100, 256, 256, 256]))
-    n = int(rng.integers(1, 6000 if sub * m <= 512 else 1500))
+    # (the oracle's float64 pass bounds the case size: ~1e7 vector elements take ~20 s)
+    n = int(rng.integers(1, max(300, min(12000, 10_000_000 // (sub * m))) if tck_only
+                         else (6000 if sub * m <= 512 else 1500)))
     scale = float(10.0 ** rng.uniform(-6, 6))
     kind = rng.choice(["normal", "int", "heavy", "sparse", "near_tie"])
     d = sub * m
@@ -37,6 +42,8 @@ while time.time() - t0 < budget:
     if kind == "near_tie":  # codewords nearly equidistant from many vectors
         cw[:, 1::2] = cw[:, 0::2][:, : cw[:, 1::2].shape[1]] * np.float32(1 + 1e-6)
     cw += (rng.normal(size=cw.shape) * scale * 1e-3).astype(np.float32)
+    if tck_only:
+        print(dict(sub=sub, m=m, l=l_count, n=n, kind=str(kind)), flush=True)
     got = pqk.encode(pqk.PQCodebook(cw), x)
     ref = O.encode(cw, x)
     cases += 1

@@ -2057,7 +2057,12 @@ __global__ void __launch_bounds__(256) encode_filter32_k_kernel(
 // g = (ks + 2) 2^-24 (x 1.01), eta = ks 2^-120 (encode_filter32_k_kernel's bound, which this
 // kernel replaces on the product path); the certificate and the reduced candidate mask
 // handed to encode_exact_cand_kernel are the same as there.
-__global__ void __launch_bounds__(256) encode_filter32_cand_kernel(
+#ifndef FILTER_OCC
+#define FILTER_OCC 2
+#endif
+// (one dependent chain flag -> row -> x -> candidate rows per pair and warp; measured at
+// config 3: 2 resident CTAs per SM 134 us, 3 or 4 (80 / 64 registers) 153 us)
+__global__ void __launch_bounds__(256, FILTER_OCC) encode_filter32_cand_kernel(
     const float* __restrict__ x, int d, const float* __restrict__ cw, int m, int l, int ks,
     const uint32_t* __restrict__ flags, const unsigned int* __restrict__ counters, uint32_t flag_cap,
     const uint32_t* __restrict__ tcmask, uint8_t* __restrict__ codes, int stride, uint32_t* __restrict__ flags2,

@@ -1076,10 +1076,10 @@ constexpr int kTrPasses = kRows / (8 * kTrGroupWarps);      // 8-row passes per 
 static_assert(kTrGroups == 1 || kTrGroups == 2, "transform groups");
 // the CTA pair variant's ring depths (half the B bytes per CTA leave room for deeper rings)
 #ifndef ENC_KPXST
-#define ENC_KPXST 3
+#define ENC_KPXST 4
 #endif
 #ifndef ENC_KPBST
-#define ENC_KPBST 3
+#define ENC_KPBST 5
 #endif
 #ifndef ENC_KPAST
 #define ENC_KPAST 2
@@ -1216,31 +1216,48 @@ __global__ void __launch_bounds__(kThreads, 1) encode_tck_kernel(const __grid_co
 
   if (warp == 0) {
     // ---------------- producer: X chunks (TMA) and B chunks (bulk copies) ----------------
+    // One lane polls both rings, so that the X tiles run ahead by the whole X ring (through
+    // an item's epilogue) whatever the state of the B ring.
     if (lane == 0) {
-      for (int g = 0; g < nchunks; ++g) {
-        const int w = g / nk, c = g - w * nk;
-        const int t = kPair ? 2 * (t0 + w * p.tstride) + cr : t0 + w * p.tstride;
-        const int xs = g % G::XST, bs = g % G::BST;
-        mbar_wait(&xempty[xs], (uint32_t)(((g / G::XST) & 1) ^ 1));
-        if ((ENC_KEXP & 16) && g >= G::XST) {
-          mbar_arrive(&xfull[xs]);
-        } else {
-          mbar_arrive_expect_tx(&xfull[xs], (uint32_t)G::X_STAGE);
-          tma_load_2d(sX + xs * G::X_STAGE, &tmap, m * ks + c * kKC, t * kRows, &xfull[xs]);
-        }
-        mbar_wait(&bempty[bs], (uint32_t)(((g / G::BST) & 1) ^ 1));
-        if ((ENC_KEXP & 1) && g >= G::BST) {
-          mbar_arrive(&bfull[bs]);
-        } else {
-          mbar_arrive_expect_tx(&bfull[bs], (uint32_t)G::B_CHUNK);
-          if (kPair) {  // this CTA's 128 codewords of the hi and of the lo block
-            const uint8_t* src = bprep + (size_t)c * G::GB_CHUNK + (size_t)cr * G::B_HI;
-            bulk_g2s(sB + bs * G::B_CHUNK, src, G::B_HI, &bfull[bs]);
-            bulk_g2s(sB + bs * G::B_CHUNK + G::B_HI, src + G::GB_HI, G::B_HI, &bfull[bs]);
-          } else {
-            bulk_g2s(sB + bs * G::B_CHUNK, bprep + (size_t)c * G::GB_CHUNK, G::B_CHUNK, &bfull[bs]);
+      int gx = 0, gb = 0;
+      while (gx < nchunks || gb < nchunks) {
+        bool did = false;
+        if (gx < nchunks) {
+          const int xs = gx % G::XST;
+          if (mbar_test(&xempty[xs], (uint32_t)(((gx / G::XST) & 1) ^ 1))) {
+            const int w = gx / nk, c = gx - w * nk;
+            const int t = kPair ? 2 * (t0 + w * p.tstride) + cr : t0 + w * p.tstride;
+            if ((ENC_KEXP & 16) && gx >= G::XST) {
+              mbar_arrive(&xfull[xs]);
+            } else {
+              mbar_arrive_expect_tx(&xfull[xs], (uint32_t)G::X_STAGE);
+              tma_load_2d(sX + xs * G::X_STAGE, &tmap, m * ks + c * kKC, t * kRows, &xfull[xs]);
+            }
+            ++gx;
+            did = true;
           }
         }
+        if (gb < nchunks) {
+          const int bs = gb % G::BST;
+          if (mbar_test(&bempty[bs], (uint32_t)(((gb / G::BST) & 1) ^ 1))) {
+            const int c = gb % nk;
+            if ((ENC_KEXP & 1) && gb >= G::BST) {
+              mbar_arrive(&bfull[bs]);
+            } else {
+              mbar_arrive_expect_tx(&bfull[bs], (uint32_t)G::B_CHUNK);
+              if (kPair) {  // this CTA's 128 codewords of the hi and of the lo block
+                const uint8_t* src = bprep + (size_t)c * G::GB_CHUNK + (size_t)cr * G::B_HI;
+                bulk_g2s(sB + bs * G::B_CHUNK, src, G::B_HI, &bfull[bs]);
+                bulk_g2s(sB + bs * G::B_CHUNK + G::B_HI, src + G::GB_HI, G::B_HI, &bfull[bs]);
+              } else {
+                bulk_g2s(sB + bs * G::B_CHUNK, bprep + (size_t)c * G::GB_CHUNK, G::B_CHUNK, &bfull[bs]);
+              }
+            }
+            ++gb;
+            did = true;
+          }
+        }
+        if (!did) __nanosleep(32);
       }
     }
   } else if (warp == 1) {

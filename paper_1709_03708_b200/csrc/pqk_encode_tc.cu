@@ -2074,6 +2074,12 @@ __global__ void __launch_bounds__(256) encode_filter32_k_kernel(
 // g = (ks + 2) 2^-24 (x 1.01), eta = ks 2^-120 (encode_filter32_k_kernel's bound, which this
 // kernel replaces on the product path); the certificate and the reduced candidate mask
 // handed to encode_exact_cand_kernel are the same as there.
+#ifndef FILTER_GRID
+#define FILTER_GRID 2  // CTAs per SM of the candidate filter's grid-stride launch: one resident wave (config 3: 126 us; 8 per SM: 134 us)
+#endif
+#ifndef EXACT_GRID
+#define EXACT_GRID 8
+#endif
 #ifndef FILTER_OCC
 #define FILTER_OCC 2
 #endif
@@ -2607,13 +2613,13 @@ int launch_encode_tck(const float* d_x, int64_t n, int d, const float* d_cw, int
                                                             stride, flags2, counters2, cmask);
     PQK_LAUNCH_CHECK("encode_filter32_k_kernel");
   } else {
-    encode_filter32_cand_kernel<<<di.sms * 8, 256, 0, stream>>>(d_x, d, d_cw, m, l, ks, flags, counters, cap, tcmask,
+    encode_filter32_cand_kernel<<<di.sms * FILTER_GRID, 256, 0, stream>>>(d_x, d, d_cw, m, l, ks, flags, counters, cap, tcmask,
                                                                  d_codes, stride, flags2, counters2, cmask);
     PQK_LAUNCH_CHECK("encode_filter32_cand_kernel");
   }
   // float64 over the candidates of each remaining pair; every row (all 256 codewords) only
   // when the pair list overflowed
-  encode_exact_cand_kernel<<<di.sms * 8, 256, 0, stream>>>(d_x, d, d_cw, m, l, ks, flags2, counters2, cap, cmask,
+  encode_exact_cand_kernel<<<di.sms * EXACT_GRID, 256, 0, stream>>>(d_x, d, d_cw, m, l, ks, flags2, counters2, cap, cmask,
                                                             d_codes, stride);
   PQK_LAUNCH_CHECK("encode_exact_cand_kernel");
   const int esmem = 2 * 256 * 33 * 4;
